@@ -1,0 +1,381 @@
+"""ImaSk hot-path benchmark on B200 (config D: 1024^2, 1440 angles, 1449 bins, r = 6).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+
+A step is one parallel ImaSk iteration (sketch_step, solvers.py:194-221) at the
+level drawn by the reference's counter-based RNG for that iteration: the
+adjoint of level i on y^k, the forward of level i on x^k fused with the
+sinogram-side SAGA update, and the image-side update. With N > 1 (torchrun)
+angles are sharded and the partial backprojection is all-reduced over NCCL.
+
+value   = iterations/s of the whole job (device time, CUDA events per step on
+          the launching stream, L2 flushed between steps, max over ranks).
+e2e     = iterations/s through the public API solvers.run(..., record_every=1,
+          x_ref=...) from host data: b copied from pinned host memory inside the
+          timed region, per-iteration metric read-back (the reference run()'s
+          rel_dist / psnr row), final x copied back.
+roofline = the dominant kernel (the level-1 backprojection) against measured
+          HBM bandwidth on its algorithmic bytes, plus its FP32-issue fraction.
+cpu_baseline / --impl reference = the reference algorithm (scipy CSR float64,
+          oracle/ restatement) on a sampled-angle slice of config D, scaled to
+          the full angle count (the full CSR needs ~130 GB).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CONFIG_KEY = "D"
+SEED = 2024
+SIGMA = 1e-6  # explicit step (theory sigma* ~ 1e-7 at raw ||K||; any positive value times the same)
+CPU_SAMPLE_ANGLES = 8
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["native", "reference"], default="native")
+    ap.add_argument("--config", default=CONFIG_KEY)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- reference arm
+
+def cpu_reference(cfg, steps: int, warmup: int, sample: int = CPU_SAMPLE_ANGLES):
+    """Reference algorithm (scipy CSR, float64) on `sample` evenly spaced angles of cfg.
+
+    Per-level times of the sampled projector applies and sinogram-side updates
+    are scaled by n_angles/sample; the image-side update (full d) is timed as is.
+    Returns (iters/s, details).
+    """
+    from oracle import sketch_oracle as sk
+    from oracle import solver_oracle as so
+
+    r = cfg.levels
+    probs = [1.0 / r] * r
+    sel = np.linspace(0, cfg.n_angles, sample, endpoint=False).astype(np.int64)
+    t_build = time.perf_counter()
+    ops = so.SketchedCT(cfg.side, cfg.n_angles, cfg.n_det, probs, angle_idx=sel)
+    t_build = time.perf_counter() - t_build
+    scale = cfg.n_angles / sample
+    rng = np.random.default_rng(0)
+    x = rng.random(cfg.d)
+    y = rng.standard_normal(ops.m)
+    b = rng.standard_normal(ops.m)
+    tab = rng.standard_normal(ops.m)
+    st = so.init_state(ops, seed=SEED)
+    per_level = []
+    for i in range(r):
+        f = ops.factors[i]
+        proj = ops.proj[f]
+        xl = sk.decimate(x.reshape(cfg.side, cfg.side), f).ravel()
+        reps = 3 if f <= 2 else 5
+        # pure CSR matvecs of the sampled rows (scale with the angle count)
+        t = time.perf_counter()
+        for _ in range(reps):
+            proj.adjoint_apply(y)
+            proj.apply(xl)
+        t_proj = (time.perf_counter() - t) / reps
+        # sinogram-side elementwise of sketch_step on the sampled rows (scales)
+        t = time.perf_counter()
+        for _ in range(reps):
+            zeta = (tab - st.psi[i]) + st.psi_sum
+            _ = st.psi_sum + probs[i] * (tab - st.psi[i])
+            _ = ((st.y + SIGMA * zeta) - SIGMA * b) / (1.0 + SIGMA)
+        t_sino = (time.perf_counter() - t) / reps
+        # the whole reference step on the sample: includes restriction / compensation /
+        # prolongation and the image-side update at full size, which do not scale
+        t = time.perf_counter()
+        for _ in range(2):
+            st.k = 0
+            phi_new = ops.adjoint_apply(i, st.y)
+            psi_new = ops.apply(i, st.x)
+            xi = (phi_new - st.phi[i]) + st.phi_sum
+            zeta = (psi_new - st.psi[i]) + st.psi_sum
+            st.phi_sum = st.phi_sum + probs[i] * (phi_new - st.phi[i])
+            st.psi_sum = st.psi_sum + probs[i] * (psi_new - st.psi[i])
+            st.phi[i] = phi_new
+            st.psi[i] = psi_new
+            st.x = (st.x - 1.0 * xi) / (1.0 + 1e-2)
+            st.y = ((st.y + SIGMA * zeta) - SIGMA * b) / (1.0 + SIGMA)
+        t_step = (time.perf_counter() - t) / 2
+        t_img = max(t_step - t_proj - t_sino, 0.0)
+        per_level.append(scale * (t_proj + t_sino) + t_img)
+    sched = so.level_schedule(SEED, warmup, steps, probs)
+    t_iter = float(np.mean([per_level[int(i)] for i in sched]))
+    detail = {
+        "sample": f"{sample} of {cfg.n_angles} angles (every {cfg.n_angles // sample}th), all "
+                  f"{r} levels; CSR matvec + sinogram-side time x{scale:g}, image-side work (restriction, "
+                  f"compensation, prolongation, primal update; full size) as measured; "
+                  f"mean over the timed steps' level schedule",
+        "per_level_s": [round(v, 6) for v in per_level],
+        "csr_build_s_excluded": round(t_build, 3),
+    }
+    return 1.0 / t_iter, detail
+
+
+# ---------------------------------------------------------------- native arm
+
+def clocks_sampler(path):
+    try:
+        return subprocess.Popen(
+            ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+             "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+            stdout=open(path, "w"), stderr=subprocess.DEVNULL,
+        )
+    except Exception:
+        return None
+
+
+def summarize_clocks(path, dev_index):
+    sm, smax, reasons = [], None, set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    try:
+        for line in open(path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9 or parts[0] != str(dev_index):
+                continue
+            sm.append(float(parts[1]))
+            smax = float(parts[2])
+            for name, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+    except Exception:
+        pass
+    return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+            "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def main():
+    args = parse()
+    from paper_2412_10249_b200.synth import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n_gpus = world if world > 1 else args.gpus
+
+    base = {
+        "metric": "imask_iters_per_sec",
+        "unit": "iter/s",
+        "n_gpus": n_gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (seeded 10-ellipse phantom, b = Kx + 1% gaussian noise)",
+    }
+    workload = {"workload": f"ImaSk sketch_step, config {cfg.name}: {cfg.side}^2 image, "
+                            f"{cfg.n_angles} angles x {cfg.n_det} bins, r={cfg.levels} levels "
+                            f"(factors 1..{2 ** (cfg.levels - 1)}), uniform level probabilities",
+                "side": cfg.side, "n_angles": cfg.n_angles, "n_det": cfg.n_det,
+                "levels": cfg.levels, "seed": SEED, "sigma": SIGMA, "mu_g": cfg.mu_g,
+                "parallelism": f"angle-sharded x{n_gpus}" if n_gpus > 1 else "single GPU"}
+
+    if args.impl == "reference":
+        if world > 1 and rank != 0:
+            return
+        t0 = time.perf_counter()
+        ips, det = cpu_reference(cfg, args.steps, args.warmup)
+        cores = 1
+        line = dict(base, impl="reference", value=ips, ms_per_step=1e3 / ips,
+                    config=dict(workload, l2="n/a (CPU)"),
+                    cpu_baseline={"value": ips, "unit": "iter/s", "cores": cores, "kind": "port",
+                                  "sample": det["sample"]},
+                    e2e={"value": ips, "unit": "iter/s", "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0},
+                    reference_detail=dict(det, wall_s=round(time.perf_counter() - t0, 2)))
+        print(json.dumps(line))
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=device)
+        group = dist.group.WORLD
+
+    from paper_2412_10249_b200 import ctmodel, mrsketch, solvers
+    from paper_2412_10249_b200 import dist as dist_mod
+    from paper_2412_10249_b200.synth import ellipse_phantom
+
+    r = cfg.levels
+    probs = [1.0 / r] * r
+    geom = ctmodel.Geometry(cfg.side, cfg.n_angles, cfg.n_det)
+    begin, end = ctmodel.slab_bounds(cfg.n_angles, rank, world)
+    x_true = ellipse_phantom(cfg.side, 0)
+    # data: b = K x_true + 1% noise, built with the device projector (the CSR oracle needs
+    # ~130 GB at this size); the same seeded arrays on every rank
+    full_plan = ctmodel.get_plan(geom)
+    sino = full_plan.project(torch.from_numpy(x_true.astype(np.float32).ravel()).to(device), 1)
+    sino_h = sino.double().cpu().numpy()
+    noise = np.random.default_rng(1).standard_normal(sino_h.size)
+    b_full = sino_h + cfg.kappa * np.abs(sino_h).max() * noise
+    b_loc = b_full.reshape(cfg.n_angles, cfg.n_det)[begin:end].ravel()
+
+    fam = mrsketch.make_family(r, cfg.side, probs, mode="coarse")
+    prob = dist_mod.make_sharded_problem(geom, b_loc, fam, cfg.mu_g, rank, world, group)
+    eng = prob.engine
+    st = solvers.init_state(prob, seed=SEED)
+    prm = solvers._params(SIGMA, cfg.mu_g, cfg.mu_g)
+    sched = solvers.draw_levels(SEED, 0, args.warmup + args.steps, prob.cum_probs)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # warm-up
+    for k in range(args.warmup):
+        solvers._device_step(eng, st, int(sched[k]), prm)
+    torch.cuda.synchronize()
+
+    # timed: per-step events on the launching stream, L2 flushed between steps
+    stream = torch.cuda.current_stream(device)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clk_path = os.path.join(REPO, f".clocks_rank{rank}.csv")
+    sampler = clocks_sampler(clk_path) if rank == 0 else None
+    time.sleep(0.3)
+    launches = 0
+    barrier()
+    torch.cuda.synchronize()
+    for s in range(args.steps):
+        flush.zero_()
+        starts[s].record(stream)
+        launches += solvers._device_step(eng, st, int(sched[args.warmup + s]), prm)
+        ends[s].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    if sampler:
+        sampler.terminate()
+        sampler.wait()
+    step_ms = np.array([a.elapsed_time(b) for a, b in zip(starts, ends)])
+    total_ms = float(step_ms.sum())
+    if world > 1:
+        t = torch.tensor([total_ms], device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ips = args.steps / (total_ms / 1e3)
+    level_counts = np.bincount(sched[args.warmup:], minlength=r).tolist()
+    lev = np.asarray(sched[args.warmup:])
+    per_level_ms = {f"f{2 ** (r - 1 - i)}": round(float(step_ms[lev == i].mean()), 4)
+                    for i in range(r) if np.any(lev == i)}
+
+    # dominant kernel: level-1 (f = 1) backprojection, timed alone with events
+    plan = eng.plan
+    ybuf = st.y.clone()
+    out = torch.empty(cfg.d, device=device)
+    reps = 20
+    for _ in range(3):
+        plan.backproject(ybuf, 1, out)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
+    for q in range(reps):
+        flush.zero_()
+        ev[2 * q].record(stream)
+        plan.backproject(ybuf, 1, out)
+        ev[2 * q + 1].record(stream)
+    torch.cuda.synchronize()
+    adj_ms = float(np.mean([ev[2 * q].elapsed_time(ev[2 * q + 1]) for q in range(reps)]))
+    for q in range(reps):
+        flush.zero_()
+        ev[2 * q].record(stream)
+        plan.project(st.x, 1, ybuf)
+        ev[2 * q + 1].record(stream)
+    torch.cuda.synchronize()
+    fwd_ms = float(np.mean([ev[2 * q].elapsed_time(ev[2 * q + 1]) for q in range(reps)]))
+    m_loc = (end - begin) * cfg.n_det
+    alg_bytes = 4.0 * (cfg.d + m_loc)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json)" if "hbm_gbs" in peaks else "fallback 6650 GB/s"
+    achieved = alg_bytes / (adj_ms * 1e-3) / 1e9
+    # FP32-issue view: footprint evaluations (nnz of the reference CSR) per second
+    nnz = 4.0 / np.pi * (end - begin) * cfg.d
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(REPO, "profiles", "traffic.json"))).get("adjoint_f1")
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": "k_adjoint<2> (level-1 backprojection)",
+                "achieved": round(achieved, 2), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 5), "traffic": traffic,
+                "algorithmic_bytes": alg_bytes, "avg_launch_ms": round(adj_ms, 4),
+                "peak_source": peak_src,
+                "note": "projector is FP32-issue bound, not HBM bound (SURVEY 0.7); "
+                        "see fp32_view",
+                "fp32_view": {"footprint_evals_per_s": round(nnz / (adj_ms * 1e-3), 1),
+                              "forward_f1_ms": round(fwd_ms, 4), "adjoint_f1_ms": round(adj_ms, 4)}}
+
+    # e2e through the public API: solvers.run with host inputs
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e_steps = min(args.steps, 100)
+        b_host = torch.from_numpy(b_loc.astype(np.float32)).pin_memory()
+        xref_host = torch.from_numpy(x_true.astype(np.float32).ravel()).pin_memory()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        b_dev = b_host.to(device, non_blocking=True)
+        xref_dev = xref_host.to(device, non_blocking=True)
+        prob2 = dist_mod.make_sharded_problem(geom, b_dev, fam, cfg.mu_g)
+        rep = solvers.run(prob2, "sketch", SIGMA, cfg.mu_g, e2e_steps, record_every=1,
+                          seed=SEED, x_ref=xref_dev)
+        x_out = rep.x.cpu()
+        dt = time.perf_counter() - t0
+        e2e = {"value": e2e_steps / dt, "unit": "iter/s",
+               "h2d_bytes_per_step": round((b_host.numel() + xref_host.numel()) * 4 / e2e_steps),
+               "d2h_bytes_per_step": round(16 + x_out.numel() * 4 / e2e_steps),
+               "api": "solvers.run(prob, 'sketch', ..., record_every=1, x_ref=...)",
+               "steps": e2e_steps}
+
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0:
+        cps, det = cpu_reference(cfg, args.steps, args.warmup)
+        cpu = {"value": cps, "unit": "iter/s", "cores": 1, "kind": "port",
+               "sample": det["sample"], "per_level_s": det["per_level_s"]}
+
+    clocks = summarize_clocks(clk_path, local) if rank == 0 else None
+    if rank == 0:
+        line = dict(base, value=ips, ms_per_step=total_ms / args.steps,
+                    config=dict(workload, l2="flushed between steps (256 MiB write outside the "
+                                             "per-step CUDA events)"),
+                    e2e=e2e, roofline=roofline, cpu_baseline=cpu, clocks=clocks,
+                    gpu_launches=launches, per_level_ms=per_level_ms, level_counts=level_counts)
+        print(json.dumps(line))
+        try:
+            os.remove(clk_path)
+        except OSError:
+            pass
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,177 @@
+/*
+ * imask_b200.h -- C-ABI of the B200-native ImaSk hot path (arXiv 2412.10249).
+ *
+ * Drop-in boundary for the reference package `mrtomo` (pure Python/scipy,
+ * /root/reference/pkg/src/mrtomo). Each entry point names the reference
+ * interface it replaces (file:line relative to pkg/src/mrtomo). All device
+ * buffers are caller-owned CUDA allocations passed as plain pointers; all
+ * calls are stream-ordered and asynchronous (no host sync) unless noted;
+ * `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *
+ * Layouts (float32 everywhere):
+ *   image   side x side, row-major, y increasing with row   (ctmodel.py:76-79)
+ *   coarse  (side/f) x (side/f), same convention, pixel width f (ctmodel.py:194-204)
+ *   sino    n_loc x n_det, angle-major, detector fastest     (ctmodel.py:176)
+ *           n_loc = angle_end - angle_begin (this rank's angle slab)
+ *
+ * Return codes: IMASK_OK, or one of the IMASK_E* codes below with a message
+ * retrievable through imask_last_error() (thread-local). The Python host maps
+ * IMASK_EDIM to linops.DimensionMismatch and IMASK_EINVAL / IMASK_ELEVEL to
+ * ValueError with the reference's messages (linops.py:19-55, mrsketch.py:120-122).
+ */
+#ifndef IMASK_B200_H
+#define IMASK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IMASK_API __attribute__((visibility("default")))
+
+#define IMASK_OK 0
+#define IMASK_EINVAL 1 /* invalid argument / configuration      -> ValueError        */
+#define IMASK_EDIM 2   /* vector length does not match geometry  -> DimensionMismatch */
+#define IMASK_ELEVEL 3 /* sketch level out of range 1..r         -> ValueError        */
+#define IMASK_ECUDA 4  /* CUDA runtime error                     -> RuntimeError      */
+#define IMASK_MAX_LEVELS 12
+
+typedef struct imask_plan imask_plan; /* opaque; owns per-angle tables + scratch */
+
+/* Solver state of one rank: every pointer is a device buffer.
+ * Mirrors SaddleState (solvers.py:119-140) with compact coarse phi rows:
+ *   x, phi_sum           : side*side
+ *   phi_tab              : sum_i (side/f_i)^2, level i (1-based) at offset
+ *                          sum_{i'<i} (side/f_i')^2 (rows hold U_f^T-scaled
+ *                          coarse values; the reference stores the same
+ *                          values replicated to full resolution)
+ *   y, b, psi_sum        : n_loc*n_det (this rank's slab)
+ *   psi_tab              : r * n_loc*n_det, level i at offset (i-1)*n_loc*n_det
+ *   bp                   : side*side scratch for the (partial) backprojection */
+typedef struct imask_state {
+  float* x;
+  float* y;
+  const float* b;
+  float* phi_sum;
+  float* psi_sum;
+  float* phi_tab;
+  float* psi_tab;
+  float* bp;
+} imask_state;
+
+/* Per-iteration scalars of sketch_step (solvers.py:194-221) with the ridge
+ * prox (proxlib.py:51-63) and the quadratic-data conjugate prox
+ * (proxlib.py:30-48). */
+typedef struct imask_step_params {
+  double sigma; /* dual step sigma; primal step is sigma/mu */
+  double mu;    /* solver strong-convexity parameter mu      */
+  double mu_g;  /* ridge weight of g(x) = mu_g/2 ||x||^2      */
+} imask_step_params;
+
+/* Library version string. */
+IMASK_API const char* imask_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+IMASK_API const char* imask_last_error(void);
+
+/* ---- plan ------------------------------------------------------------- */
+
+/* Geometry + sketch family of one rank. Replaces Geometry (ctmodel.py:38-70),
+ * the per-geometry projector cache _projector_pair (ctmodel.py:157-167) and
+ * the SketchFamily probabilities/factors (mrsketch.py:76-118).
+ *   side, n_angles, n_det : Geometry(side, n_angles, n_detectors)
+ *   angle_begin/end       : this rank's contiguous angle slab [begin, end)
+ *   cos_tab, sin_tab      : float64 cos/sin of the slab's angles a*pi/n_angles,
+ *                           ALREADY snapped to 0 below 1e-14 (ctmodel.py:88-93);
+ *                           a ray family is axis-parallel iff one is exactly 0
+ *   r, probs              : levels and selection probabilities (level i has
+ *                           factor 2^(r-i), mrsketch.py:107-109)
+ *   scale                 : operator scale (1/||K|| when normalised,
+ *                           expcli.py:173-180; 1.0 otherwise)
+ *   device                : CUDA device ordinal the plan lives on            */
+IMASK_API int imask_plan_create(int side, int n_angles, int n_det, int angle_begin,
+                                int angle_end, const double* cos_tab, const double* sin_tab,
+                                int r, const double* probs, double scale, int device,
+                                imask_plan** out);
+IMASK_API int imask_plan_destroy(imask_plan* plan);
+/* Scratch bytes the plan owns on the device (for memory accounting). */
+IMASK_API int64_t imask_plan_scratch_bytes(const imask_plan* plan);
+
+/* ---- projector (kernels 1 and 2) ------------------------------------ */
+
+/* sino = R_f u : exact-chord forward projection of a coarse image.
+ * Replaces coarse_projector(geom, f).apply (ctmodel.py:194-204) and, for
+ * f = 1, projector_op(geom).apply / project (ctmodel.py:170-191). */
+IMASK_API int imask_project(imask_plan* plan, int factor, const float* u, int64_t u_len,
+                            float* sino, int64_t sino_len, void* stream);
+/* u = R_f^T sino : matched pixel-driven backprojection, no atomics.
+ * Replaces coarse_projector(geom, f).adjoint_apply and backproject
+ * (ctmodel.py:179-185,194-204). */
+IMASK_API int imask_backproject(imask_plan* plan, int factor, const float* sino,
+                                int64_t sino_len, float* u, int64_t u_len, void* stream);
+
+/* ---- sketch family (kernel 3) ----------------------------------------- */
+
+/* u = T_f x (block mean).  Replaces decimate (mrsketch.py:23-32) and
+ * decimate_op(side, f).apply (mrsketch.py:44-57). */
+IMASK_API int imask_restrict(int side, int factor, const float* x, float* u, void* stream);
+/* x = alpha * U_f u (replication).  alpha = 1: upsample (mrsketch.py:35-41);
+ * alpha = 1/f^2: decimate_op adjoint (mrsketch.py:54-55). */
+IMASK_API int imask_prolong(int side, int factor, const float* u, float* x, float alpha,
+                            void* stream);
+/* out = S_r x, the full-resolution compensation (mrsketch.py:133-153) of the
+ * family (r, probs). S_r is symmetric, so this is also its adjoint
+ * (mrsketch.py:155-160). Requires side % 2^(r-1) == 0, r <= 7. */
+IMASK_API int imask_compensate(int side, int r, const double* probs, const float* x, float* out,
+                               void* stream);
+/* sino = K_i x and out = K_i^T sino for the sketched operator of level i
+ * (1-based): coarse mode K_i = R_f T_f for i < r, K_r = K S_r
+ * (sketch_forward, mrsketch.py:181-204). x / out are full resolution. */
+IMASK_API int imask_sketch_forward(imask_plan* plan, int level, const float* x, float* sino,
+                                   void* stream);
+IMASK_API int imask_sketch_adjoint(imask_plan* plan, int level, const float* sino, float* out,
+                                   void* stream);
+
+/* ---- sketched SAGA iteration (kernel 4) -------------------------------- */
+
+/* Host-side level schedule, bit-exact with draw_level (solvers.py:30-48):
+ * out[n] = draw_level(seed, k0 + n, cum_probs) for n in [0, count).
+ * cum_probs = numpy.cumsum(probs) (solvers.py:81). Pure host function. */
+IMASK_API int imask_draw_levels(uint64_t seed, int64_t k0, int64_t count,
+                                const double* cum_probs, int r, int32_t* out);
+/* uniform_at(seed, k) (solvers.py:37-41). Pure host function. */
+IMASK_API double imask_uniform_at(uint64_t seed, int64_t k);
+
+/* One parallel ImaSk iteration at 0-based level index `level0` (the value
+ * draw_level returns) on one GPU: replaces sketch_step (solvers.py:194-221)
+ * minus the host bookkeeping (k, cost, resum cadence stay on the host).
+ * Equivalent to step_adjoint + step_forward + step_image below. */
+IMASK_API int imask_sketch_step(imask_plan* plan, const imask_state* st, int level0,
+                                const imask_step_params* prm, void* stream);
+/* The three phases of one iteration, for angle-sharded multi-GPU runs:
+ *  step_adjoint : st->bp = partial (this slab) coarse backprojection R_f^T y
+ *                 (or K^T y at the full level), reads y^k.
+ *  step_forward : psi_new = K_i x^k on this slab, fused with the sinogram-
+ *                 side SAGA update (psi table row, psi_sum, y prox). Must be
+ *                 enqueued after step_adjoint (it overwrites y).
+ *  step_image   : after st->bp has been all-reduced over ranks: phi_new,
+ *                 phi table row, phi_sum and the x prox (x^k -> x^{k+1}).
+ *                 Must be enqueued after step_forward's image read. */
+IMASK_API int imask_step_adjoint(imask_plan* plan, const imask_state* st, int level0,
+                                 void* stream);
+IMASK_API int imask_step_forward(imask_plan* plan, const imask_state* st, int level0,
+                                 const imask_step_params* prm, void* stream);
+IMASK_API int imask_step_image(imask_plan* plan, const imask_state* st, int level0,
+                               const imask_step_params* prm, void* stream);
+/* Recompute phi_sum / psi_sum from the tables in index order (_resum,
+ * solvers.py:184-191). */
+IMASK_API int imask_resum(imask_plan* plan, const imask_state* st, void* stream);
+
+/* Number of kernel launches the last imask_* device call on this thread
+ * enqueued (instrumentation for the benchmark's gpu_launches count). */
+IMASK_API int imask_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IMASK_B200_H */

@@ -1,0 +1,581 @@
+// C-ABI of the ImaSk B200 hot path (declared in include/imask_b200.h).
+//
+// The plan replaces the reference's per-geometry projector cache
+// (_projector_pair, ctmodel.py:157-167): instead of a CSR matrix it holds the
+// float64-derived per-angle parameter tables of every level factor (a few KB)
+// and the staging buffers of the forward projector. Everything else is
+// caller-owned device memory.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "imask_b200.h"
+#include "imask_common.cuh"
+#include "sketch.cuh"
+
+namespace imask {
+cudaError_t launch_forward(const float2* P, const float2* PT, int n, const FwdAngle* ang,
+                           int n_loc, int n_det, float* sino, const SinoSaga* saga,
+                           cudaStream_t stream);
+cudaError_t launch_adjoint(const float* sino, float* out, int n, int factor, int n_loc,
+                           int n_det, const AdjAngle* ang, cudaStream_t stream);
+cudaError_t launch_restrict(const float* x, float* u, int side, int f, cudaStream_t s);
+cudaError_t launch_prolong(const float* u, float* x, int side, int f, float alpha,
+                           cudaStream_t s);
+cudaError_t launch_compensate(const float* x, float* out, int side, const CompParams& cp,
+                              cudaStream_t s);
+cudaError_t launch_prepare(const float* u, int n, float2* P, float2* PT, cudaStream_t s);
+cudaError_t launch_saga_image_coarse(const float* bp, int side, int f, const ImageSaga& sg,
+                                     cudaStream_t s);
+cudaError_t launch_saga_image_full(const float* bp, int side, const CompParams& cp,
+                                   const ImageSaga& sg, cudaStream_t s);
+cudaError_t launch_saga_sino(const float* psi_new, size_t m, const SinoSaga& sg, cudaStream_t s);
+cudaError_t launch_resum(const float* phi_tab, float* phi_sum, int side, const float* psi_tab,
+                         float* psi_sum, size_t m, const ResumParams& rp, cudaStream_t s);
+}  // namespace imask
+
+using namespace imask;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct LevelTables {
+  FwdAngle* fwd = nullptr;  // device
+  AdjAngle* adj = nullptr;  // device
+};
+
+}  // namespace
+
+struct imask_plan {
+  int side, n_angles, n_det, a_begin, a_end, n_loc, r, device;
+  double scale;
+  std::vector<double> probs, cosv, sinv;
+  std::vector<int> factors;        // factor of level i (0-based)
+  std::vector<long long> phi_off;  // phi table offsets
+  std::map<int, LevelTables> tables;
+  std::mutex mu;
+  float2* P = nullptr;
+  float2* PT = nullptr;
+  float* u = nullptr;
+  float* sino_tmp = nullptr;
+  int64_t scratch = 0;
+  CompParams cp{};
+  ResumParams rp{};
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return fail(IMASK_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return IMASK_OK;
+}
+
+#define LAUNCH(expr, what)                                   \
+  do {                                                       \
+    ++g_launches;                                            \
+    int _rc = cuda_check((expr), what);                      \
+    if (_rc != IMASK_OK) return _rc;                         \
+  } while (0)
+
+// Float64 per-angle parameters of one level factor (see imask_common.cuh).
+void build_tables(const imask_plan& pl, int f, std::vector<FwdAngle>& fw,
+                  std::vector<AdjAngle>& ad) {
+  const double h = (double)f;
+  const double half = pl.side / 2.0;  // n*h/2 at every level
+  const double t0 = -(pl.n_det - 1) / 2.0;
+  fw.resize(pl.n_loc);
+  ad.resize(pl.n_loc);
+  for (int a = 0; a < pl.n_loc; ++a) {
+    const double c = pl.cosv[a], s = pl.sinv[a];
+    const double ac = std::fabs(c), as = std::fabs(s);
+    const bool axis = (c == 0.0 || s == 0.0);
+    FwdAngle F{};
+    double step, tau, wmax;
+    if (ac >= as) {  // bands are pixel rows: x where the ray meets the row centre line
+      F.transposed = 0;
+      F.xi_dj = 1.0 / (c * h);
+      F.xi_base = t0 / (c * h) + (half - h / 2) * s / (c * h) + half / h - 0.5;
+      step = -s / c;
+      tau = as / ac;
+      wmax = h / ac;
+    } else {  // bands are pixel columns (transposed image)
+      F.transposed = 1;
+      F.xi_dj = 1.0 / (s * h);
+      F.xi_base = t0 / (s * h) + (half - h / 2) * c / (s * h) + half / h - 0.5;
+      step = -c / s;
+      tau = ac / as;
+      wmax = h / as;
+    }
+    F.step = std::llrint(step * kFix);
+    if (axis) {
+      // g = [frac >= 1/2]: the ray on a gridline goes to the upper/right pixel
+      F.S = 16777216.0f;   // 2^24
+      F.B = -25165822.0f;  // 2 - 1.5*2^24
+    } else {
+      F.S = (float)(1.0 / tau);
+      F.B = (float)(-(3.0 - tau) / (2.0 * tau));
+    }
+    F.wsc = (float)(wmax * pl.scale);
+    fw[a] = F;
+
+    AdjAngle A{};
+    A.ch = c * h;
+    A.sh = s * h;
+    const double R = (ac + as) * h / 2.0;
+    A.eta0 = (-half + h / 2.0) * (c + s) + (pl.n_det - 1) / 2.0 - R;
+    A.Dc = std::llrint(A.ch * kFix);
+    A.Ds = std::llrint(A.sh * kFix);
+    A.R = (float)R;
+    A.wsc = (float)(wmax * pl.scale);
+    if (axis) {
+      A.axis = 1;
+      A.nb = f;
+      A.kneg = 0.f;
+      A.Rk = 0.f;
+    } else {
+      const double kk = 1.0 / (std::fmin(ac, as) * h);  // 1/(R - plateau half-width)
+      A.axis = 0;
+      A.nb = (int)std::floor(2.0 * R) + 1;
+      A.kneg = (float)(-kk);
+      A.Rk = (float)(R * kk);
+    }
+    ad[a] = A;
+  }
+}
+
+int get_tables(imask_plan* pl, int f, LevelTables** out) {
+  std::lock_guard<std::mutex> lk(pl->mu);
+  auto it = pl->tables.find(f);
+  if (it == pl->tables.end()) {
+    std::vector<FwdAngle> fw;
+    std::vector<AdjAngle> ad;
+    build_tables(*pl, f, fw, ad);
+    LevelTables t;
+    if (pl->n_loc > 0) {
+      int rc = cuda_check(cudaMalloc(&t.fwd, sizeof(FwdAngle) * pl->n_loc), "cudaMalloc");
+      if (rc) return rc;
+      rc = cuda_check(cudaMalloc(&t.adj, sizeof(AdjAngle) * pl->n_loc), "cudaMalloc");
+      if (rc) return rc;
+      rc = cuda_check(cudaMemcpy(t.fwd, fw.data(), sizeof(FwdAngle) * pl->n_loc,
+                                 cudaMemcpyHostToDevice),
+                      "cudaMemcpy");
+      if (rc) return rc;
+      rc = cuda_check(cudaMemcpy(t.adj, ad.data(), sizeof(AdjAngle) * pl->n_loc,
+                                 cudaMemcpyHostToDevice),
+                      "cudaMemcpy");
+      if (rc) return rc;
+    }
+    it = pl->tables.emplace(f, t).first;
+  }
+  *out = &it->second;
+  return IMASK_OK;
+}
+
+int check_factor(const imask_plan* pl, int f) {
+  if (f < 1 || pl->side % f != 0)
+    return fail(IMASK_EINVAL, "side " + std::to_string(pl->side) + " not divisible by factor " +
+                                  std::to_string(f));
+  return IMASK_OK;
+}
+
+int check_level0(const imask_plan* pl, int level0) {
+  if (level0 < 0 || level0 >= pl->r)
+    return fail(IMASK_ELEVEL, "level " + std::to_string(level0 + 1) + " out of range 1.." +
+                                  std::to_string(pl->r));
+  return IMASK_OK;
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+
+}  // namespace
+
+extern "C" {
+
+const char* imask_version(void) { return "imask_b200 0.1 (sm_100a)"; }
+const char* imask_last_error(void) { return g_err.c_str(); }
+int imask_last_launch_count(void) { return g_launches; }
+
+int imask_plan_create(int side, int n_angles, int n_det, int angle_begin, int angle_end,
+                      const double* cos_tab, const double* sin_tab, int r, const double* probs,
+                      double scale, int device, imask_plan** out) {
+  g_err.clear();
+  g_launches = 0;
+  if (!out) return fail(IMASK_EINVAL, "out must not be null");
+  *out = nullptr;
+  if (side < 1) return fail(IMASK_EINVAL, "side must be positive");
+  if (n_angles < 1 || n_det < 1) return fail(IMASK_EINVAL, "n_angles and n_det must be positive");
+  if (angle_begin < 0 || angle_end > n_angles || angle_begin > angle_end)
+    return fail(IMASK_EINVAL, "angle slab [" + std::to_string(angle_begin) + ", " +
+                                  std::to_string(angle_end) + ") outside 0.." +
+                                  std::to_string(n_angles));
+  if (r < 1 || r > 7) return fail(IMASK_EINVAL, "levels r must be in 1..7");
+  const int coarsest = 1 << (r - 1);
+  if (side % coarsest != 0)
+    return fail(IMASK_EINVAL, "side " + std::to_string(side) + " not divisible by 2^(r-1) = " +
+                                  std::to_string(coarsest));
+  double psum = 0.0;
+  for (int i = 0; i < r; ++i) {
+    if (!(probs[i] > 0.0)) return fail(IMASK_EINVAL, "all probabilities must be positive");
+    psum += probs[i];
+  }
+  if (std::fabs(psum - 1.0) > 1e-12)
+    return fail(IMASK_EINVAL, "probabilities sum to " + std::to_string(psum) + ", expected 1");
+  const int n_loc = angle_end - angle_begin;
+  if ((n_loc > 0) && (!cos_tab || !sin_tab)) return fail(IMASK_EINVAL, "angle tables missing");
+  for (int a = 0; a < n_loc; ++a)
+    if (cos_tab[a] == 0.0 && sin_tab[a] == 0.0)
+      return fail(IMASK_EINVAL, "angle with cos = sin = 0");
+
+  DeviceGuard g(device);
+  imask_plan* pl = new imask_plan();
+  pl->side = side;
+  pl->n_angles = n_angles;
+  pl->n_det = n_det;
+  pl->a_begin = angle_begin;
+  pl->a_end = angle_end;
+  pl->n_loc = n_loc;
+  pl->r = r;
+  pl->device = device;
+  pl->scale = scale;
+  pl->probs.assign(probs, probs + r);
+  pl->cosv.assign(cos_tab, cos_tab + n_loc);
+  pl->sinv.assign(sin_tab, sin_tab + n_loc);
+  long long off = 0;
+  pl->cp.r = r;
+  pl->rp.r = r;
+  for (int i = 0; i < r; ++i) {
+    const int f = 1 << (r - 1 - i);
+    pl->factors.push_back(f);
+    pl->phi_off.push_back(off);
+    const long long n = side / f;
+    pl->cp.p[i] = (float)probs[i];
+    pl->rp.p[i] = (float)probs[i];
+    pl->rp.factor[i] = f;
+    pl->rp.offset[i] = off;
+    off += n * n;
+  }
+  pl->cp.pr = (float)probs[r - 1];
+
+  const size_t pair_bytes = sizeof(float2) * (size_t)side * (side + 1);
+  const size_t img_bytes = sizeof(float) * (size_t)side * side;
+  const size_t sino_bytes = sizeof(float) * (size_t)n_loc * n_det;
+  int rc = IMASK_OK;
+  if ((rc = cuda_check(cudaMalloc(&pl->P, pair_bytes), "cudaMalloc P")) ||
+      (rc = cuda_check(cudaMalloc(&pl->PT, pair_bytes), "cudaMalloc PT")) ||
+      (rc = cuda_check(cudaMalloc(&pl->u, img_bytes), "cudaMalloc u")) ||
+      (rc = cuda_check(cudaMalloc(&pl->sino_tmp, sino_bytes > 0 ? sino_bytes : 4),
+                       "cudaMalloc sino"))) {
+    imask_plan_destroy(pl);
+    return rc;
+  }
+  pl->scratch = (int64_t)(2 * pair_bytes + img_bytes + sino_bytes);
+  for (int f : pl->factors) {
+    LevelTables* t;
+    if ((rc = get_tables(pl, f, &t))) {
+      imask_plan_destroy(pl);
+      return rc;
+    }
+  }
+  *out = pl;
+  return IMASK_OK;
+}
+
+int imask_plan_destroy(imask_plan* pl) {
+  if (!pl) return IMASK_OK;
+  DeviceGuard g(pl->device);
+  for (auto& kv : pl->tables) {
+    cudaFree(kv.second.fwd);
+    cudaFree(kv.second.adj);
+  }
+  cudaFree(pl->P);
+  cudaFree(pl->PT);
+  cudaFree(pl->u);
+  cudaFree(pl->sino_tmp);
+  delete pl;
+  return IMASK_OK;
+}
+
+int64_t imask_plan_scratch_bytes(const imask_plan* pl) { return pl ? pl->scratch : 0; }
+
+int imask_project(imask_plan* pl, int factor, const float* u, int64_t u_len, float* sino,
+                  int64_t sino_len, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  int rc = check_factor(pl, factor);
+  if (rc) return rc;
+  const int n = pl->side / factor;
+  if (u_len != (int64_t)n * n)
+    return fail(IMASK_EDIM, "operator expects domain dim " + std::to_string((int64_t)n * n) +
+                                ", got vector of length " + std::to_string(u_len));
+  if (sino_len != (int64_t)pl->n_loc * pl->n_det)
+    return fail(IMASK_EDIM, "operator expects range dim " +
+                                std::to_string((int64_t)pl->n_loc * pl->n_det) +
+                                ", got vector of length " + std::to_string(sino_len));
+  DeviceGuard g(pl->device);
+  LevelTables* t;
+  if ((rc = get_tables(pl, factor, &t))) return rc;
+  if (pl->n_loc == 0) return IMASK_OK;
+  LAUNCH(launch_prepare(u, n, pl->P, pl->PT, S(stream)), "prepare");
+  LAUNCH(launch_forward(pl->P, pl->PT, n, t->fwd, pl->n_loc, pl->n_det, sino, nullptr, S(stream)),
+         "forward");
+  return IMASK_OK;
+}
+
+int imask_backproject(imask_plan* pl, int factor, const float* sino, int64_t sino_len, float* u,
+                      int64_t u_len, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  int rc = check_factor(pl, factor);
+  if (rc) return rc;
+  const int n = pl->side / factor;
+  if (sino_len != (int64_t)pl->n_loc * pl->n_det)
+    return fail(IMASK_EDIM, "operator adjoint expects range dim " +
+                                std::to_string((int64_t)pl->n_loc * pl->n_det) +
+                                ", got vector of length " + std::to_string(sino_len));
+  if (u_len != (int64_t)n * n)
+    return fail(IMASK_EDIM, "operator adjoint output has domain dim " +
+                                std::to_string((int64_t)n * n) + ", got buffer of length " +
+                                std::to_string(u_len));
+  DeviceGuard g(pl->device);
+  LevelTables* t;
+  if ((rc = get_tables(pl, factor, &t))) return rc;
+  if (pl->n_loc == 0) {
+    LAUNCH(cudaMemsetAsync(u, 0, sizeof(float) * n * n, S(stream)), "memset");
+    return IMASK_OK;
+  }
+  LAUNCH(launch_adjoint(sino, u, n, factor, pl->n_loc, pl->n_det, t->adj, S(stream)), "adjoint");
+  return IMASK_OK;
+}
+
+int imask_restrict(int side, int factor, const float* x, float* u, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (side < 1 || factor < 1 || side % factor != 0)
+    return fail(IMASK_EINVAL, "side " + std::to_string(side) + " not divisible by factor " +
+                                  std::to_string(factor));
+  LAUNCH(launch_restrict(x, u, side, factor, S(stream)), "restrict");
+  return IMASK_OK;
+}
+
+int imask_prolong(int side, int factor, const float* u, float* x, float alpha, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (side < 1 || factor < 1 || side % factor != 0)
+    return fail(IMASK_EINVAL, "side " + std::to_string(side) + " not divisible by factor " +
+                                  std::to_string(factor));
+  LAUNCH(launch_prolong(u, x, side, factor, alpha, S(stream)), "prolong");
+  return IMASK_OK;
+}
+
+int imask_compensate(int side, int r, const double* probs, const float* x, float* out,
+                     void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (r < 1 || r > 7) return fail(IMASK_EINVAL, "levels r must be in 1..7");
+  if (side < 1 || side % (1 << (r - 1)) != 0)
+    return fail(IMASK_EINVAL, "side " + std::to_string(side) + " not divisible by 2^(r-1) = " +
+                                  std::to_string(1 << (r - 1)));
+  CompParams cp{};
+  cp.r = r;
+  for (int i = 0; i < r; ++i) cp.p[i] = (float)probs[i];
+  cp.pr = (float)probs[r - 1];
+  LAUNCH(launch_compensate(x, out, side, cp, S(stream)), "compensate");
+  return IMASK_OK;
+}
+
+int imask_sketch_forward(imask_plan* pl, int level, const float* x, float* sino, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  int rc = check_level0(pl, level - 1);
+  if (rc) return rc;
+  DeviceGuard g(pl->device);
+  const int f = pl->factors[level - 1];
+  const int n = pl->side / f;
+  LevelTables* t;
+  if ((rc = get_tables(pl, f, &t))) return rc;
+  if (level < pl->r)
+    LAUNCH(launch_restrict(x, pl->u, pl->side, f, S(stream)), "restrict");
+  else
+    LAUNCH(launch_compensate(x, pl->u, pl->side, pl->cp, S(stream)), "compensate");
+  if (pl->n_loc == 0) return IMASK_OK;
+  LAUNCH(launch_prepare(pl->u, n, pl->P, pl->PT, S(stream)), "prepare");
+  LAUNCH(launch_forward(pl->P, pl->PT, n, t->fwd, pl->n_loc, pl->n_det, sino, nullptr, S(stream)),
+         "forward");
+  return IMASK_OK;
+}
+
+int imask_sketch_adjoint(imask_plan* pl, int level, const float* sino, float* out,
+                         void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  int rc = check_level0(pl, level - 1);
+  if (rc) return rc;
+  DeviceGuard g(pl->device);
+  const int f = pl->factors[level - 1];
+  const int n = pl->side / f;
+  LevelTables* t;
+  if ((rc = get_tables(pl, f, &t))) return rc;
+  if (pl->n_loc == 0)
+    LAUNCH(cudaMemsetAsync(pl->u, 0, sizeof(float) * n * n, S(stream)), "memset");
+  else
+    LAUNCH(launch_adjoint(sino, pl->u, n, f, pl->n_loc, pl->n_det, t->adj, S(stream)), "adjoint");
+  if (level < pl->r)
+    LAUNCH(launch_prolong(pl->u, out, pl->side, f, 1.0f / (float)(f * f), S(stream)), "prolong");
+  else
+    LAUNCH(launch_compensate(pl->u, out, pl->side, pl->cp, S(stream)), "compensate");
+  return IMASK_OK;
+}
+
+int imask_draw_levels(uint64_t seed, int64_t k0, int64_t count, const double* cum_probs, int r,
+                      int32_t* out) {
+  g_err.clear();
+  if (r < 1 || !cum_probs || (count > 0 && !out)) return fail(IMASK_EINVAL, "bad arguments");
+  for (int64_t n = 0; n < count; ++n) {
+    const double u = imask_uniform_at(seed, k0 + n);
+    int idx = 0;
+    while (idx < r && cum_probs[idx] <= u) ++idx;  // searchsorted(..., side="right")
+    out[n] = idx < r - 1 ? idx : r - 1;
+  }
+  return IMASK_OK;
+}
+
+double imask_uniform_at(uint64_t seed, int64_t k) {
+  uint64_t z = mix64(seed + kGolden * (uint64_t)(k + 1));
+  z = mix64(z + kGolden);
+  return (double)(z >> 11) * 0x1.0p-53;
+}
+
+int imask_step_adjoint(imask_plan* pl, const imask_state* st, int level0, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  int rc = check_level0(pl, level0);
+  if (rc) return rc;
+  DeviceGuard g(pl->device);
+  const int f = pl->factors[level0];
+  const int n = pl->side / f;
+  LevelTables* t;
+  if ((rc = get_tables(pl, f, &t))) return rc;
+  if (pl->n_loc == 0)
+    LAUNCH(cudaMemsetAsync(st->bp, 0, sizeof(float) * n * n, S(stream)), "memset");
+  else
+    LAUNCH(launch_adjoint(st->y, st->bp, n, f, pl->n_loc, pl->n_det, t->adj, S(stream)),
+           "adjoint");
+  return IMASK_OK;
+}
+
+int imask_step_forward(imask_plan* pl, const imask_state* st, int level0,
+                       const imask_step_params* prm, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  int rc = check_level0(pl, level0);
+  if (rc) return rc;
+  if (!(prm->sigma > 0.0)) return fail(IMASK_EINVAL, "sigma must be positive");
+  DeviceGuard g(pl->device);
+  const int f = pl->factors[level0];
+  const int n = pl->side / f;
+  LevelTables* t;
+  if ((rc = get_tables(pl, f, &t))) return rc;
+  if (level0 < pl->r - 1)
+    LAUNCH(launch_restrict(st->x, pl->u, pl->side, f, S(stream)), "restrict");
+  else
+    LAUNCH(launch_compensate(st->x, pl->u, pl->side, pl->cp, S(stream)), "compensate");
+  if (pl->n_loc == 0) return IMASK_OK;
+  LAUNCH(launch_prepare(pl->u, n, pl->P, pl->PT, S(stream)), "prepare");
+  const size_t m = (size_t)pl->n_loc * pl->n_det;
+  SinoSaga sg;
+  sg.psi_tab = st->psi_tab + (size_t)level0 * m;
+  sg.psi_sum = st->psi_sum;
+  sg.y = st->y;
+  sg.b = st->b;
+  sg.p_i = (float)pl->probs[level0];
+  sg.sigma = (float)prm->sigma;
+  sg.inv_1ps = (float)(1.0 / (1.0 + prm->sigma));
+  LAUNCH(launch_forward(pl->P, pl->PT, n, t->fwd, pl->n_loc, pl->n_det, nullptr, &sg, S(stream)),
+         "forward+saga");
+  return IMASK_OK;
+}
+
+int imask_step_image(imask_plan* pl, const imask_state* st, int level0,
+                     const imask_step_params* prm, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  int rc = check_level0(pl, level0);
+  if (rc) return rc;
+  if (!(prm->sigma > 0.0) || !(prm->mu_g > 0.0))
+    return fail(IMASK_EINVAL, "sigma and mu_g must be positive");
+  if (!(prm->mu > 0.0)) return fail(IMASK_EINVAL, "mu must be positive");
+  DeviceGuard g(pl->device);
+  const int f = pl->factors[level0];
+  ImageSaga sg;
+  sg.phi_tab = st->phi_tab + pl->phi_off[level0];
+  sg.phi_sum = st->phi_sum;
+  sg.x = st->x;
+  sg.p_i = (float)pl->probs[level0];
+  const double s = prm->sigma / prm->mu;
+  sg.s = (float)s;
+  sg.inv_den = (float)(1.0 / (1.0 + s * prm->mu_g));
+  if (level0 < pl->r - 1)
+    LAUNCH(launch_saga_image_coarse(st->bp, pl->side, f, sg, S(stream)), "saga_image");
+  else
+    LAUNCH(launch_saga_image_full(st->bp, pl->side, pl->cp, sg, S(stream)), "saga_image_full");
+  return IMASK_OK;
+}
+
+int imask_sketch_step(imask_plan* pl, const imask_state* st, int level0,
+                      const imask_step_params* prm, void* stream) {
+  int total = 0, rc;
+  if ((rc = imask_step_adjoint(pl, st, level0, stream))) return rc;
+  total += g_launches;
+  if ((rc = imask_step_forward(pl, st, level0, prm, stream))) return rc;
+  total += g_launches;
+  if ((rc = imask_step_image(pl, st, level0, prm, stream))) return rc;
+  total += g_launches;
+  g_launches = total;
+  return IMASK_OK;
+}
+
+int imask_resum(imask_plan* pl, const imask_state* st, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  DeviceGuard g(pl->device);
+  const size_t m = (size_t)pl->n_loc * pl->n_det;
+  ++g_launches;
+  LAUNCH(launch_resum(st->phi_tab, st->phi_sum, pl->side, st->psi_tab, st->psi_sum, m, pl->rp,
+                      S(stream)),
+         "resum");
+  return IMASK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,78 @@
+// Shared definitions of the sm_100a ImaSk kernels.
+//
+// Ray/pixel geometry (reference ctmodel.py:73-154, restated in
+// oracle/ct_oracle.py): pixel (row, col) of the n x n grid of width h has
+// centre X = -half + (col+.5)h, Y = -half + (row+.5)h, half = n*h/2 (= side/2
+// at every level); ray (a, j) is the line X cos + Y sin = t_j,
+// t_j = j - (n_det-1)/2.
+//
+// Positions along a ray and across a pixel's footprint are carried in signed
+// Q32.32 fixed point (int64): the integer word is a pixel / detector index,
+// the fraction word feeds the weights through a float built from its top 23
+// bits. Stepping is an exact integer add, so no drift builds up along a ray
+// and ties on gridlines (axis-parallel rays with integer offsets) are decided
+// exactly, as the reference's half-open rule requires (ctmodel.py:99-114).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace imask {
+
+constexpr double kFix = 4294967296.0;  // 2^32
+
+// Forward projector, one entry per (level factor, local angle).
+// A ray crosses `n` bands (pixel rows, or columns when |sin| > |cos|); at
+// band b its band coordinate is xi = xi_base + j*xi_dj + b*(step/2^32), in
+// pixel-index units measured from the centre of pixel 0. The band's chord
+// (length wsc/scale) splits between pixel floor(xi) and floor(xi)+1 with
+// fractions (1-g, g), g = sat(onep*S + B), onep = 1 + frac(xi).
+struct FwdAngle {
+  double xi_base;
+  double xi_dj;
+  long long step;
+  float S, B;
+  float wsc;       // h / max(|cos|,|sin|) * scale
+  int transposed;  // 0: bands are rows (row-major image), 1: columns (transposed image)
+};
+
+// Adjoint projector, one entry per (level factor, local angle).
+// For pixel (col,row) the footprint covers detector coordinates
+// eta = X cos + Y sin + (n_det-1)/2 within +-R, a trapezoid of height
+// wsc/scale, plateau half-width |a-b|, support half-width R = a+b
+// (a = |cos|h/2, b = |sin|h/2). eta0 is eta at pixel (0,0) minus R.
+struct AdjAngle {
+  double eta0;
+  double ch, sh;       // cos*h, sin*h
+  long long Dc, Ds;    // Q32.32 of ch, sh
+  float R;             // support half-width in detector units
+  float kneg, Rk;      // w = sat(|u|*kneg + Rk), kneg = -1/(2 min(a,b)), Rk = R/(2 min(a,b))
+  float wsc;           // h / max(|cos|,|sin|) * scale
+  int nb;              // candidate bins per pixel
+  int axis;            // 1: axis-parallel half-open box rule
+};
+
+// 1 + (top 23 bits of a Q0.32 fraction) as a float in [1, 2)
+__device__ __forceinline__ float onep_from_frac(uint32_t frac) {
+  return __uint_as_float((frac >> 9) | 0x3F800000u);
+}
+
+struct SinoSaga {  // sinogram side of the SAGA step, fused into the forward epilogue
+  float* psi_tab;        // level row of the psi table
+  float* psi_sum;
+  float* y;
+  const float* b;
+  float p_i;
+  float sigma;
+  float inv_1ps;  // 1 / (1 + sigma)
+};
+
+struct ImageSaga {
+  float* phi_tab;  // level row of the phi table (coarse, or full at the full level)
+  float* phi_sum;
+  float* x;
+  float p_i;
+  float s;        // sigma / mu
+  float inv_den;  // 1 / (1 + s*mu_g)
+};
+
+}  // namespace imask

@@ -1,0 +1,287 @@
+// Kernels (3) and (4): the multiresolution sketch family and the fused SAGA
+// updates.
+//   restrict   : T_f block mean                 (mrsketch.py:23-32)
+//   prolong    : alpha * U_f replication        (mrsketch.py:35-41, 54-55)
+//   compensate : S_r = (I - sum_{i<r} p_i S_i)/p_r by a tile-local pyramid
+//                (mrsketch.py:133-153); block means are aligned to the
+//                2^(r-1) grid, so every 2^(r-1)-tile is independent.
+//   prepare    : coarse image -> the forward projector's pair layouts
+//                P[row][c+1] = (u[row][c], u[row][c+1]-u[row][c]), c = -1..n-1,
+//                and the same on the transpose, zero outside the image.
+//   saga_image : image side of sketch_step (solvers.py:204-214): new adjoint
+//                product (prolonged /f^2 or compensated), table row, phi_sum,
+//                primal ridge prox (proxlib.py:51-55), one pass over HBM.
+//   resum      : _resum (solvers.py:184-191).
+#include "imask_common.cuh"
+#include "sketch.cuh"
+
+namespace imask {
+
+// ---- restriction / prolongation -------------------------------------------
+
+// thread per coarse pixel (small factors)
+__global__ void k_restrict_small(const float* __restrict__ x, float* __restrict__ u, int side,
+                                 int f) {
+  const int n = side / f;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * n) return;
+  const int R = idx / n, C = idx % n;
+  const float* base = x + (size_t)R * f * side + (size_t)C * f;
+  float s = 0.f;
+  for (int i = 0; i < f; ++i) {
+    float rs = 0.f;
+    for (int j = 0; j < f; ++j) rs += __ldg(base + (size_t)i * side + j);
+    s += rs;
+  }
+  u[idx] = s * (1.0f / (float)(f * f));
+}
+
+// warp per coarse pixel (factors >= 16)
+__global__ void k_restrict_warp(const float* __restrict__ x, float* __restrict__ u, int side,
+                                int f) {
+  const int n = side / f;
+  const int w = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= n * n) return;
+  const int R = w / n, C = w % n;
+  const float* base = x + (size_t)R * f * side + (size_t)C * f;
+  float s = 0.f;
+  for (int e = lane; e < f * f; e += 32) s += __ldg(base + (size_t)(e / f) * side + (e % f));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) u[w] = s * (1.0f / (float)(f * f));
+}
+
+__global__ void k_prolong(const float* __restrict__ u, float* __restrict__ x, int side, int f,
+                          float alpha) {
+  const int n = side / f;
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (size_t)side * side) return;
+  const int row = (int)(idx / side), col = (int)(idx % side);
+  x[idx] = alpha * __ldg(u + (size_t)(row / f) * n + col / f);
+}
+
+// ---- compensation -----------------------------------------------------------
+
+template <int TT>
+__global__ void __launch_bounds__(256)
+k_compensate(const float* __restrict__ x, float* __restrict__ out, int side, CompParams cp) {
+  __shared__ float tile[TT * TT];
+  __shared__ float pyr[TT * TT / 3 + 8];
+  const int ts = min(TT, side);
+  const int x0 = blockIdx.x * ts, y0 = blockIdx.y * ts;
+  for (int e = threadIdx.x; e < ts * ts; e += blockDim.x)
+    tile[e] = __ldg(x + (size_t)(y0 + e / ts) * side + x0 + e % ts);
+  __syncthreads();
+  build_pyramid(tile, pyr, ts, cp.r);
+  for (int e = threadIdx.x; e < ts * ts; e += blockDim.x) {
+    const int py = e / ts, px = e % ts;
+    out[(size_t)(y0 + py) * side + x0 + px] = compensated(tile[e], pyr, ts, cp, py, px);
+  }
+}
+
+// ---- projector staging ------------------------------------------------------
+
+// One 32x32 block of u per CTA: writes P rows [r0,r0+32) entries c+1 for
+// c in [c0, c0+32), PT rows [c0,c0+32) entries r+1 for r in [r0, r0+32);
+// the c = -1 / r = -1 entries come from the blocks at c0 = 0 / r0 = 0.
+__global__ void __launch_bounds__(256)
+k_prepare(const float* __restrict__ u, int n, float2* __restrict__ P, float2* __restrict__ PT) {
+  __shared__ float t[33][34];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int pitch = n + 1;
+  for (int e = threadIdx.x; e < 33 * 33; e += blockDim.x) {
+    const int rr = e / 33, cc = e % 33;
+    const int R = r0 + rr, C = c0 + cc;
+    t[rr][cc] = (R < n && C < n) ? __ldg(u + (size_t)R * n + C) : 0.f;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+    const int rr = e / 32, cc = e % 32;
+    const int R = r0 + rr, C = c0 + cc;
+    if (R < n && C < n) {
+      const float v = t[rr][cc];
+      P[(size_t)R * pitch + C + 1] = make_float2(v, t[rr][cc + 1] - v);
+      if (C == 0) P[(size_t)R * pitch] = make_float2(0.f, v);
+    }
+    // transpose: consecutive threads walk rows of u (= entries of a PT row)
+    const int Rt = r0 + cc, Ct = c0 + rr;
+    if (Rt < n && Ct < n) {
+      const float v = t[cc][rr];
+      PT[(size_t)Ct * pitch + Rt + 1] = make_float2(v, t[cc + 1][rr] - v);
+      if (Rt == 0) PT[(size_t)Ct * pitch] = make_float2(0.f, v);
+    }
+  }
+}
+
+// ---- SAGA image side --------------------------------------------------------
+
+// Coarse level (factor f > 1): phi_new = U_f(bp)/f^2 is constant on f x f
+// blocks, so the table row is stored compactly (one value per coarse pixel).
+// A CTA owns whole blocks (tile side ts is a multiple of f), reads every old
+// row value it needs, synchronises, then replaces the row entries it owns.
+__global__ void __launch_bounds__(256)
+k_saga_image_coarse(const float* __restrict__ bp, int side, int f, int ts, float inv_f2,
+                    ImageSaga sg) {
+  const int n = side / f;
+  const int x0 = blockIdx.x * ts, y0 = blockIdx.y * ts;
+  for (int e = threadIdx.x; e < ts * ts; e += blockDim.x) {
+    const int row = y0 + e / ts, col = x0 + e % ts;
+    const int q = (row / f) * n + col / f;
+    const size_t p = (size_t)row * side + col;
+    const float pn = __ldg(bp + q) * inv_f2;
+    const float d = pn - sg.phi_tab[q];
+    const float ps = sg.phi_sum[p];
+    const float xi = d + ps;
+    sg.phi_sum[p] = fmaf(sg.p_i, d, ps);
+    sg.x[p] = fmaf(-sg.s, xi, sg.x[p]) * sg.inv_den;
+  }
+  __syncthreads();
+  const int tc = ts / f;
+  for (int e = threadIdx.x; e < tc * tc; e += blockDim.x) {
+    const int q = (y0 / f + e / tc) * n + x0 / f + e % tc;
+    sg.phi_tab[q] = __ldg(bp + q) * inv_f2;
+  }
+}
+
+// Full level: phi_new = S_r(bp) computed tile-locally, then the update.
+template <int TT>
+__global__ void __launch_bounds__(256)
+k_saga_image_full(const float* __restrict__ bp, int side, CompParams cp, ImageSaga sg) {
+  __shared__ float tile[TT * TT];
+  __shared__ float pyr[TT * TT / 3 + 8];
+  const int ts = min(TT, side);
+  const int x0 = blockIdx.x * ts, y0 = blockIdx.y * ts;
+  for (int e = threadIdx.x; e < ts * ts; e += blockDim.x)
+    tile[e] = __ldg(bp + (size_t)(y0 + e / ts) * side + x0 + e % ts);
+  __syncthreads();
+  build_pyramid(tile, pyr, ts, cp.r);
+  for (int e = threadIdx.x; e < ts * ts; e += blockDim.x) {
+    const int py = e / ts, px = e % ts;
+    const size_t p = (size_t)(y0 + py) * side + x0 + px;
+    const float pn = compensated(tile[e], pyr, ts, cp, py, px);
+    const float d = pn - sg.phi_tab[p];
+    const float ps = sg.phi_sum[p];
+    const float xi = d + ps;
+    sg.phi_sum[p] = fmaf(sg.p_i, d, ps);
+    sg.phi_tab[p] = pn;
+    sg.x[p] = fmaf(-sg.s, xi, sg.x[p]) * sg.inv_den;
+  }
+}
+
+// Standalone sinogram-side update (used when the forward is not fused).
+__global__ void k_saga_sino(const float* __restrict__ psi_new, size_t m, SinoSaga sg) {
+  const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  const float pn = psi_new[q];
+  const float d = pn - sg.psi_tab[q];
+  const float ps = sg.psi_sum[q];
+  const float zeta = d + ps;
+  sg.psi_sum[q] = fmaf(sg.p_i, d, ps);
+  sg.psi_tab[q] = pn;
+  const float yv = fmaf(sg.sigma, zeta, sg.y[q]);
+  sg.y[q] = (yv - sg.sigma * sg.b[q]) * sg.inv_1ps;
+}
+
+// ---- resum (solvers.py:184-191) --------------------------------------------
+
+__global__ void k_resum_image(const float* __restrict__ phi_tab, float* __restrict__ phi_sum,
+                              int side, ResumParams rp) {
+  const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (size_t)side * side) return;
+  const int row = (int)(p / side), col = (int)(p % side);
+  float acc = 0.f;
+  for (int i = 0; i < rp.r; ++i) {
+    const int f = rp.factor[i], n = side / f;
+    const float v = rp.p[i] * __ldg(phi_tab + rp.offset[i] + (size_t)(row / f) * n + col / f);
+    acc = (i == 0) ? v : acc + v;
+  }
+  phi_sum[p] = acc;
+}
+
+__global__ void k_resum_sino(const float* __restrict__ psi_tab, float* __restrict__ psi_sum,
+                             size_t m, ResumParams rp) {
+  const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  float acc = 0.f;
+  for (int i = 0; i < rp.r; ++i) {
+    const float v = rp.p[i] * __ldg(psi_tab + (size_t)i * m + q);
+    acc = (i == 0) ? v : acc + v;
+  }
+  psi_sum[q] = acc;
+}
+
+// ---- launchers --------------------------------------------------------------
+
+static inline unsigned blocks_for(size_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+cudaError_t launch_restrict(const float* x, float* u, int side, int f, cudaStream_t s) {
+  const int n = side / f;
+  if (f >= 16) {
+    k_restrict_warp<<<blocks_for((size_t)n * n * 32, 256), 256, 0, s>>>(x, u, side, f);
+  } else {
+    k_restrict_small<<<blocks_for((size_t)n * n, 256), 256, 0, s>>>(x, u, side, f);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prolong(const float* u, float* x, int side, int f, float alpha,
+                           cudaStream_t s) {
+  k_prolong<<<blocks_for((size_t)side * side, 256), 256, 0, s>>>(u, x, side, f, alpha);
+  return cudaGetLastError();
+}
+
+static inline int comp_tile(int r) { return (r <= 6) ? 32 : 64; }
+
+cudaError_t launch_compensate(const float* x, float* out, int side, const CompParams& cp,
+                              cudaStream_t s) {
+  const int TT = comp_tile(cp.r);
+  const int ts = side < TT ? side : TT;
+  dim3 grid(side / ts, side / ts);
+  if (TT == 32)
+    k_compensate<32><<<grid, 256, 0, s>>>(x, out, side, cp);
+  else
+    k_compensate<64><<<grid, 256, 0, s>>>(x, out, side, cp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prepare(const float* u, int n, float2* P, float2* PT, cudaStream_t s) {
+  dim3 grid((n + 31) / 32, (n + 31) / 32);
+  k_prepare<<<grid, 256, 0, s>>>(u, n, P, PT);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_saga_image_coarse(const float* bp, int side, int f, const ImageSaga& sg,
+                                     cudaStream_t s) {
+  int ts = f > 32 ? f : 32;
+  if (ts > side) ts = side;
+  dim3 grid(side / ts, side / ts);
+  k_saga_image_coarse<<<grid, 256, 0, s>>>(bp, side, f, ts, 1.0f / (float)(f * f), sg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_saga_image_full(const float* bp, int side, const CompParams& cp,
+                                   const ImageSaga& sg, cudaStream_t s) {
+  const int TT = comp_tile(cp.r);
+  const int ts = side < TT ? side : TT;
+  dim3 grid(side / ts, side / ts);
+  if (TT == 32)
+    k_saga_image_full<32><<<grid, 256, 0, s>>>(bp, side, cp, sg);
+  else
+    k_saga_image_full<64><<<grid, 256, 0, s>>>(bp, side, cp, sg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_saga_sino(const float* psi_new, size_t m, const SinoSaga& sg, cudaStream_t s) {
+  k_saga_sino<<<blocks_for(m, 256), 256, 0, s>>>(psi_new, m, sg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_resum(const float* phi_tab, float* phi_sum, int side, const float* psi_tab,
+                         float* psi_sum, size_t m, const ResumParams& rp, cudaStream_t s) {
+  k_resum_image<<<blocks_for((size_t)side * side, 256), 256, 0, s>>>(phi_tab, phi_sum, side, rp);
+  k_resum_sino<<<blocks_for(m, 256), 256, 0, s>>>(psi_tab, psi_sum, m, rp);
+  return cudaGetLastError();
+}
+
+}  // namespace imask

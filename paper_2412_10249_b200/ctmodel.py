@@ -1,0 +1,278 @@
+"""2-D parallel-beam projector on the B200 (drop-in for `mrtomo.ctmodel`).
+
+Surface of the reference module for the hot path (pkg/src/mrtomo/ctmodel.py):
+`Geometry` (ctmodel.py:38-70), `project` / `backproject` (ctmodel.py:170-185),
+`projector_op` (ctmodel.py:188-191) and `coarse_projector`
+(ctmodel.py:194-204). Instead of a cached scipy CSR matrix
+(`_projector_pair`, ctmodel.py:157-167) each geometry gets a cached native
+`Plan` holding float64-derived per-angle tables; the chords are evaluated on
+the fly by the sm_100a kernels in `csrc/projector.cu`.
+
+Phantoms, noise and the PGM I/O (ctmodel.py:207-333) are host-side data
+tooling, out of scope for this path; the BASELINE's
+synthetic inputs live in `synth.py`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import threading
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .linops import LinOp, default_device, to_device
+
+AXIS_SNAP = 1e-14  # ctmodel.py:20
+
+
+@dataclass(frozen=True)
+class Geometry:
+    """Parallel-beam scan geometry over a unit-pitch square grid (ctmodel.py:38-70)."""
+
+    side: int
+    n_angles: int = 100
+    n_detectors: Optional[int] = None
+
+    def __post_init__(self):
+        if self.side < 1:
+            raise ValueError("side must be positive")
+        if self.n_detectors is None:
+            object.__setattr__(
+                self, "n_detectors", math.ceil(math.sqrt(2.0 * self.side * self.side))
+            )
+
+    @property
+    def m(self) -> int:
+        return self.n_angles * self.n_detectors
+
+    @property
+    def angles(self) -> np.ndarray:
+        return np.arange(self.n_angles) * (np.pi / self.n_angles)
+
+    @property
+    def offsets(self) -> np.ndarray:
+        n = self.n_detectors
+        return np.arange(n, dtype=float) - (n - 1) / 2.0
+
+    def cos_sin(self, begin: int = 0, end: Optional[int] = None):
+        """float64 cos/sin of angles [begin, end), snapped below 1e-14 (ctmodel.py:88-93).
+
+        The snap is decided here, in float64, and passed to the device, so the
+        axis-parallel tie rule never depends on float32 rounding.
+        """
+        end = self.n_angles if end is None else end
+        th = self.angles[begin:end]
+        c = np.array([math.cos(t) for t in th])
+        s = np.array([math.sin(t) for t in th])
+        c[np.abs(c) < AXIS_SNAP] = 0.0
+        s[np.abs(s) < AXIS_SNAP] = 0.0
+        return c, s
+
+
+def slab_bounds(n_angles: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous angle slab of one rank; uneven splits put the extra angles first."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of world {world}")
+    base, extra = divmod(n_angles, world)
+    begin = rank * base + min(rank, extra)
+    return begin, begin + base + (1 if rank < extra else 0)
+
+
+def _stream_ptr(device: torch.device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _ptr(t: torch.Tensor) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Plan:
+    """Native plan of one geometry, angle slab, sketch family and scale on one device."""
+
+    def __init__(
+        self,
+        geom: Geometry,
+        r: int = 1,
+        probs: Sequence[float] = (1.0,),
+        scale: float = 1.0,
+        angle_begin: int = 0,
+        angle_end: Optional[int] = None,
+        device: Optional[torch.device] = None,
+    ):
+        self.geom = geom
+        self.device = device or default_device()
+        self.angle_begin = angle_begin
+        self.angle_end = geom.n_angles if angle_end is None else angle_end
+        self.n_loc = self.angle_end - self.angle_begin
+        self.m_loc = self.n_loc * geom.n_detectors
+        self.r = int(r)
+        self.probs = np.asarray(probs, dtype=float)
+        self.scale = float(scale)
+        self.factors = tuple(2 ** (self.r - i) for i in range(1, self.r + 1))
+        c, s = geom.cos_sin(self.angle_begin, self.angle_end)
+        self._c = np.ascontiguousarray(c)
+        self._s = np.ascontiguousarray(s)
+        dp = ctypes.POINTER(ctypes.c_double)
+        handle = ctypes.c_void_p()
+        L = _lib.lib()
+        with torch.cuda.device(self.device):
+            _lib.check(
+                L.imask_plan_create(
+                    geom.side, geom.n_angles, geom.n_detectors, self.angle_begin, self.angle_end,
+                    self._c.ctypes.data_as(dp), self._s.ctypes.data_as(dp), self.r,
+                    self.probs.ctypes.data_as(dp), self.scale, self.device.index, ctypes.byref(handle),
+                )
+            )
+        self.handle = handle
+        self.phi_offsets = []
+        off = 0
+        for f in self.factors:
+            self.phi_offsets.append(off)
+            off += (geom.side // f) ** 2
+        self.phi_tab_len = off
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().imask_plan_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    @property
+    def stream(self) -> ctypes.c_void_p:
+        return _stream_ptr(self.device)
+
+    def project(self, u: torch.Tensor, factor: int, out: Optional[torch.Tensor] = None):
+        """sino = R_f u on this slab (float32 device tensors)."""
+        if out is None:
+            out = torch.empty(self.m_loc, device=self.device, dtype=torch.float32)
+        _lib.check(
+            _lib.lib().imask_project(
+                self.handle, factor, _ptr(u), u.numel(), _ptr(out), out.numel(), self.stream
+            )
+        )
+        return out
+
+    def backproject(self, y: torch.Tensor, factor: int, out: Optional[torch.Tensor] = None):
+        n = self.geom.side // factor if self.geom.side % factor == 0 else 0
+        if out is None:
+            out = torch.empty(n * n, device=self.device, dtype=torch.float32)
+        _lib.check(
+            _lib.lib().imask_backproject(
+                self.handle, factor, _ptr(y), y.numel(), _ptr(out), out.numel(), self.stream
+            )
+        )
+        return out
+
+    def sketch_forward(self, level: int, x: torch.Tensor, out: Optional[torch.Tensor] = None):
+        if out is None:
+            out = torch.empty(self.m_loc, device=self.device, dtype=torch.float32)
+        _lib.check(
+            _lib.lib().imask_sketch_forward(self.handle, level, _ptr(x), _ptr(out), self.stream)
+        )
+        return out
+
+    def sketch_adjoint(self, level: int, y: torch.Tensor, out: Optional[torch.Tensor] = None):
+        if out is None:
+            out = torch.empty(self.geom.side ** 2, device=self.device, dtype=torch.float32)
+        _lib.check(
+            _lib.lib().imask_sketch_adjoint(self.handle, level, _ptr(y), _ptr(out), self.stream)
+        )
+        return out
+
+
+_plan_cache: dict = {}
+_plan_lock = threading.Lock()
+
+
+def get_plan(geom: Geometry, r=1, probs=(1.0,), scale=1.0, angle_begin=0, angle_end=None,
+             device=None) -> Plan:
+    """Cached plan per (geometry, family, scale, slab, device), like _projector_pair."""
+    device = device or default_device()
+    angle_end = geom.n_angles if angle_end is None else angle_end
+    key = (geom, int(r), tuple(float(p) for p in probs), float(scale), angle_begin, angle_end,
+           str(device))
+    with _plan_lock:
+        plan = _plan_cache.get(key)
+        if plan is None:
+            plan = Plan(geom, r, probs, scale, angle_begin, angle_end, device)
+            _plan_cache[key] = plan
+    return plan
+
+
+@dataclass(frozen=True)
+class ProjectorMeta:
+    """What the fused solver needs to know about a projector LinOp."""
+
+    geom: Geometry
+    factor: int
+    scale: float = 1.0
+    angle_begin: int = 0
+    angle_end: Optional[int] = None
+
+    def scaled(self, alpha: float) -> "ProjectorMeta":
+        return ProjectorMeta(self.geom, self.factor, self.scale * alpha, self.angle_begin,
+                             self.angle_end)
+
+
+def _projector_linop(geom: Geometry, factor: int, scale: float = 1.0, angle_begin: int = 0,
+                     angle_end: Optional[int] = None) -> LinOp:
+    """R_f restricted to the angle slab [angle_begin, angle_end) (all angles by default).
+
+    The plan is resolved at first apply (after the caller has picked its CUDA device).
+    """
+    angle_end = geom.n_angles if angle_end is None else angle_end
+    low = geom.side // factor
+    meta = ProjectorMeta(geom, factor, scale, angle_begin, angle_end)
+
+    def plan():
+        return get_plan(geom, scale=scale, angle_begin=angle_begin, angle_end=angle_end)
+
+    return LinOp(
+        low * low,
+        (angle_end - angle_begin) * geom.n_detectors,
+        lambda x: plan().project(to_device(x), factor),
+        lambda y: plan().backproject(to_device(y), factor),
+        meta,
+    )
+
+
+def project(geom: Geometry, x, pixel_width: float = 1.0) -> torch.Tensor:
+    """(n_angles, n_detectors) sinogram of an image (ctmodel.py:170-176)."""
+    if pixel_width != 1.0:
+        raise NotImplementedError("only unit pixel width is on the B200 path")
+    t = to_device(x)
+    if t.numel() != geom.side * geom.side:
+        raise ValueError(f"image has {t.numel()} pixels, geometry expects {geom.side}^2")
+    return get_plan(geom).project(t, 1).reshape(geom.n_angles, geom.n_detectors)
+
+
+def backproject(geom: Geometry, y, pixel_width: float = 1.0) -> torch.Tensor:
+    """Exact adjoint of project; (side, side) image (ctmodel.py:179-185)."""
+    if pixel_width != 1.0:
+        raise NotImplementedError("only unit pixel width is on the B200 path")
+    t = to_device(y)
+    if t.numel() != geom.m:
+        raise ValueError(f"sinogram has {t.numel()} bins, geometry expects {geom.m}")
+    return get_plan(geom).backproject(t, 1).reshape(geom.side, geom.side)
+
+
+def projector_op(geom: Geometry, pixel_width: float = 1.0) -> LinOp:
+    """Full-resolution forward model as a flat LinOp (ctmodel.py:188-191)."""
+    if pixel_width != 1.0:
+        raise NotImplementedError("only unit pixel width is on the B200 path")
+    return _projector_linop(geom, 1)
+
+
+def coarse_projector(geom: Geometry, factor: int) -> LinOp:
+    """Forward model on the grid coarsened by ``factor`` (ctmodel.py:194-204)."""
+    if geom.side % factor != 0:
+        raise ValueError(f"side {geom.side} not divisible by factor {factor}")
+    return _projector_linop(geom, factor)

@@ -1,0 +1,396 @@
+"""Device-resident sketched SAGA solver (drop-in for the hot path of `mrtomo.solvers`).
+
+Mirrors reference pkg/src/mrtomo/solvers.py: the counter-based level RNG
+(`uniform_at`, `draw_level`, solvers.py:30-48; evaluated bit-exactly by the
+C library), `Problem` / `make_problem` (solvers.py:51-102), `SaddleState`
+(solvers.py:119-140), `init_state` (solvers.py:143-181), `_resum`
+(solvers.py:184-191), `sketch_step` (solvers.py:194-221), `SolveReport` and
+`run` for the "sketch" algorithm (solvers.py:345-480).
+
+One iteration is three native calls (csrc/capi.cu): the adjoint of level i
+on y^k, the forward of level i on x^k fused with the sinogram-side update
+(psi row, psi_sum, dual prox), and the image-side update (phi row, phi_sum,
+primal prox). Host work per iteration is the level draw and the ledger.
+With an angle-sharded problem (`dist.py`) the partial backprojection is
+all-reduced between the first and the last call while the forward runs.
+
+Storage difference: coarse phi rows are kept compact ((side/f)^2 values)
+since the reference's full-resolution rows are their replication
+(mrsketch.py:54-55); `SaddleState.phi_full(i)` returns the reference layout.
+The other algorithms of `run` (pdhg, sketch-seq, saga-saddle) are the
+SURVEY §8(f) "next" rows.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+from typing import Any, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .ctmodel import Geometry, get_plan, slab_bounds
+from .linops import LinOp, to_device
+from .mrsketch import SketchFamily, SketchedMeta, cost_fraction, forward_family
+from .proxlib import ProxFn
+
+_MASK64 = (1 << 64) - 1
+ALGORITHMS = ("sketch", "sketch-seq", "pdhg", "saga-saddle")
+
+
+def uniform_at(seed: int, k: int) -> float:
+    """Counter-based uniform in [0,1) (solvers.py:37-41), from the C library."""
+    return float(_lib.lib().imask_uniform_at(seed & _MASK64, k))
+
+
+def draw_levels(seed: int, k0: int, count: int, cum_probs: np.ndarray) -> np.ndarray:
+    """draw_level(seed, k) for k in [k0, k0+count) (solvers.py:44-48), bit-exact."""
+    cum = np.ascontiguousarray(cum_probs, dtype=float)
+    out = np.empty(max(count, 0), dtype=np.int32)
+    _lib.check(
+        _lib.lib().imask_draw_levels(
+            seed & _MASK64, k0, count, cum.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+            cum.size, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+        )
+    )
+    return out
+
+
+def draw_level(seed: int, k: int, cum_probs: np.ndarray) -> int:
+    """0-based level index via inverse CDF in index order (solvers.py:44-48)."""
+    return int(draw_levels(seed, k, 1, cum_probs)[0])
+
+
+@dataclass(frozen=True)
+class Shard:
+    """This rank's angle slab and the process group the backprojection is reduced over."""
+
+    rank: int = 0
+    world: int = 1
+    group: Any = None
+
+
+class Engine:
+    """Native state of the fused sketch_step for one problem on one device."""
+
+    def __init__(self, geom: Geometry, family: SketchFamily, scale: float, mu_g: float,
+                 b: torch.Tensor, shard: Shard, begin: int, end: int):
+        self.geom = geom
+        self.family = family
+        self.shard = shard
+        self.plan = get_plan(geom, family.r, tuple(family.probs), scale, begin, end)
+        self.device = self.plan.device
+        self.mu_g = float(mu_g)
+        self.b = b
+        self.m_loc = self.plan.m_loc
+        self.d = geom.side * geom.side
+
+
+@dataclass(frozen=True)
+class Problem:
+    """A regularised linear inverse problem plus its sketched operators (solvers.py:51-85).
+
+    For an angle-sharded problem ``b`` and every operator act on this rank's
+    slab of the sinogram (see dist.make_sharded_problem).
+    """
+
+    K: LinOp
+    b: Any
+    g: ProxFn
+    f_conj: ProxFn
+    probs: np.ndarray
+    ops: tuple
+    fractions: np.ndarray
+    family: Optional[SketchFamily] = None
+    shard: Shard = Shard()
+    cum_probs: np.ndarray = field(init=False)
+    engine: Optional[Engine] = field(init=False, default=None, compare=False)
+
+    def __post_init__(self):
+        b = to_device(self.b)
+        if b.numel() != self.K.range_dim:
+            raise ValueError(
+                f"data has {b.numel()} entries, operator range is {self.K.range_dim}"
+            )
+        probs = np.asarray(self.probs, dtype=float)
+        if probs.size != len(self.ops):
+            raise ValueError("one probability per operator level required")
+        object.__setattr__(self, "b", b)
+        object.__setattr__(self, "probs", probs)
+        object.__setattr__(self, "fractions", np.asarray(self.fractions, dtype=float))
+        object.__setattr__(self, "cum_probs", np.cumsum(probs))
+        object.__setattr__(self, "engine", self._build_engine())
+
+    @property
+    def r(self) -> int:
+        return len(self.ops)
+
+    def _build_engine(self) -> Optional[Engine]:
+        metas = [getattr(op, "meta", None) for op in self.ops]
+        if self.family is None or not all(isinstance(m, SketchedMeta) for m in metas):
+            return None
+        proj = metas[0].projector
+        if proj is None or any(m.projector != proj or m.family != self.family for m in metas):
+            return None
+        if self.g.kind != "ridge" or self.f_conj.kind != "quadratic_conjugate":
+            return None
+        begin = proj.angle_begin
+        end = proj.geom.n_angles if proj.angle_end is None else proj.angle_end
+        if self.shard.world > 1 and (begin, end) != slab_bounds(
+                proj.geom.n_angles, self.shard.rank, self.shard.world):
+            raise ValueError("projector angle slab does not match this rank's shard")
+        return Engine(proj.geom, self.family, proj.scale, self.g.param, self.f_conj.param,
+                      self.shard, begin, end)
+
+
+def make_problem(K: LinOp, b, family: SketchFamily, g: ProxFn, f_conj: ProxFn,
+                 coarse_projector=None, shard: Shard = Shard()) -> Problem:
+    """Assemble a Problem from a sketch family (solvers.py:88-102)."""
+    ops = tuple(forward_family(family, K, coarse_projector))
+    fractions = np.array([cost_fraction(family, i) for i in range(1, family.r + 1)])
+    return Problem(K=K, b=b, g=g, f_conj=f_conj, probs=family.probs, ops=ops,
+                   fractions=fractions, family=family, shard=shard)
+
+
+@dataclass
+class SaddleState:
+    """Iterate pair plus per-level memory tables and their weighted sums (solvers.py:119-140).
+
+    All arrays are float32 device tensors; ``phi[i]`` is compact for coarse levels.
+    """
+
+    x: torch.Tensor
+    y: torch.Tensor
+    phi: list
+    psi: list
+    phi_sum: torch.Tensor
+    psi_sum: torch.Tensor
+    k: int = 0
+    cost: float = 0.0
+    seed: int = 0
+    last_level: int = 0
+    xbar: Optional[torch.Tensor] = None
+    resum_every: int = 1000
+    phi_tab: Optional[torch.Tensor] = None
+    psi_tab: Optional[torch.Tensor] = None
+    bp: Optional[torch.Tensor] = None
+    _cstate: Any = field(default=None, repr=False)
+
+    def phi_full(self, i: int, family: SketchFamily) -> torch.Tensor:
+        """Row i (0-based) in the reference's full-resolution layout."""
+        f = family.decim_factors[i]
+        if f == 1:
+            return self.phi[i]
+        from .mrsketch import upsample
+
+        low = family.side // f
+        return upsample(self.phi[i].reshape(low, low), f).reshape(-1)
+
+    def c_state(self, b: torch.Tensor) -> _lib.ImaskState:
+        if self._cstate is None:
+            self._cstate = _lib.ImaskState(
+                self.x.data_ptr(), self.y.data_ptr(), b.data_ptr(), self.phi_sum.data_ptr(),
+                self.psi_sum.data_ptr(), self.phi_tab.data_ptr(), self.psi_tab.data_ptr(),
+                self.bp.data_ptr(),
+            )
+        return self._cstate
+
+
+def _require_engine(prob: Problem) -> Engine:
+    if prob.engine is None:
+        raise TypeError(
+            "the B200 sketch_step needs a coarse-mode problem built by make_problem from this "
+            "package's projector_op / coarse_projector, with ridge g and the quadratic-data "
+            "conjugate f*"
+        )
+    return prob.engine
+
+
+def init_state(prob: Problem, seed: int = 0, x0=None, y0=None, exact_memory: bool = False,
+               resum_every: int = 1000) -> SaddleState:
+    """Fresh device state: zero start with zero memory unless told otherwise (solvers.py:143-181)."""
+    eng = _require_engine(prob)
+    dev = eng.device
+    d, m, r = eng.d, eng.m_loc, prob.r
+    x = torch.zeros(d, device=dev) if x0 is None else to_device(x0, dev).clone()
+    y = torch.zeros(m, device=dev) if y0 is None else to_device(y0, dev).clone()
+    plan = eng.plan
+    phi_tab = torch.zeros(plan.phi_tab_len, device=dev)
+    psi_tab = torch.zeros(r * m, device=dev)
+    phi = [phi_tab[o:o + (eng.geom.side // f) ** 2] for o, f in zip(plan.phi_offsets, plan.factors)]
+    psi = [psi_tab[i * m:(i + 1) * m] for i in range(r)]
+    st = SaddleState(
+        x=x, y=y, phi=phi, psi=psi, phi_sum=torch.zeros(d, device=dev),
+        psi_sum=torch.zeros(m, device=dev), seed=seed, xbar=x.clone(), resum_every=resum_every,
+        phi_tab=phi_tab, psi_tab=psi_tab, bp=torch.empty(d, device=dev),
+    )
+    if exact_memory:
+        for i in range(r):
+            f = plan.factors[i]
+            if f > 1:
+                bp = plan.backproject(y, f)
+                _allreduce(eng, bp)
+                phi[i].copy_(bp * (1.0 / (f * f)))
+            else:
+                bp = plan.backproject(y, 1)
+                _allreduce(eng, bp)
+                phi[i].copy_(prob.family._apply_compensation(bp.reshape(eng.geom.side, -1)).reshape(-1))
+            psi[i].copy_(plan.sketch_forward(i + 1, x))
+        _resum(st, prob)
+    return st
+
+
+def _allreduce(eng: Engine, t: torch.Tensor, async_op: bool = False):
+    if eng.shard.world == 1:
+        return None
+    import torch.distributed as dist
+
+    return dist.all_reduce(t, op=dist.ReduceOp.SUM, group=eng.shard.group, async_op=async_op)
+
+
+def _resum(state: SaddleState, prob: Problem) -> None:
+    """Recompute phi_sum / psi_sum from the tables in index order (solvers.py:184-191)."""
+    eng = _require_engine(prob)
+    _lib.check(_lib.lib().imask_resum(eng.plan.handle, ctypes.byref(state.c_state(eng.b)),
+                                      eng.plan.stream))
+
+
+def _params(sigma: float, mu: float, mu_g: float) -> _lib.ImaskStepParams:
+    if sigma <= 0 or mu_g <= 0:
+        raise ValueError("sigma and mu_g must be positive")
+    if mu <= 0:
+        raise ValueError("mu must be positive")
+    return _lib.ImaskStepParams(float(sigma), float(mu), float(mu_g))
+
+
+def _device_step(eng: Engine, state: SaddleState, level0: int, prm: _lib.ImaskStepParams) -> int:
+    """Enqueue one iteration; returns the number of kernels launched."""
+    L = _lib.lib()
+    cst = ctypes.byref(state.c_state(eng.b))
+    h, s = eng.plan.handle, eng.plan.stream
+    if eng.shard.world == 1:
+        _lib.check(L.imask_sketch_step(h, cst, level0, ctypes.byref(prm), s))
+        return _lib.last_launch_count()
+    # angle-sharded: adjoint -> all-reduce (NCCL stream) || forward -> image update
+    n = (eng.geom.side // eng.plan.factors[level0]) ** 2
+    _lib.check(L.imask_step_adjoint(h, cst, level0, s))
+    launches = _lib.last_launch_count()
+    work = _allreduce(eng, state.bp[:n], async_op=True)
+    _lib.check(L.imask_step_forward(h, cst, level0, ctypes.byref(prm), s))
+    launches += _lib.last_launch_count()
+    work.wait()
+    _lib.check(L.imask_step_image(h, cst, level0, ctypes.byref(prm), s))
+    return launches + _lib.last_launch_count()
+
+
+def sketch_step(state: SaddleState, prob: Problem, sigma: float, mu: float) -> SaddleState:
+    """One parallel-update sketched iteration (solvers.py:194-221), on the device."""
+    eng = _require_engine(prob)
+    i = draw_level(state.seed, state.k, prob.cum_probs)
+    _device_step(eng, state, i, _params(sigma, mu, eng.mu_g))
+    state.k += 1
+    state.cost += 2.0 * prob.fractions[i]
+    state.last_level = i + 1
+    if state.k % state.resum_every == 0:
+        _resum(state, prob)
+    return state
+
+
+def psnr(x: torch.Tensor, ref: torch.Tensor, peak: float = 1.0) -> float:
+    """10 log10(peak^2 d / ||x - ref||^2), capped at 300 dB (expcli.py:32-43)."""
+    if peak <= 0:
+        raise ValueError("peak must be positive")
+    diff = (x.double() - ref.double())
+    err = float(torch.dot(diff, diff))
+    if err == 0.0:
+        return 300.0
+    return min(300.0, 10.0 * float(np.log10(peak * peak * x.numel() / err)))
+
+
+def _metrics(x: torch.Tensor, x_ref: Optional[torch.Tensor]):
+    """(rel_dist, psnr) as solvers._metrics (solvers.py:382-390): squared relative distance."""
+    if x_ref is None:
+        return float("nan"), float("nan")
+    diff = x.double() - x_ref.double()
+    ref_sq = float(torch.dot(x_ref.double(), x_ref.double()))
+    rel = float(torch.dot(diff, diff)) / ref_sq if ref_sq > 0 else float("nan")
+    return rel, psnr(x, x_ref, peak=1.0)
+
+
+@dataclass
+class SolveReport:
+    """Recorded metric rows plus the final iterate (solvers.py:345-379)."""
+
+    rows: list
+    x: torch.Tensor
+    y: Optional[torch.Tensor]
+    algorithm: str
+    seed: int
+    snapshots: dict = field(default_factory=dict)
+
+    CSV_HEADER = "k,cost,level,rel_dist,psnr,seconds"
+
+    def to_csv(self, include_timing: bool = False) -> str:
+        lines = [self.CSV_HEADER]
+        for k, cost, level, rel, snr, secs in self.rows:
+            secs_out = secs if include_timing else 0.0
+            lines.append(f"{k},{cost:.12g},{level},{rel:.12g},{snr:.12g},{secs_out:.12g}")
+        return "\n".join(lines) + "\n"
+
+    def write_csv(self, path: str, include_timing: bool = False) -> None:
+        with open(path, "w") as f:
+            f.write(self.to_csv(include_timing=include_timing))
+
+    def costs(self) -> np.ndarray:
+        return np.array([row[1] for row in self.rows])
+
+    def rel_dists(self) -> np.ndarray:
+        return np.array([row[3] for row in self.rows])
+
+
+def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
+        record_every: int = 1, seed: int = 0, x_ref=None, theta_extrap: float = 1.0,
+        resum_every: int = 1000, snapshot_costs: Sequence[float] = ()) -> SolveReport:
+    """Run the sketched solver for ``iters`` iterations, recording metric rows (solvers.py:393-480).
+
+    The level schedule is drawn once up front (it depends only on (seed, k));
+    device work is enqueued without host synchronisation between records.
+    """
+    if algorithm not in ALGORITHMS:
+        raise ValueError(f"unknown algorithm {algorithm!r}; expected one of {ALGORITHMS}")
+    if algorithm != "sketch":
+        raise NotImplementedError(
+            f"{algorithm!r} is a SURVEY 8(f) 'next' row; the B200 path runs 'sketch'"
+        )
+    eng = _require_engine(prob)
+    x_ref_t = None if x_ref is None else to_device(x_ref, eng.device)
+    t0 = time.perf_counter()
+    rows: list = []
+    snapshots: dict = {}
+    budgets = sorted(float(cb) for cb in snapshot_costs)
+    state = init_state(prob, seed=seed, resum_every=resum_every)
+    prm = _params(sigma, mu, eng.mu_g)
+    schedule = draw_levels(seed, 0, iters, prob.cum_probs)
+
+    def record(k, cost, level, x):
+        rel, snr = _metrics(x, x_ref_t)
+        rows.append((k, cost, level, rel, snr, time.perf_counter() - t0))
+
+    record(0, 0.0, 0, state.x)
+    for k in range(1, iters + 1):
+        i = int(schedule[k - 1])
+        _device_step(eng, state, i, prm)
+        state.k += 1
+        state.cost += 2.0 * prob.fractions[i]
+        state.last_level = i + 1
+        if state.k % state.resum_every == 0:
+            _resum(state, prob)
+        while budgets and state.cost >= budgets[0]:
+            snapshots[budgets.pop(0)] = state.x.clone()
+        if k % record_every == 0 or k == iters:
+            record(k, state.cost, state.last_level, state.x)
+    return SolveReport(rows=rows, x=state.x, y=state.y, algorithm=algorithm, seed=seed,
+                       snapshots=snapshots)

@@ -1,0 +1,183 @@
+"""Parity of the fused sketched SAGA iteration (kernel 4 + engine) with the reference.
+
+Budget (north star): the level sequence bit-exact; iterates after a fixed
+iteration count within 1e-3 relative L2 of the reference on the same inputs,
+sigma, mu and seed.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_l2
+from oracle import ct_oracle, solver_oracle as so
+from paper_2412_10249_b200 import ctmodel, linops, mrsketch, proxlib, solvers
+from paper_2412_10249_b200.synth import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.double().cpu().numpy().ravel()
+
+
+def build(side, na, nd, probs, b, mu_g=1e-2, scale=1.0):
+    geom = ctmodel.Geometry(side, na, nd)
+    K = ctmodel.projector_op(geom)
+    coarse = lambda f: ctmodel.coarse_projector(geom, f)
+    if scale != 1.0:
+        K = linops.scale(K, scale)
+        coarse = lambda f, c=coarse: linops.scale(c(f), scale)
+    fam = mrsketch.make_family(len(probs), side, probs, mode="coarse")
+    prob = solvers.make_problem(K, b, fam, proxlib.ridge_fn(mu_g),
+                                proxlib.quadratic_conjugate_fn(b), coarse_projector=coarse)
+    assert prob.engine is not None
+    return prob
+
+
+def test_trajectory_config_A(g_solver_A):
+    cfg = CONFIGS["A"]
+    b = g_solver_A["b"]
+    prob = build(cfg.side, cfg.n_angles, cfg.n_det, [1 / 3] * 3, b, cfg.mu_g)
+    sigma, mu = float(g_solver_A["sigma"]), float(g_solver_A["mu"])
+    st = solvers.init_state(prob, seed=int(g_solver_A["seed"]))
+    levels = []
+    for k in range(1, 201):
+        solvers.sketch_step(st, prob, sigma, mu)
+        levels.append(st.last_level)
+        if k in (18, 200):
+            assert rel_l2(host(st.x), g_solver_A[f"x_{k}"]) <= 1e-3, k
+            assert rel_l2(host(st.y), g_solver_A[f"y_{k}"]) <= 1e-3, k
+            assert rel_l2(host(st.phi_sum), g_solver_A[f"phi_sum_{k}"]) <= 1e-3, k
+            assert rel_l2(host(st.psi_sum), g_solver_A[f"psi_sum_{k}"]) <= 1e-3, k
+            assert st.cost == float(g_solver_A[f"cost_{k}"])
+    assert levels == g_solver_A["levels"].astype(int).tolist()
+
+
+def test_single_steps_tables_vs_oracle():
+    side, na, nd, probs = 64, 90, 91, [0.3, 0.3, 0.2, 0.2]
+    orc = so.SketchedCT(side, na, nd, probs)
+    rng = np.random.default_rng(0)
+    b = orc.proj[1].apply(rng.random(side * side))
+    prob = build(side, na, nd, probs, b)
+    st = solvers.init_state(prob, seed=5)
+    ost = so.init_state(orc, seed=5)
+    fam = prob.family
+    for _ in range(6):
+        solvers.sketch_step(st, prob, 2e-4, 1e-2)
+        so.sketch_step(ost, orc, b, 2e-4, 1e-2, 1e-2)
+        assert st.last_level == ost.last_level
+        i = st.last_level - 1
+        assert rel_l2(host(st.phi_full(i, fam)), ost.phi[i]) <= 1e-4
+        assert rel_l2(host(st.psi[i]), ost.psi[i]) <= 1e-4
+        assert rel_l2(host(st.x), ost.x) <= 1e-4
+        assert rel_l2(host(st.y), ost.y) <= 1e-4
+
+
+def test_resum_matches_direct_sums():
+    side, na, nd, probs = 32, 36, 47, [0.3, 0.3, 0.2, 0.2]
+    orc = so.SketchedCT(side, na, nd, probs)
+    b = orc.proj[1].apply(np.random.default_rng(1).random(side * side))
+    prob = build(side, na, nd, probs, b)
+    st = solvers.init_state(prob, seed=8, resum_every=7)
+    for _ in range(30):
+        solvers.sketch_step(st, prob, 1e-3, 1e-2)
+    direct_phi = sum(probs[i] * st.phi_full(i, prob.family).double() for i in range(4))
+    direct_psi = sum(probs[i] * st.psi[i].double() for i in range(4))
+    assert rel_l2(host(st.phi_sum), host(direct_phi)) <= 1e-5
+    assert rel_l2(host(st.psi_sum), host(direct_psi)) <= 1e-5
+
+
+def test_cost_ledger_and_run_report():
+    side, na, nd, probs = 32, 36, 47, [0.25] * 4
+    orc = so.SketchedCT(side, na, nd, probs)
+    x_true = np.random.default_rng(2).random(side * side)
+    b = orc.proj[1].apply(x_true)
+    prob = build(side, na, nd, probs, b)
+    rep = solvers.run(prob, "sketch", 1e-3, 1e-2, 50, record_every=10, seed=1, x_ref=x_true)
+    assert [row[0] for row in rep.rows] == [0, 10, 20, 30, 40, 50]
+    sched = so.level_schedule(1, 0, 50, probs)
+    expected = 0.0
+    for i in sched:
+        expected += 2.0 * orc.fraction(int(i))
+    assert rep.rows[-1][1] == expected
+    assert rep.rows[-1][2] == int(sched[-1]) + 1
+    ost = so.init_state(orc, seed=1)
+    for _ in range(50):
+        so.sketch_step(ost, orc, b, 1e-3, 1e-2, 1e-2)
+    assert rel_l2(host(rep.x), ost.x) <= 1e-3
+    rel_ref = float(np.dot(ost.x - x_true, ost.x - x_true) / np.dot(x_true, x_true))
+    assert abs(rep.rows[-1][3] - rel_ref) <= 1e-3 * rel_ref
+    assert rep.to_csv().startswith("k,cost,level,rel_dist,psnr,seconds\n0,0,0,")
+
+
+def test_fixed_point_with_exact_memory():
+    """test_solvers.py:121-131 on the device: the saddle point is stationary."""
+    side, na, nd, probs, mu_g = 16, 20, 23, [0.25] * 4, 1.0
+    orc = ct_oracle.ProjectorOracle(side, na, nd)
+    Kd = orc.to_csr().toarray()
+    b = Kd @ np.random.default_rng(3).random(side * side)
+    x_star = np.linalg.solve(Kd.T @ Kd + mu_g * np.eye(side * side), Kd.T @ b)
+    y_star = Kd @ x_star - b
+    prob = build(side, na, nd, probs, b, mu_g=mu_g)
+    st = solvers.init_state(prob, seed=5, x0=x_star, y0=y_star, exact_memory=True)
+    scale_ref = max(np.linalg.norm(x_star), np.linalg.norm(y_star))
+    for _ in range(8):
+        solvers.sketch_step(st, prob, 2e-3, mu_g)
+        assert np.linalg.norm(host(st.x) - x_star) <= 1e-5 * scale_ref
+        assert np.linalg.norm(host(st.y) - y_star) <= 1e-5 * scale_ref
+
+
+def test_normalised_operator_scale():
+    side, na, nd, probs = 32, 36, 47, [1 / 3] * 3
+    alpha = 1.0 / 37.5
+    orc = so.SketchedCT(side, na, nd, probs, scale=alpha)
+    b = orc.proj[1].apply(np.random.default_rng(6).random(side * side))
+    prob = build(side, na, nd, probs, b, scale=alpha)
+    st = solvers.init_state(prob, seed=2)
+    ost = so.init_state(orc, seed=2)
+    for _ in range(20):
+        solvers.sketch_step(st, prob, 0.05, 1e-2)
+        so.sketch_step(ost, orc, b, 0.05, 1e-2, 1e-2)
+    assert rel_l2(host(st.x), ost.x) <= 1e-3
+    assert rel_l2(host(st.y), ost.y) <= 1e-3
+
+
+def test_long_run_config_B_levels_and_iterates():
+    """Config B (r = 4) over 120 iterations at an empirically stable sigma."""
+    cfg = CONFIGS["B"]
+    probs = [0.25] * 4
+    orc = so.SketchedCT(cfg.side, cfg.n_angles, cfg.n_det, probs)
+    from paper_2412_10249_b200.synth import add_gaussian_noise, ellipse_phantom
+
+    x_true = ellipse_phantom(cfg.side, 0).ravel()
+    b = add_gaussian_noise(orc.proj[1].apply(x_true), cfg.kappa, 1)
+    prob = build(cfg.side, cfg.n_angles, cfg.n_det, probs, b, cfg.mu_g)
+    st = solvers.init_state(prob, seed=21)
+    ost = so.init_state(orc, seed=21)
+    for _ in range(120):
+        solvers.sketch_step(st, prob, 1e-5, cfg.mu_g)
+        so.sketch_step(ost, orc, b, 1e-5, cfg.mu_g, cfg.mu_g)
+        assert st.last_level == ost.last_level
+    assert rel_l2(host(st.x), ost.x) <= 1e-3
+    assert rel_l2(host(st.y), ost.y) <= 1e-3
+
+
+def test_rejects_unsupported_problems():
+    geom = ctmodel.Geometry(16, 20, 23)
+    K = ctmodel.projector_op(geom)
+    fam = mrsketch.make_family(2, 16, [0.5, 0.5], mode="exact")
+    b = np.zeros(geom.m)
+    prob = solvers.make_problem(K, b, fam, proxlib.ridge_fn(1.0), proxlib.quadratic_conjugate_fn(b))
+    with pytest.raises(TypeError, match="coarse-mode"):
+        solvers.init_state(prob)
+    fam = mrsketch.make_family(2, 16, [0.5, 0.5], mode="coarse")
+    with pytest.raises(ValueError, match="coarse_projector factory"):
+        solvers.make_problem(K, b, fam, proxlib.ridge_fn(1.0), proxlib.quadratic_conjugate_fn(b))
+    prob = build(16, 20, 23, [0.5, 0.5], b)
+    st = solvers.init_state(prob)
+    with pytest.raises(ValueError, match="sigma and mu_g must be positive"):
+        solvers.sketch_step(st, prob, 0.0, 1.0)
+    with pytest.raises(NotImplementedError):
+        solvers.run(prob, "pdhg", 1e-3, 1.0, 3)
