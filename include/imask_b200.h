@@ -167,6 +167,17 @@ IMASK_API int imask_step_image(imask_plan* plan, const imask_state* st, int leve
  * solvers.py:184-191). */
 IMASK_API int imask_resum(imask_plan* plan, const imask_state* st, void* stream);
 
+/* CUDA graph of one single-GPU iteration at level0 (imask_sketch_step with the
+ * state pointers and scalars baked in), so a run loop issues one launch per
+ * iteration. The graph stays valid while the plan and the state buffers live.
+ * *launches receives the number of kernels one replay executes. */
+typedef struct imask_graph imask_graph;
+IMASK_API int imask_step_graph_create(imask_plan* plan, const imask_state* st, int level0,
+                                      const imask_step_params* prm, imask_graph** out,
+                                      int* launches);
+IMASK_API int imask_graph_launch(imask_graph* graph, void* stream);
+IMASK_API int imask_graph_destroy(imask_graph* graph);
+
 /* Number of kernel launches the last imask_* device call on this thread
  * enqueued (instrumentation for the benchmark's gpu_launches count). */
 IMASK_API int imask_last_launch_count(void);

@@ -95,6 +95,13 @@ SIGNATURES = {
         [_vp, ctypes.POINTER(ImaskState), ctypes.c_int, ctypes.POINTER(ImaskStepParams), _vp],
     ),
     "imask_resum": (ctypes.c_int, [_vp, ctypes.POINTER(ImaskState), _vp]),
+    "imask_step_graph_create": (
+        ctypes.c_int,
+        [_vp, ctypes.POINTER(ImaskState), ctypes.c_int, ctypes.POINTER(ImaskStepParams),
+         ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int)],
+    ),
+    "imask_graph_launch": (ctypes.c_int, [_vp, _vp]),
+    "imask_graph_destroy": (ctypes.c_int, [_vp]),
 }
 
 _lib: Optional[ctypes.CDLL] = None

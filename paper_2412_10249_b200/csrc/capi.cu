@@ -21,8 +21,10 @@ namespace imask {
 cudaError_t launch_forward(const float2* P, const float2* PT, int n, const FwdAngle* ang,
                            int n_loc, int n_det, float* sino, const SinoSaga* saga,
                            cudaStream_t stream);
-cudaError_t launch_adjoint(const float* sino, float* out, int n, int factor, int n_loc,
-                           int n_det, const AdjAngle* ang, cudaStream_t stream);
+cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n, int factor,
+                           int n_loc, int n_det, const AdjAngle* ang, cudaStream_t stream,
+                           int* launches);
+void adjoint_layout(int n, int factor, int n_loc, int* T_out, int* S_out);
 cudaError_t launch_restrict(const float* x, float* u, int side, int f, cudaStream_t s);
 cudaError_t launch_prolong(const float* u, float* x, int side, int f, float alpha,
                            cudaStream_t s);
@@ -36,7 +38,14 @@ cudaError_t launch_saga_image_full(const float* bp, int side, const CompParams& 
 cudaError_t launch_saga_sino(const float* psi_new, size_t m, const SinoSaga& sg, cudaStream_t s);
 cudaError_t launch_resum(const float* phi_tab, float* phi_sum, int side, const float* psi_tab,
                          float* psi_sum, size_t m, const ResumParams& rp, cudaStream_t s);
+void init_kernel_attributes();
 }  // namespace imask
+
+struct imask_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int device = 0;
+};
 
 using namespace imask;
 
@@ -69,6 +78,8 @@ struct imask_plan {
   float2* PT = nullptr;
   float* u = nullptr;
   float* sino_tmp = nullptr;
+  float* adj_partial = nullptr;  // per-split partial backprojections (coarse levels)
+  size_t adj_partial_len = 0;
   int64_t scratch = 0;
   CompParams cp{};
   ResumParams rp{};
@@ -131,6 +142,7 @@ void build_tables(const imask_plan& pl, int f, std::vector<FwdAngle>& fw,
       wmax = h / as;
     }
     F.step = std::llrint(step * kFix);
+    F.inv_step = F.step != 0 ? kFix / (double)F.step : 0.0;
     if (axis) {
       // g = [frac >= 1/2]: the ray on a gridline goes to the upper/right pixel
       F.S = 16777216.0f;   // 2^24
@@ -193,6 +205,32 @@ int get_tables(imask_plan* pl, int f, LevelTables** out) {
   }
   *out = &it->second;
   return IMASK_OK;
+}
+
+int ensure_partial(imask_plan* pl, int f) {
+  int T, S;
+  const int n = pl->side / f;
+  adjoint_layout(n, f, pl->n_loc, &T, &S);
+  const size_t need = S > 1 ? (size_t)S * n * n : 0;
+  if (need > pl->adj_partial_len) {
+    if (pl->adj_partial) cudaFree(pl->adj_partial);
+    pl->adj_partial = nullptr;
+    pl->adj_partial_len = 0;
+    int rc = cuda_check(cudaMalloc(&pl->adj_partial, need * sizeof(float)), "cudaMalloc partial");
+    if (rc) return rc;
+    pl->adj_partial_len = need;
+    pl->scratch += (int64_t)(need * sizeof(float));
+  }
+  return IMASK_OK;
+}
+
+int run_adjoint(imask_plan* pl, int f, const float* sino, float* out, const AdjAngle* ang,
+                cudaStream_t s) {
+  int launches = 0;
+  cudaError_t e = launch_adjoint(sino, out, pl->adj_partial, pl->side / f, f, pl->n_loc, pl->n_det,
+                                 ang, s, &launches);
+  g_launches += launches;
+  return cuda_check(e, "adjoint");
 }
 
 int check_factor(const imask_plan* pl, int f) {
@@ -259,6 +297,7 @@ int imask_plan_create(int side, int n_angles, int n_det, int angle_begin, int an
       return fail(IMASK_EINVAL, "angle with cos = sin = 0");
 
   DeviceGuard g(device);
+  init_kernel_attributes();
   imask_plan* pl = new imask_plan();
   pl->side = side;
   pl->n_angles = n_angles;
@@ -303,7 +342,7 @@ int imask_plan_create(int side, int n_angles, int n_det, int angle_begin, int an
   pl->scratch = (int64_t)(2 * pair_bytes + img_bytes + sino_bytes);
   for (int f : pl->factors) {
     LevelTables* t;
-    if ((rc = get_tables(pl, f, &t))) {
+    if ((rc = get_tables(pl, f, &t)) || (rc = ensure_partial(pl, f))) {
       imask_plan_destroy(pl);
       return rc;
     }
@@ -323,6 +362,7 @@ int imask_plan_destroy(imask_plan* pl) {
   cudaFree(pl->PT);
   cudaFree(pl->u);
   cudaFree(pl->sino_tmp);
+  cudaFree(pl->adj_partial);
   delete pl;
   return IMASK_OK;
 }
@@ -375,8 +415,8 @@ int imask_backproject(imask_plan* pl, int factor, const float* sino, int64_t sin
     LAUNCH(cudaMemsetAsync(u, 0, sizeof(float) * n * n, S(stream)), "memset");
     return IMASK_OK;
   }
-  LAUNCH(launch_adjoint(sino, u, n, factor, pl->n_loc, pl->n_det, t->adj, S(stream)), "adjoint");
-  return IMASK_OK;
+  if ((rc = ensure_partial(pl, factor))) return rc;
+  return run_adjoint(pl, factor, sino, u, t->adj, S(stream));
 }
 
 int imask_restrict(int side, int factor, const float* x, float* u, void* stream) {
@@ -450,7 +490,7 @@ int imask_sketch_adjoint(imask_plan* pl, int level, const float* sino, float* ou
   if (pl->n_loc == 0)
     LAUNCH(cudaMemsetAsync(pl->u, 0, sizeof(float) * n * n, S(stream)), "memset");
   else
-    LAUNCH(launch_adjoint(sino, pl->u, n, f, pl->n_loc, pl->n_det, t->adj, S(stream)), "adjoint");
+    if ((rc = run_adjoint(pl, f, sino, pl->u, t->adj, S(stream)))) return rc;
   if (level < pl->r)
     LAUNCH(launch_prolong(pl->u, out, pl->side, f, 1.0f / (float)(f * f), S(stream)), "prolong");
   else
@@ -490,8 +530,7 @@ int imask_step_adjoint(imask_plan* pl, const imask_state* st, int level0, void* 
   if (pl->n_loc == 0)
     LAUNCH(cudaMemsetAsync(st->bp, 0, sizeof(float) * n * n, S(stream)), "memset");
   else
-    LAUNCH(launch_adjoint(st->y, st->bp, n, f, pl->n_loc, pl->n_det, t->adj, S(stream)),
-           "adjoint");
+    if ((rc = run_adjoint(pl, f, st->y, st->bp, t->adj, S(stream)))) return rc;
   return IMASK_OK;
 }
 
@@ -563,6 +602,54 @@ int imask_sketch_step(imask_plan* pl, const imask_state* st, int level0,
   if ((rc = imask_step_image(pl, st, level0, prm, stream))) return rc;
   total += g_launches;
   g_launches = total;
+  return IMASK_OK;
+}
+
+int imask_step_graph_create(imask_plan* pl, const imask_state* st, int level0,
+                            const imask_step_params* prm, imask_graph** out, int* launches) {
+  g_err.clear();
+  int rc = check_level0(pl, level0);
+  if (rc) return rc;
+  if (!out) return fail(IMASK_EINVAL, "out must not be null");
+  DeviceGuard g(pl->device);
+  cudaStream_t s;
+  if ((rc = cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create")))
+    return rc;
+  imask_graph* gr = new imask_graph();
+  gr->device = pl->device;
+  rc = cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+  int step_rc = IMASK_OK;
+  if (!rc) step_rc = imask_sketch_step(pl, st, level0, prm, s);
+  const int n_launch = g_launches;
+  const std::string step_err = g_err;
+  cudaError_t end = rc ? cudaSuccess : cudaStreamEndCapture(s, &gr->graph);
+  if (!rc && step_rc) rc = fail(step_rc, step_err);
+  if (!rc) rc = cuda_check(end, "end capture");
+  if (!rc) rc = cuda_check(cudaGraphInstantiate(&gr->exec, gr->graph, 0), "graph instantiate");
+  cudaStreamDestroy(s);
+  if (rc) {
+    imask_graph_destroy(gr);
+    return rc;
+  }
+  *out = gr;
+  if (launches) *launches = n_launch;
+  g_launches = 0;
+  return IMASK_OK;
+}
+
+int imask_graph_launch(imask_graph* gr, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (!gr) return fail(IMASK_EINVAL, "null graph");
+  return cuda_check(cudaGraphLaunch(gr->exec, S(stream)), "graph launch");
+}
+
+int imask_graph_destroy(imask_graph* gr) {
+  if (!gr) return IMASK_OK;
+  DeviceGuard g(gr->device);
+  if (gr->exec) cudaGraphExecDestroy(gr->exec);
+  if (gr->graph) cudaGraphDestroy(gr->graph);
+  delete gr;
   return IMASK_OK;
 }
 

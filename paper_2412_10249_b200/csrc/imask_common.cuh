@@ -29,6 +29,7 @@ constexpr double kFix = 4294967296.0;  // 2^32
 struct FwdAngle {
   double xi_base;
   double xi_dj;
+  double inv_step;  // 2^32 / step (0 when step == 0): band-range estimate without division
   long long step;
   float S, B;
   float wsc;       // h / max(|cos|,|sin|) * scale
@@ -40,6 +41,8 @@ struct FwdAngle {
 // eta = X cos + Y sin + (n_det-1)/2 within +-R, a trapezoid of height
 // wsc/scale, plateau half-width |a-b|, support half-width R = a+b
 // (a = |cos|h/2, b = |sin|h/2). eta0 is eta at pixel (0,0) minus R.
+// Inside a CTA tile, positions are Q32.32 fixed point relative to the tile's
+// staged sinogram window (Dc, Ds = per-column / per-row increments).
 struct AdjAngle {
   double eta0;
   double ch, sh;       // cos*h, sin*h

@@ -10,40 +10,34 @@
 // Row-family angles read the row-major pair image, column-family angles the
 // transposed one, so both families read along contiguous memory.
 //
-// Adjoint (pixel-driven gather, no atomics): one thread per 4 pixels of a
-// 32x32 tile, looping over all angles; per angle the pixel's footprint covers
-// nb detector bins whose weights come from the same trapezoid the forward's
-// chords integrate (reference operator: ctmodel.py:73-154).
+// Adjoint (pixel-driven gather, no atomics): see the adjoint section below;
+// per angle a pixel's footprint covers nb detector bins whose weights are the
+// trapezoid the forward's chords integrate (reference operator:
+// ctmodel.py:73-154).
 #include "imask_common.cuh"
 
 namespace imask {
 
-// rows b in [lo, hi) where the ray's left chord partner floor(xi) is in [-1, n-1]
+// bands b in [lo, hi) where the ray's left chord partner floor(xi) is in [-1, n-1]
 __device__ __forceinline__ bool band_ok(long long X0, long long step, int b, int n) {
-  long long X = X0 + (long long)b * step;
+  const long long X = X0 + (long long)b * step;
   return X >= -(1LL << 32) && X < ((long long)n << 32);
 }
 
-__device__ void band_range(long long X0, long long step, int n, int* lo_out, int* hi_out) {
+__device__ __forceinline__ void band_range(long long X0, long long step, double inv_step, int n,
+                                           int* lo_out, int* hi_out) {
   int lo, hi;
   if (step == 0) {
-    bool ok = band_ok(X0, 0, 0, n);
     lo = 0;
-    hi = ok ? n : 0;
+    hi = band_ok(X0, 0, 0, n) ? n : 0;
   } else {
-    double x0 = (double)X0, st = (double)step;
-    double e1 = (-kFix - x0) / st;
-    double e2 = ((double)n * kFix - x0) / st;
-    double elo = fmin(e1, e2), ehi = fmax(e1, e2);
-    elo = fmax(elo, 0.0);
-    ehi = fmin(ehi + 1.0, (double)n);
-    lo = (int)ceil(elo) - 1;
-    if (lo < 0) lo = 0;
-    if (lo > n) lo = n;
-    hi = (int)ehi;
-    if (hi > n) hi = n;
-    if (hi < lo) hi = lo;
-    // exact fix-up (the valid set is an interval)
+    // float64 estimate (no division: inv_step = 2^32/step), then exact integer fix-up
+    const double x0 = (double)X0 * (1.0 / kFix);
+    const double e1 = (-1.0 - x0) * inv_step;
+    const double e2 = ((double)n - x0) * inv_step;
+    const double elo = fmax(fmin(e1, e2), -1.0), ehi = fmin(fmax(e1, e2), (double)n + 1.0);
+    lo = min(max((int)ceil(elo), 0), n);
+    hi = min(max((int)ceil(ehi), lo), n);
     while (lo > 0 && band_ok(X0, step, lo - 1, n)) --lo;
     while (lo < n && !band_ok(X0, step, lo, n)) ++lo;
     if (hi < lo) hi = lo;
@@ -54,6 +48,9 @@ __device__ void band_range(long long X0, long long step, int n, int* lo_out, int
   *hi_out = hi;
 }
 
+// The band offset is folded into the integer word of the Q32.32 position:
+// Y = X + b * pitch * 2^32, so hi(Y) is directly the pair-image index of the
+// left chord partner and one 64-bit add advances both position and band.
 template <bool kSaga>
 __global__ void __launch_bounds__(256)
 k_forward(const float2* __restrict__ P, const float2* __restrict__ PT, int n, int pitch,
@@ -65,26 +62,56 @@ k_forward(const float2* __restrict__ P, const float2* __restrict__ PT, int n, in
   if (a >= n_loc) return;
   const int j = blockIdx.x * 32 + lane;
   const FwdAngle A = ang[a];
-  const float2* __restrict__ img = A.transposed ? PT : P;
+  const float2* __restrict__ img = (A.transposed ? PT : P) + 1;  // index -1 -> slot 0
   float acc = 0.f;
-  if (j < n_det) {
-    const long long X0 = __double2ll_rn(fma((double)j, A.xi_dj, A.xi_base) * kFix);
-    int lo, hi;
-    band_range(X0, A.step, n, &lo, &hi);
-    long long X = X0 + (long long)lo * A.step;
-    const float2* prow = img + (size_t)lo * pitch + 1;
-    const float S = A.S, B = A.B;
-    const long long step = A.step;
-#pragma unroll 4
-    for (int b = lo; b < hi; ++b) {
-      const int c0 = (int)(X >> 32);
-      const float g = __saturatef(fmaf(onep_from_frac((uint32_t)X), S, B));
-      const float2 v = __ldg(prow + c0);
-      acc += v.x;
-      acc = fmaf(g, v.y, acc);
-      X += step;
-      prow += pitch;
+  // Lanes whose detector is past n_det still walk the warp's bands (inactive),
+  // so every load below is issued by the whole warp on one image row.
+  const long long X0 = __double2ll_rn(fma((double)j, A.xi_dj, A.xi_base) * kFix);
+  int lo, hi;
+  band_range(X0, A.step, A.inv_step, n, &lo, &hi);
+  if (j >= n_det) {
+    lo = n;
+    hi = 0;
+  }
+  // the warp walks the union of its lanes' band ranges in lockstep: at every
+  // step all 32 lanes read the same image row (coalesced); lanes outside their
+  // own range are predicated off
+  int wlo = lo, whi = hi;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    wlo = min(wlo, __shfl_xor_sync(0xffffffffu, wlo, o));
+    whi = max(whi, __shfl_xor_sync(0xffffffffu, whi, o));
+  }
+  const long long dY = A.step + ((long long)pitch << 32);
+  long long Y = X0 + (long long)wlo * dY;
+  const float S = A.S, B = A.B;
+  int b = wlo;
+#pragma unroll 1
+  for (; b + 4 <= whi; b += 4) {
+    float2 v[4];
+    float g[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool in = (b + k >= lo) && (b + k < hi);
+      v[k] = in ? __ldg(img + (int)(Y >> 32)) : make_float2(0.f, 0.f);
+      g[k] = __saturatef(fmaf(onep_from_frac((uint32_t)Y), S, B));
+      Y += dY;
     }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      acc += v[k].x;
+      acc = fmaf(g[k], v[k].y, acc);
+    }
+  }
+  for (; b < whi; ++b) {
+    const bool in = (b >= lo) && (b < hi);
+    const float2 v = in ? __ldg(img + (int)(Y >> 32)) : make_float2(0.f, 0.f);
+    const float g = __saturatef(fmaf(onep_from_frac((uint32_t)Y), S, B));
+    acc += v.x;
+    acc = fmaf(g, v.y, acc);
+    Y += dY;
+  }
+  if (j < n_det) {
     acc *= A.wsc;
     const size_t q = (size_t)a * n_det + j;
     if (kSaga) {
@@ -103,90 +130,206 @@ k_forward(const float2* __restrict__ P, const float2* __restrict__ PT, int n, in
   }
 }
 
-constexpr int kAdjChunk = 64;   // angles staged per smem round
-constexpr int kTile = 32;       // pixels per tile side
-constexpr int kRowsPerThread = 4;
+// ---- adjoint -----------------------------------------------------------------
+//
+// Pixel-driven gather, no atomics. A CTA owns a T x T pixel tile and a range of
+// angles (grid.z splits the angles when the level has few tiles; the per-split
+// partial images are then summed in a fixed order by k_adjoint_reduce, so the
+// result is deterministic). For each chunk of angles the CTA stages, per angle,
+// the W-bin window of the sinogram the tile's footprint can touch, pre-scaled
+// by that angle's chord scale. Pixel positions are Q32.32 fixed point whose
+// integer word is the window slot: exact integer increments per column/row,
+// so ties on gridlines (axis-parallel rays, integer detector offsets) are
+// decided exactly, and 1 + frac is one LEA.HI away from the fraction word.
+//
+// With v = eta - R - window base for a pixel, the candidate bins are
+// floor(v)+1 .. floor(v)+nb and bin b has offset u_b = (2 - R + b) - onep,
+// onep = 1 + frac(v); oblique weights are sat(|u| * kneg + Rk) (the trapezoid),
+// axis-parallel angles use v - 2^-32 (ceil rule of the half-open box) and
+// constant weights (kneg = 0, Rk = 1 for the h bins of the box).
+
+constexpr int kAdjThreads = 128;
+constexpr int kAdjPPT = 8;  // pixels per thread (one column of a tile)
 
 struct AdjStage {
-  long long E;  // Q32.32 of (eta - R) at the tile origin, plus 2^32-1 (ceil bias)
+  long long E0;     // Q32.32 of v at the tile origin (minus one ulp for axis angles), integer
+                    // word offset by this angle's window slot base t*W
   long long Dc, Ds;
-  float kneg, Rk, R, wsc;
-  int nb, axis;
+  long long estep;  // Ds * (rows between a thread's pixels)
+  float c0;         // 2 - R
+  float kneg, Rk;   // trapezoid weight: sat(|u| * kneg + Rk)
+  float k1a, k1b;   // factor-1 path: w1 = sat(onep * k1a + k1b)
+  int nb;           // candidate bins per pixel
+  int axis;
+  int jb;           // window slot 0 holds detector bin jb
+  float wsc;
 };
 
-// NB > 0: compile-time bin count (all non-axis angles at factor 1 have 2 bins)
-template <int NB>
-__global__ void __launch_bounds__(256)
-k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int n_loc, int n_det,
-          const AdjAngle* __restrict__ ang) {
-  __shared__ AdjStage st[kAdjChunk];
-  const int x0 = blockIdx.x * kTile, y0 = blockIdx.y * kTile;
-  const int dx = threadIdx.x & 31, dy = threadIdx.x >> 5;  // rows dy + 8k
-  float acc[kRowsPerThread];
-#pragma unroll
-  for (int k = 0; k < kRowsPerThread; ++k) acc[k] = 0.f;
+__device__ __forceinline__ float onep32(uint32_t frac) {
+  return __uint_as_float(0x3F800000u + (frac >> 9));
+}
 
-  for (int a0 = 0; a0 < n_loc; a0 += kAdjChunk) {
-    const int na = min(kAdjChunk, n_loc - a0);
+// kPair: factor-1 path (two bins per pixel, float2 window pairs, T = 32).
+// T: tile side; lanes = T*T/8 threads share one angle, G = 128/lanes angle groups.
+template <bool kPair, int T>
+__global__ void __launch_bounds__(kAdjThreads, 10)
+k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W, int CA,
+          int a_per_split, int n_loc, int n_det, const AdjAngle* __restrict__ ang) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int lanes = T * T / kAdjPPT;
+  constexpr int G = kAdjThreads / lanes;
+  constexpr int dy_step = lanes / T;  // rows between a thread's pixels
+  AdjStage* st = reinterpret_cast<AdjStage*>(smem_raw);
+  float* red = reinterpret_cast<float*>(st + CA);
+  float* win = red + kAdjThreads * kAdjPPT;  // CA x W floats, or CA x W float2 pairs
+  float2* win2 = reinterpret_cast<float2*>(win);
+
+  const int tid = threadIdx.x;
+  const int grp = tid / lanes;
+  const int pix0 = tid % lanes;
+  const int x0 = blockIdx.x * T, y0 = blockIdx.y * T;
+  const int a_lo = blockIdx.z * a_per_split;
+  const int a_hi = min(n_loc, a_lo + a_per_split);
+  const int dx = pix0 % T, dy = pix0 / T;
+  const int warp = tid >> 5, lane = tid & 31;
+  float acc[kAdjPPT];
+#pragma unroll
+  for (int k = 0; k < kAdjPPT; ++k) acc[k] = 0.f;
+
+  for (int a0 = a_lo; a0 < a_hi; a0 += CA) {
+    const int na = min(CA, a_hi - a0);
     __syncthreads();
-    for (int t = threadIdx.x; t < na; t += blockDim.x) {
+    for (int t = tid; t < na; t += kAdjThreads) {
       const AdjAngle A = ang[a0 + t];
+      const double eta = A.eta0 + (double)x0 * A.ch + (double)y0 * A.sh;  // eta - R at origin
+      const double emin = eta + fmin(0.0, (T - 1) * A.ch) + fmin(0.0, (T - 1) * A.sh);
+      const int jb = (int)floor(emin) - 1;
       AdjStage s;
-      const double eta = A.eta0 + (double)x0 * A.ch + (double)y0 * A.sh;
-      s.E = __double2ll_rn(eta * kFix) + 0xFFFFFFFFLL;
+      s.E0 = __double2ll_rn((eta - (double)jb) * kFix) - (A.axis ? 1 : 0) +
+             ((long long)(t * W) << 32);
       s.Dc = A.Dc;
       s.Ds = A.Ds;
-      s.kneg = A.kneg;
-      s.Rk = A.Rk;
-      s.R = A.R;
-      s.wsc = A.wsc;
-      s.nb = A.nb;
+      s.estep = (long long)dy_step * A.Ds;
+      s.c0 = 2.0f - A.R;
       s.axis = A.axis;
+      if (A.axis) {
+        s.kneg = 0.f;
+        s.Rk = 1.f;
+        s.k1a = 0.f;
+        s.k1b = 0.f;  // factor 1: the box holds one bin
+        s.nb = A.nb;
+      } else {
+        s.kneg = A.kneg;
+        s.Rk = A.Rk;
+        // factor 1: u1 = (3 - R) - onep > 0, so w1 = sat(onep * (-kneg) + Rk + kneg * (3 - R))
+        s.k1a = -A.kneg;
+        s.k1b = A.Rk + A.kneg * (3.0f - A.R);
+        s.nb = A.nb;
+      }
+      s.jb = jb + 1;
+      s.wsc = A.wsc;
       st[t] = s;
     }
     __syncthreads();
-    for (int t = 0; t < na; ++t) {
-      const AdjStage s = st[t];
-      const float* __restrict__ yrow = sino + (size_t)(a0 + t) * n_det;
-      long long E = s.E + (long long)dx * s.Dc + (long long)dy * s.Ds;
-      const long long E8 = 8LL * s.Ds;
+    // stage windows (one warp per angle): W bins scaled by wsc, zero outside the detector
+    for (int t = warp; t < na; t += kAdjThreads / 32) {
+      const int jb = st[t].jb;
+      const float wsc = st[t].wsc;
+      const float* yrow = sino + (size_t)(a0 + t) * n_det;
+      for (int k = lane; k < W; k += 32) {
+        const int j = jb + k;
+        const float v0 = (j >= 0 && j < n_det) ? __ldg(yrow + j) * wsc : 0.f;
+        if (kPair) {
+          const float v1 = (j + 1 < n_det && j + 1 >= 0) ? __ldg(yrow + j + 1) * wsc : 0.f;
+          win2[t * W + k] = make_float2(v0, v1);
+        } else {
+          win[t * W + k] = v0;
+        }
+      }
+    }
+    __syncthreads();
+    if (kPair) {
+#pragma unroll 2
+      for (int t = 0; t < na; ++t) {
+        const AdjStage s = st[t];
+        long long e = s.E0 + (long long)dx * s.Dc + (long long)dy * s.Ds;
 #pragma unroll
-      for (int k = 0; k < kRowsPerThread; ++k) {
-        const int lo = (int)(E >> 32);
-        const float onep = onep_from_frac(~(uint32_t)E);  // 1 + (ceil(v) - v)
-        float part = 0.f;
+        for (int k = 0; k < kAdjPPT; ++k) {
+          const float2 pr = win2[(int)(e >> 32)];
+          const float onep = onep32((uint32_t)e);
+          const float w0 = __saturatef(fmaf(fabsf(s.c0 - onep), s.kneg, s.Rk));
+          const float w1 = __saturatef(fmaf(onep, s.k1a, s.k1b));
+          acc[k] = fmaf(w0, pr.x, acc[k]);
+          acc[k] = fmaf(w1, pr.y, acc[k]);
+          e += s.estep;
+        }
+      }
+    } else {
+      for (int t = grp; t < na; t += G) {
+        const AdjStage s = st[t];
+        long long e = s.E0 + (long long)dx * s.Dc + (long long)dy * s.Ds;
         if (s.axis) {
-          // half-open box [eta - h/2, eta + h/2): bins lo .. lo+nb-1, weight h
-          for (int bb = 0; bb < s.nb; ++bb) {
-            const int jj = lo + bb;
-            if (jj >= 0 && jj < n_det) part += __ldg(yrow + jj);
-          }
-        } else if (NB > 0) {
+          // half-open box [eta - h/2, eta + h/2): nb bins of weight 1 from ceil(v)
 #pragma unroll
-          for (int bb = 0; bb < NB; ++bb) {
-            const int jj = lo + bb;
-            const float u = onep + (float)(bb - 1) - s.R;
-            const float w = __saturatef(fmaf(fabsf(u), s.kneg, s.Rk));
-            if (jj >= 0 && jj < n_det) part = fmaf(w, __ldg(yrow + jj), part);
+          for (int k = 0; k < kAdjPPT; ++k) {
+            const float* wp = win + (int)(e >> 32);
+            float part = 0.f;
+            for (int b = 0; b < s.nb; ++b) part += wp[b];
+            acc[k] += part;
+            e += s.estep;
           }
         } else {
-          for (int bb = 0; bb < s.nb; ++bb) {
-            const int jj = lo + bb;
-            const float u = onep + (float)(bb - 1) - s.R;
-            const float w = __saturatef(fmaf(fabsf(u), s.kneg, s.Rk));
-            if (jj >= 0 && jj < n_det) part = fmaf(w, __ldg(yrow + jj), part);
+          // bins outer, pixels inner: eight independent accumulation chains
+          int base[kAdjPPT];
+          float u[kAdjPPT];
+#pragma unroll
+          for (int k = 0; k < kAdjPPT; ++k) {
+            base[k] = (int)(e >> 32);
+            u[k] = s.c0 - onep32((uint32_t)e);
+            e += s.estep;
+          }
+          for (int b = 0; b < s.nb; ++b) {
+#pragma unroll
+            for (int k = 0; k < kAdjPPT; ++k) {
+              acc[k] = fmaf(__saturatef(fmaf(fabsf(u[k]), s.kneg, s.Rk)), win[base[k] + b], acc[k]);
+              u[k] += 1.0f;
+            }
           }
         }
-        acc[k] = fmaf(s.wsc, part, acc[k]);
-        E += E8;
       }
     }
   }
+  float* dst = out + (size_t)blockIdx.z * n * n;  // per-split partial image when gridDim.z > 1
+  if (G > 1) {
+    // fixed-order sum over the angle groups
+    __syncthreads();
 #pragma unroll
-  for (int k = 0; k < kRowsPerThread; ++k) {
-    const int row = y0 + dy + 8 * k, col = x0 + dx;
-    if (row < n && col < n) out[(size_t)row * n + col] = acc[k];
+    for (int k = 0; k < kAdjPPT; ++k) red[(grp * kAdjPPT + k) * lanes + pix0] = acc[k];
+    __syncthreads();
+    for (int q = tid; q < lanes * kAdjPPT; q += kAdjThreads) {
+      const int k = q / lanes, p = q % lanes;
+      float v = 0.f;
+      for (int g = 0; g < G; ++g) v += red[(g * kAdjPPT + k) * lanes + p];
+      const int row = y0 + p / T + k * dy_step, col = x0 + p % T;
+      if (row < n && col < n) dst[(size_t)row * n + col] = v;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kAdjPPT; ++k) {
+      const int row = y0 + dy + k * dy_step, col = x0 + dx;
+      if (row < n && col < n) dst[(size_t)row * n + col] = acc[k];
+    }
   }
+}
+
+// Sum of the per-split partial images in split order (deterministic).
+__global__ void k_adjoint_reduce(const float* __restrict__ part, float* __restrict__ out,
+                                 int npix, int S) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npix) return;
+  float v = 0.f;
+  for (int s = 0; s < S; ++s) v += __ldg(part + (size_t)s * npix + p);
+  out[p] = v;
 }
 
 // ---- launchers ----------------------------------------------------------
@@ -204,13 +347,70 @@ cudaError_t launch_forward(const float2* P, const float2* PT, int n, const FwdAn
   return cudaGetLastError();
 }
 
-cudaError_t launch_adjoint(const float* sino, float* out, int n, int factor, int n_loc,
-                           int n_det, const AdjAngle* ang, cudaStream_t stream) {
-  dim3 grid((n + kTile - 1) / kTile, (n + kTile - 1) / kTile);
-  if (factor == 1) {
-    k_adjoint<2><<<grid, 256, 0, stream>>>(sino, out, n, n_loc, n_det, ang);
-  } else {
-    k_adjoint<0><<<grid, 256, 0, stream>>>(sino, out, n, n_loc, n_det, ang);
+// Opt-in shared memory beyond 48 KB (called once per device at plan creation,
+// outside any stream capture).
+void init_kernel_attributes() {
+  cudaFuncSetAttribute(k_adjoint<true, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_adjoint<false, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_adjoint<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_adjoint<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
+// Tile / split choice of the adjoint at one level (shared with the plan's
+// scratch sizing): T = 32 at factors 1-2, 16 at factor 4, else 8; T shrinks
+// to the next power of two >= n (>= 8) for small images. Enough angle splits
+// that the grid has ~4 CTAs per SM.
+void adjoint_layout(int n, int factor, int n_loc, int* T_out, int* S_out) {
+  int T = factor <= 2 ? 32 : (factor == 4 ? 16 : 8);
+  int np2 = 8;
+  while (np2 < n) np2 <<= 1;
+  if (T > np2) T = np2;
+  const int tiles = ((n + T - 1) / T) * ((n + T - 1) / T);
+  int S = 1;
+  if (factor > 1) {
+    const int target = 16 * 148;
+    S = (target + tiles - 1) / tiles;
+    const int max_s = n_loc / 8 > 1 ? n_loc / 8 : 1;
+    if (S > max_s) S = max_s;
+    if (S < 1) S = 1;
+  }
+  *T_out = T;
+  *S_out = S;
+}
+
+cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n, int factor,
+                           int n_loc, int n_det, const AdjAngle* ang, cudaStream_t stream,
+                           int* launches) {
+  int T, S;
+  adjoint_layout(n, factor, n_loc, &T, &S);
+  const bool pair = (factor == 1 && T == 32);
+  const int W = (int)floor(1.41422 * T * factor) + 6;
+  const int lanes = T * T / kAdjPPT;
+  const int G = kAdjThreads / lanes;
+  const int per_split = (n_loc + S - 1) / S;
+  int CA = G > 32 ? G : 32;
+  const size_t elem = pair ? sizeof(float2) : sizeof(float);
+  while (CA > G && (size_t)CA * W * elem > 100 * 1024) CA >>= 1;
+  const size_t smem = (size_t)CA * sizeof(AdjStage) + kAdjThreads * kAdjPPT * sizeof(float) +
+                      (size_t)CA * W * elem;
+  dim3 grid((n + T - 1) / T, (n + T - 1) / T, S);
+  float* dst = S > 1 ? partial : out;
+#define ADJ_LAUNCH(P_, T_)                                                                   \
+  k_adjoint<P_, T_><<<grid, kAdjThreads, smem, stream>>>(sino, dst, n, W, CA, per_split, n_loc, \
+                                                         n_det, ang)
+  if (pair)
+    ADJ_LAUNCH(true, 32);
+  else if (T == 32)
+    ADJ_LAUNCH(false, 32);
+  else if (T == 16)
+    ADJ_LAUNCH(false, 16);
+  else
+    ADJ_LAUNCH(false, 8);
+#undef ADJ_LAUNCH
+  *launches = 1;
+  if (S > 1) {
+    k_adjoint_reduce<<<(n * n + 255) / 256, 256, 0, stream>>>(partial, out, n * n, S);
+    *launches = 2;
   }
   return cudaGetLastError();
 }

@@ -87,6 +87,32 @@ class Engine:
         self.b = b
         self.m_loc = self.plan.m_loc
         self.d = geom.side * geom.side
+        self._graphs: dict = {}  # (state id, level, sigma, mu) -> (graph handle, launches)
+        self.use_graphs = True
+
+    def graph(self, state: "SaddleState", level0: int, prm) -> tuple:
+        key = (id(state), level0, prm.sigma, prm.mu)
+        hit = self._graphs.get(key)
+        if hit is None:
+            h = ctypes.c_void_p()
+            n = ctypes.c_int(0)
+            _lib.check(_lib.lib().imask_step_graph_create(
+                self.plan.handle, ctypes.byref(state.c_state(self.b)), level0, ctypes.byref(prm),
+                ctypes.byref(h), ctypes.byref(n)))
+            hit = (h, n.value, state)  # keep the state alive while its graph exists
+            self._graphs[key] = hit
+        return hit
+
+    def release_graphs(self, state: Optional["SaddleState"] = None) -> None:
+        for key in list(self._graphs):
+            if state is None or key[0] == id(state):
+                _lib.lib().imask_graph_destroy(self._graphs.pop(key)[0])
+
+    def __del__(self):
+        try:
+            self.release_graphs()
+        except Exception:
+            pass
 
 
 @dataclass(frozen=True)
@@ -269,8 +295,12 @@ def _params(sigma: float, mu: float, mu_g: float) -> _lib.ImaskStepParams:
 def _device_step(eng: Engine, state: SaddleState, level0: int, prm: _lib.ImaskStepParams) -> int:
     """Enqueue one iteration; returns the number of kernels launched."""
     L = _lib.lib()
-    cst = ctypes.byref(state.c_state(eng.b))
     h, s = eng.plan.handle, eng.plan.stream
+    if eng.shard.world == 1 and eng.use_graphs:
+        g, launches, _ = eng.graph(state, level0, prm)
+        _lib.check(L.imask_graph_launch(g, s))
+        return launches
+    cst = ctypes.byref(state.c_state(eng.b))
     if eng.shard.world == 1:
         _lib.check(L.imask_sketch_step(h, cst, level0, ctypes.byref(prm), s))
         return _lib.last_launch_count()
@@ -392,5 +422,6 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
             snapshots[budgets.pop(0)] = state.x.clone()
         if k % record_every == 0 or k == iters:
             record(k, state.cost, state.last_level, state.x)
+    eng.release_graphs(state)
     return SolveReport(rows=rows, x=state.x, y=state.y, algorithm=algorithm, seed=seed,
                        snapshots=snapshots)
