@@ -327,7 +327,7 @@ int imask_plan_create(int side, int n_angles, int n_det, int angle_begin, int an
   }
   pl->cp.pr = (float)probs[r - 1];
 
-  const size_t pair_bytes = sizeof(float2) * (size_t)side * (side + 1);
+  const size_t pair_bytes = sizeof(float2) * (size_t)side * pair_pitch(side);
   const size_t img_bytes = sizeof(float) * (size_t)side * side;
   const size_t sino_bytes = sizeof(float) * (size_t)n_loc * n_det;
   int rc = IMASK_OK;

@@ -20,6 +20,14 @@ namespace imask {
 
 constexpr double kFix = 4294967296.0;  // 2^32
 
+// Zero columns on each side of every pair-image row (see k_forward): a lane
+// walking its warp's band range outside its own valid range is at most
+// 31*sqrt(2) < 48 columns from a lane inside it, so it reads zeros instead of
+// needing a predicate. Column c in [-1-kPadC, n-1+kPadC] is stored at index
+// c + 1 + kPadC of a row of pitch n + 2*kPadC + 1.
+constexpr int kPadC = 48;
+__host__ __device__ inline int pair_pitch(int n) { return n + 2 * kPadC + 1; }
+
 // Forward projector, one entry per (level factor, local angle).
 // A ray crosses `n` bands (pixel rows, or columns when |sin| > |cos|); at
 // band b its band coordinate is xi = xi_base + j*xi_dj + b*(step/2^32), in
@@ -53,6 +61,20 @@ struct AdjAngle {
   int nb;              // candidate bins per pixel
   int axis;            // 1: axis-parallel half-open box rule
 };
+
+// Q32.32 position held as two 32-bit words; one add-with-carry pair advances it
+// and the integer word is used directly as an index (no 64-bit shifts).
+struct Fix32 {
+  uint32_t lo, hi;
+};
+__device__ __forceinline__ Fix32 fix_from(long long v) {
+  return Fix32{(uint32_t)(unsigned long long)v, (uint32_t)((unsigned long long)v >> 32)};
+}
+__device__ __forceinline__ void fix_add(Fix32& a, const Fix32& d) {
+  asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;"
+      : "+r"(a.lo), "+r"(a.hi)
+      : "r"(d.lo), "r"(d.hi));
+}
 
 // 1 + (top 23 bits of a Q0.32 fraction) as a float in [1, 2)
 __device__ __forceinline__ float onep_from_frac(uint32_t frac) {

@@ -62,28 +62,26 @@ k_forward(const float2* __restrict__ P, const float2* __restrict__ PT, int n, in
   if (a >= n_loc) return;
   const int j = blockIdx.x * 32 + lane;
   const FwdAngle A = ang[a];
-  const float2* __restrict__ img = (A.transposed ? PT : P) + 1;  // index -1 -> slot 0
+  const float2* __restrict__ img = A.transposed ? PT : P;
   float acc = 0.f;
-  // Lanes whose detector is past n_det still walk the warp's bands (inactive),
-  // so every load below is issued by the whole warp on one image row.
-  const long long X0 = __double2ll_rn(fma((double)j, A.xi_dj, A.xi_base) * kFix);
+  // lanes past n_det trace the last detector's ray (result discarded)
+  const int jr = min(j, n_det - 1);
+  const long long X0 = __double2ll_rn(fma((double)jr, A.xi_dj, A.xi_base) * kFix);
   int lo, hi;
   band_range(X0, A.step, A.inv_step, n, &lo, &hi);
-  if (j >= n_det) {
-    lo = n;
-    hi = 0;
-  }
-  // the warp walks the union of its lanes' band ranges in lockstep: at every
-  // step all 32 lanes read the same image row (coalesced); lanes outside their
-  // own range are predicated off
-  int wlo = lo, whi = hi;
+  // the warp walks the union of its lanes' band ranges in lockstep, so every
+  // load instruction reads one image row (coalesced); a lane outside its own
+  // range reads the zero padding of the row (kPadC), so no predicate is needed
+  int wlo = lo < hi ? lo : n, whi = lo < hi ? hi : 0;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     wlo = min(wlo, __shfl_xor_sync(0xffffffffu, wlo, o));
     whi = max(whi, __shfl_xor_sync(0xffffffffu, whi, o));
   }
-  const long long dY = A.step + ((long long)pitch << 32);
-  long long Y = X0 + (long long)wlo * dY;
+  // Y = X + (band * pitch + 1 + kPadC) * 2^32: hi(Y) is the pair-image index
+  const long long dYl = A.step + ((long long)pitch << 32);
+  Fix32 Y = fix_from(X0 + (long long)wlo * dYl + ((long long)(1 + kPadC) << 32));
+  const Fix32 dY = fix_from(dYl);
   const float S = A.S, B = A.B;
   int b = wlo;
 #pragma unroll 1
@@ -92,10 +90,9 @@ k_forward(const float2* __restrict__ P, const float2* __restrict__ PT, int n, in
     float g[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const bool in = (b + k >= lo) && (b + k < hi);
-      v[k] = in ? __ldg(img + (int)(Y >> 32)) : make_float2(0.f, 0.f);
-      g[k] = __saturatef(fmaf(onep_from_frac((uint32_t)Y), S, B));
-      Y += dY;
+      v[k] = __ldg(img + Y.hi);
+      g[k] = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
+      fix_add(Y, dY);
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -104,12 +101,11 @@ k_forward(const float2* __restrict__ P, const float2* __restrict__ PT, int n, in
     }
   }
   for (; b < whi; ++b) {
-    const bool in = (b >= lo) && (b < hi);
-    const float2 v = in ? __ldg(img + (int)(Y >> 32)) : make_float2(0.f, 0.f);
-    const float g = __saturatef(fmaf(onep_from_frac((uint32_t)Y), S, B));
+    const float2 v = __ldg(img + Y.hi);
+    const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
     acc += v.x;
     acc = fmaf(g, v.y, acc);
-    Y += dY;
+    fix_add(Y, dY);
   }
   if (j < n_det) {
     acc *= A.wsc;
@@ -252,31 +248,33 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
 #pragma unroll 2
       for (int t = 0; t < na; ++t) {
         const AdjStage s = st[t];
-        long long e = s.E0 + (long long)dx * s.Dc + (long long)dy * s.Ds;
+        Fix32 e = fix_from(s.E0 + (long long)dx * s.Dc + (long long)dy * s.Ds);
+        const Fix32 estep = fix_from(s.estep);
 #pragma unroll
         for (int k = 0; k < kAdjPPT; ++k) {
-          const float2 pr = win2[(int)(e >> 32)];
-          const float onep = onep32((uint32_t)e);
+          const float2 pr = win2[e.hi];
+          const float onep = onep32(e.lo);
           const float w0 = __saturatef(fmaf(fabsf(s.c0 - onep), s.kneg, s.Rk));
           const float w1 = __saturatef(fmaf(onep, s.k1a, s.k1b));
           acc[k] = fmaf(w0, pr.x, acc[k]);
           acc[k] = fmaf(w1, pr.y, acc[k]);
-          e += s.estep;
+          fix_add(e, estep);
         }
       }
     } else {
       for (int t = grp; t < na; t += G) {
         const AdjStage s = st[t];
-        long long e = s.E0 + (long long)dx * s.Dc + (long long)dy * s.Ds;
+        Fix32 e = fix_from(s.E0 + (long long)dx * s.Dc + (long long)dy * s.Ds);
+        const Fix32 estep = fix_from(s.estep);
         if (s.axis) {
           // half-open box [eta - h/2, eta + h/2): nb bins of weight 1 from ceil(v)
 #pragma unroll
           for (int k = 0; k < kAdjPPT; ++k) {
-            const float* wp = win + (int)(e >> 32);
+            const float* wp = win + e.hi;
             float part = 0.f;
             for (int b = 0; b < s.nb; ++b) part += wp[b];
             acc[k] += part;
-            e += s.estep;
+            fix_add(e, estep);
           }
         } else {
           // bins outer, pixels inner: eight independent accumulation chains
@@ -284,9 +282,9 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
           float u[kAdjPPT];
 #pragma unroll
           for (int k = 0; k < kAdjPPT; ++k) {
-            base[k] = (int)(e >> 32);
-            u[k] = s.c0 - onep32((uint32_t)e);
-            e += s.estep;
+            base[k] = (int)e.hi;
+            u[k] = s.c0 - onep32(e.lo);
+            fix_add(e, estep);
           }
           for (int b = 0; b < s.nb; ++b) {
 #pragma unroll
@@ -339,10 +337,12 @@ cudaError_t launch_forward(const float2* P, const float2* PT, int n, const FwdAn
                            cudaStream_t stream) {
   dim3 grid((n_det + 31) / 32, (n_loc + 7) / 8);
   if (saga) {
-    k_forward<true><<<grid, 256, 0, stream>>>(P, PT, n, n + 1, ang, n_loc, n_det, nullptr, *saga);
+    k_forward<true><<<grid, 256, 0, stream>>>(P, PT, n, pair_pitch(n), ang, n_loc, n_det, nullptr,
+                                              *saga);
   } else {
     SinoSaga none{};
-    k_forward<false><<<grid, 256, 0, stream>>>(P, PT, n, n + 1, ang, n_loc, n_det, sino, none);
+    k_forward<false><<<grid, 256, 0, stream>>>(P, PT, n, pair_pitch(n), ang, n_loc, n_det, sino,
+                                               none);
   }
   return cudaGetLastError();
 }

@@ -82,34 +82,41 @@ k_compensate(const float* __restrict__ x, float* __restrict__ out, int side, Com
 
 // ---- projector staging ------------------------------------------------------
 
-// One 32x32 block of u per CTA: writes P rows [r0,r0+32) entries c+1 for
-// c in [c0, c0+32), PT rows [c0,c0+32) entries r+1 for r in [r0, r0+32);
-// the c = -1 / r = -1 entries come from the blocks at c0 = 0 / r0 = 0.
+// Pair layouts of the n x n image u for the forward projector, rows padded by
+// kPadC zero columns on each side (imask_common.cuh):
+//   P [R][c + 1 + kPadC]  = (u[R][c], u[R][c+1] - u[R][c])   c in [-1-kPadC, n-1+kPadC]
+//   PT[C][r + 1 + kPadC]  = (u[r][C], u[r+1][C] - u[r][C])   r in [-1-kPadC, n-1+kPadC]
+// with u = 0 outside the image. The grid tiles the padded index range in both
+// dimensions; each 32x32 tile (plus a one-element halo) is staged in shared
+// memory so both the row-major and the transposed writes are coalesced.
 __global__ void __launch_bounds__(256)
 k_prepare(const float* __restrict__ u, int n, float2* __restrict__ P, float2* __restrict__ PT) {
   __shared__ float t[33][34];
-  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-  const int pitch = n + 1;
+  const int pitch = pair_pitch(n);
+  const int r0 = blockIdx.y * 32 - 1 - kPadC, c0 = blockIdx.x * 32 - 1 - kPadC;
   for (int e = threadIdx.x; e < 33 * 33; e += blockDim.x) {
     const int rr = e / 33, cc = e % 33;
     const int R = r0 + rr, C = c0 + cc;
-    t[rr][cc] = (R < n && C < n) ? __ldg(u + (size_t)R * n + C) : 0.f;
+    t[rr][cc] = (R >= 0 && R < n && C >= 0 && C < n) ? __ldg(u + (size_t)R * n + C) : 0.f;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
     const int rr = e / 32, cc = e % 32;
-    const int R = r0 + rr, C = c0 + cc;
-    if (R < n && C < n) {
-      const float v = t[rr][cc];
-      P[(size_t)R * pitch + C + 1] = make_float2(v, t[rr][cc + 1] - v);
-      if (C == 0) P[(size_t)R * pitch] = make_float2(0.f, v);
+    // row-major pairs: real rows, padded column index
+    {
+      const int R = r0 + rr, idx = c0 + cc + 1 + kPadC;
+      if (R >= 0 && R < n && idx < pitch) {
+        const float v = t[rr][cc];
+        P[(size_t)R * pitch + idx] = make_float2(v, t[rr][cc + 1] - v);
+      }
     }
-    // transpose: consecutive threads walk rows of u (= entries of a PT row)
-    const int Rt = r0 + cc, Ct = c0 + rr;
-    if (Rt < n && Ct < n) {
-      const float v = t[cc][rr];
-      PT[(size_t)Ct * pitch + Rt + 1] = make_float2(v, t[cc + 1][rr] - v);
-      if (Rt == 0) PT[(size_t)Ct * pitch] = make_float2(0.f, v);
+    // transposed pairs: real columns, padded row index (consecutive threads walk rows of u)
+    {
+      const int C = c0 + rr, idx = r0 + cc + 1 + kPadC;
+      if (C >= 0 && C < n && idx < pitch) {
+        const float v = t[cc][rr];
+        PT[(size_t)C * pitch + idx] = make_float2(v, t[cc + 1][rr] - v);
+      }
     }
   }
 }
@@ -246,7 +253,8 @@ cudaError_t launch_compensate(const float* x, float* out, int side, const CompPa
 }
 
 cudaError_t launch_prepare(const float* u, int n, float2* P, float2* PT, cudaStream_t s) {
-  dim3 grid((n + 31) / 32, (n + 31) / 32);
+  const int tiles = (pair_pitch(n) + 31) / 32;
+  dim3 grid(tiles, tiles);
   k_prepare<<<grid, 256, 0, s>>>(u, n, P, PT);
   return cudaGetLastError();
 }
