@@ -367,8 +367,8 @@ void adjoint_layout(int n, int factor, int n_loc, int* T_out, int* S_out) {
   if (T > np2) T = np2;
   const int tiles = ((n + T - 1) / T) * ((n + T - 1) / T);
   int S = 1;
-  if (factor > 1) {
-    const int target = 16 * 148;
+  {
+    const int target = (factor == 1 ? 20 : 16) * 148;
     S = (target + tiles - 1) / tiles;
     const int max_s = n_loc / 8 > 1 ? n_loc / 8 : 1;
     if (S > max_s) S = max_s;
