@@ -18,19 +18,22 @@
 #include "sketch.cuh"
 
 namespace imask {
-cudaError_t launch_forward(const float2* P, const float2* PT, int n, const FwdAngle* ang,
-                           int n_loc, int n_det, float* sino, const SinoSaga* saga,
-                           cudaStream_t stream);
+cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, const float2* PTM,
+                           int n, const FwdAngle* ang, int n_loc, int n_det,
+                           const int2* sym_entries, int n_entries, float* sino,
+                           const SinoSaga* saga, cudaStream_t stream);
 cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n, int factor,
-                           int n_loc, int n_det, const AdjAngle* ang, cudaStream_t stream,
-                           int* launches);
-void adjoint_layout(int n, int factor, int n_loc, int* T_out, int* S_out);
+                           int n_loc, int n_det, const AdjAngle* ang, bool full_even_set,
+                           cudaStream_t stream, int* launches);
+int adjoint_planes(int n, int factor, int n_loc, bool sym);
+bool adjoint_sym_ok(int n, int factor, int n_loc, bool full_even_set);
 cudaError_t launch_restrict(const float* x, float* u, int side, int f, cudaStream_t s);
 cudaError_t launch_prolong(const float* u, float* x, int side, int f, float alpha,
                            cudaStream_t s);
 cudaError_t launch_compensate(const float* x, float* out, int side, const CompParams& cp,
                               cudaStream_t s);
-cudaError_t launch_prepare(const float* u, int n, float2* P, float2* PT, cudaStream_t s);
+cudaError_t launch_prepare(const float* u, int n, float2* P, float2* PT, float2* PM,
+                           float2* PTM, cudaStream_t s);
 cudaError_t launch_saga_image_coarse(const float* bp, int side, int f, const ImageSaga& sg,
                                      cudaStream_t s);
 cudaError_t launch_saga_image_full(const float* bp, int side, const CompParams& cp,
@@ -76,6 +79,11 @@ struct imask_plan {
   std::mutex mu;
   float2* P = nullptr;
   float2* PT = nullptr;
+  float2* PM = nullptr;   // mirrored pair images (mirror-symmetric forward)
+  float2* PTM = nullptr;
+  bool sym = false;       // whole, even-sized angle set: mirror-symmetric kernels
+  int2* fwd_entries = nullptr;  // (angle, mirror angle or -1) per forward warp
+  int n_entries = 0;
   float* u = nullptr;
   float* sino_tmp = nullptr;
   float* adj_partial = nullptr;  // per-split partial backprojections (coarse levels)
@@ -208,10 +216,9 @@ int get_tables(imask_plan* pl, int f, LevelTables** out) {
 }
 
 int ensure_partial(imask_plan* pl, int f) {
-  int T, S;
   const int n = pl->side / f;
-  adjoint_layout(n, f, pl->n_loc, &T, &S);
-  const size_t need = S > 1 ? (size_t)S * n * n : 0;
+  const bool sym = adjoint_sym_ok(n, f, pl->n_loc, pl->sym);
+  const size_t need = (size_t)adjoint_planes(n, f, pl->n_loc, sym) * n * n;
   if (need > pl->adj_partial_len) {
     if (pl->adj_partial) cudaFree(pl->adj_partial);
     pl->adj_partial = nullptr;
@@ -228,7 +235,7 @@ int run_adjoint(imask_plan* pl, int f, const float* sino, float* out, const AdjA
                 cudaStream_t s) {
   int launches = 0;
   cudaError_t e = launch_adjoint(sino, out, pl->adj_partial, pl->side / f, f, pl->n_loc, pl->n_det,
-                                 ang, s, &launches);
+                                 ang, pl->sym, s, &launches);
   g_launches += launches;
   return cuda_check(e, "adjoint");
 }
@@ -331,15 +338,32 @@ int imask_plan_create(int side, int n_angles, int n_det, int angle_begin, int an
   const size_t img_bytes = sizeof(float) * (size_t)side * side;
   const size_t sino_bytes = sizeof(float) * (size_t)n_loc * n_det;
   int rc = IMASK_OK;
+  pl->sym = (angle_begin == 0 && angle_end == n_angles && n_angles % 2 == 0 && n_angles >= 4);
+  if (pl->sym) {
+    std::vector<int2> ent;
+    for (int a = 1; a < n_angles / 2; ++a) ent.push_back(make_int2(a, n_angles - a));
+    ent.push_back(make_int2(0, -1));             // tie rule not mirror-invariant
+    ent.push_back(make_int2(n_angles / 2, -1));  // self-mirrored
+    pl->n_entries = (int)ent.size();
+    if ((rc = cuda_check(cudaMalloc(&pl->fwd_entries, sizeof(int2) * ent.size()), "cudaMalloc")) ||
+        (rc = cuda_check(cudaMemcpy(pl->fwd_entries, ent.data(), sizeof(int2) * ent.size(),
+                                    cudaMemcpyHostToDevice),
+                         "cudaMemcpy"))) {
+      imask_plan_destroy(pl);
+      return rc;
+    }
+  }
   if ((rc = cuda_check(cudaMalloc(&pl->P, pair_bytes), "cudaMalloc P")) ||
       (rc = cuda_check(cudaMalloc(&pl->PT, pair_bytes), "cudaMalloc PT")) ||
+      (pl->sym && (rc = cuda_check(cudaMalloc(&pl->PM, pair_bytes), "cudaMalloc PM"))) ||
+      (pl->sym && (rc = cuda_check(cudaMalloc(&pl->PTM, pair_bytes), "cudaMalloc PTM"))) ||
       (rc = cuda_check(cudaMalloc(&pl->u, img_bytes), "cudaMalloc u")) ||
       (rc = cuda_check(cudaMalloc(&pl->sino_tmp, sino_bytes > 0 ? sino_bytes : 4),
                        "cudaMalloc sino"))) {
     imask_plan_destroy(pl);
     return rc;
   }
-  pl->scratch = (int64_t)(2 * pair_bytes + img_bytes + sino_bytes);
+  pl->scratch = (int64_t)((pl->sym ? 4 : 2) * pair_bytes + img_bytes + sino_bytes);
   for (int f : pl->factors) {
     LevelTables* t;
     if ((rc = get_tables(pl, f, &t)) || (rc = ensure_partial(pl, f))) {
@@ -360,6 +384,9 @@ int imask_plan_destroy(imask_plan* pl) {
   }
   cudaFree(pl->P);
   cudaFree(pl->PT);
+  cudaFree(pl->PM);
+  cudaFree(pl->PTM);
+  cudaFree(pl->fwd_entries);
   cudaFree(pl->u);
   cudaFree(pl->sino_tmp);
   cudaFree(pl->adj_partial);
@@ -387,8 +414,9 @@ int imask_project(imask_plan* pl, int factor, const float* u, int64_t u_len, flo
   LevelTables* t;
   if ((rc = get_tables(pl, factor, &t))) return rc;
   if (pl->n_loc == 0) return IMASK_OK;
-  LAUNCH(launch_prepare(u, n, pl->P, pl->PT, S(stream)), "prepare");
-  LAUNCH(launch_forward(pl->P, pl->PT, n, t->fwd, pl->n_loc, pl->n_det, sino, nullptr, S(stream)),
+  LAUNCH(launch_prepare(u, n, pl->P, pl->PT, pl->PM, pl->PTM, S(stream)), "prepare");
+  LAUNCH(launch_forward(pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->n_loc, pl->n_det,
+                        pl->fwd_entries, pl->n_entries, sino, nullptr, S(stream)),
          "forward");
   return IMASK_OK;
 }
@@ -470,8 +498,9 @@ int imask_sketch_forward(imask_plan* pl, int level, const float* x, float* sino,
   else
     LAUNCH(launch_compensate(x, pl->u, pl->side, pl->cp, S(stream)), "compensate");
   if (pl->n_loc == 0) return IMASK_OK;
-  LAUNCH(launch_prepare(pl->u, n, pl->P, pl->PT, S(stream)), "prepare");
-  LAUNCH(launch_forward(pl->P, pl->PT, n, t->fwd, pl->n_loc, pl->n_det, sino, nullptr, S(stream)),
+  LAUNCH(launch_prepare(pl->u, n, pl->P, pl->PT, pl->PM, pl->PTM, S(stream)), "prepare");
+  LAUNCH(launch_forward(pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->n_loc, pl->n_det,
+                        pl->fwd_entries, pl->n_entries, sino, nullptr, S(stream)),
          "forward");
   return IMASK_OK;
 }
@@ -551,7 +580,7 @@ int imask_step_forward(imask_plan* pl, const imask_state* st, int level0,
   else
     LAUNCH(launch_compensate(st->x, pl->u, pl->side, pl->cp, S(stream)), "compensate");
   if (pl->n_loc == 0) return IMASK_OK;
-  LAUNCH(launch_prepare(pl->u, n, pl->P, pl->PT, S(stream)), "prepare");
+  LAUNCH(launch_prepare(pl->u, n, pl->P, pl->PT, pl->PM, pl->PTM, S(stream)), "prepare");
   const size_t m = (size_t)pl->n_loc * pl->n_det;
   SinoSaga sg;
   sg.psi_tab = st->psi_tab + (size_t)level0 * m;
@@ -561,7 +590,8 @@ int imask_step_forward(imask_plan* pl, const imask_state* st, int level0,
   sg.p_i = (float)pl->probs[level0];
   sg.sigma = (float)prm->sigma;
   sg.inv_1ps = (float)(1.0 / (1.0 + prm->sigma));
-  LAUNCH(launch_forward(pl->P, pl->PT, n, t->fwd, pl->n_loc, pl->n_det, nullptr, &sg, S(stream)),
+  LAUNCH(launch_forward(pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->n_loc, pl->n_det,
+                        pl->fwd_entries, pl->n_entries, nullptr, &sg, S(stream)),
          "forward+saga");
   return IMASK_OK;
 }

@@ -126,6 +126,107 @@ k_forward(const float2* __restrict__ P, const float2* __restrict__ PT, int n, in
   }
 }
 
+// Mirror-symmetric forward (full, even-sized angle set): ray (a, j) and ray
+// (n-a, j) are mirror images (theta -> pi-theta, x -> -x), so one warp walks
+// both with the same fixed-point position: band b of the mirrored ray reads
+// the mirrored pair image (PM: rows reversed left-right; PTM: PT with its
+// bands reversed) at the same index. entries[e] = (a, mirror angle or -1);
+// angle 0 is traced alone (its tie rule is not mirror-invariant) and so is
+// the self-mirrored angle n/2.
+template <bool kSaga>
+__global__ void __launch_bounds__(256)
+k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
+              const float2* __restrict__ PM, const float2* __restrict__ PTM, int n, int pitch,
+              const FwdAngle* __restrict__ ang, const int2* __restrict__ entries, int n_entries,
+              int n_det, float* __restrict__ sino, SinoSaga saga) {
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.y * 8 + warp;
+  if (e >= n_entries) return;
+  const int2 ent = entries[e];
+  const int a = ent.x, am = ent.y;
+  const int j = blockIdx.x * 32 + lane;
+  const FwdAngle A = ang[a];
+  const float2* __restrict__ img = A.transposed ? PT : P;
+  const float2* __restrict__ imgm = A.transposed ? PTM : PM;
+  const int jr = min(j, n_det - 1);
+  const long long X0 = __double2ll_rn(fma((double)jr, A.xi_dj, A.xi_base) * kFix);
+  int lo, hi;
+  band_range(X0, A.step, A.inv_step, n, &lo, &hi);
+  int wlo = lo < hi ? lo : n, whi = lo < hi ? hi : 0;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    wlo = min(wlo, __shfl_xor_sync(0xffffffffu, wlo, o));
+    whi = max(whi, __shfl_xor_sync(0xffffffffu, whi, o));
+  }
+  const long long dYl = A.step + ((long long)pitch << 32);
+  Fix32 Y = fix_from(X0 + (long long)wlo * dYl + ((long long)(1 + kPadC) << 32));
+  const Fix32 dY = fix_from(dYl);
+  const float S = A.S, B = A.B;
+  float acc = 0.f, accm = 0.f;
+  int b = wlo;
+  if (am >= 0) {
+#pragma unroll 1
+    for (; b + 4 <= whi; b += 4) {
+      float2 v[4], vm[4];
+      float g[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[k] = __ldg(img + Y.hi);
+        vm[k] = __ldg(imgm + Y.hi);
+        g[k] = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
+        fix_add(Y, dY);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        acc += v[k].x;
+        acc = fmaf(g[k], v[k].y, acc);
+        accm += vm[k].x;
+        accm = fmaf(g[k], vm[k].y, accm);
+      }
+    }
+    for (; b < whi; ++b) {
+      const float2 v = __ldg(img + Y.hi), vm = __ldg(imgm + Y.hi);
+      const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
+      acc += v.x;
+      acc = fmaf(g, v.y, acc);
+      accm += vm.x;
+      accm = fmaf(g, vm.y, accm);
+      fix_add(Y, dY);
+    }
+  } else {
+#pragma unroll 4
+    for (; b < whi; ++b) {
+      const float2 v = __ldg(img + Y.hi);
+      const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
+      acc += v.x;
+      acc = fmaf(g, v.y, acc);
+      fix_add(Y, dY);
+    }
+  }
+  if (j < n_det) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int row = r == 0 ? a : am;
+      if (row < 0) break;
+      const float val = (r == 0 ? acc : accm) * A.wsc;
+      const size_t q = (size_t)row * n_det + j;
+      if (kSaga) {
+        const float po = saga.psi_tab[q];
+        const float d = val - po;
+        const float ps = saga.psi_sum[q];
+        const float zeta = d + ps;
+        saga.psi_sum[q] = fmaf(saga.p_i, d, ps);
+        saga.psi_tab[q] = val;
+        const float yv = fmaf(saga.sigma, zeta, saga.y[q]);
+        saga.y[q] = (yv - saga.sigma * saga.b[q]) * saga.inv_1ps;
+      } else {
+        sino[q] = val;
+      }
+    }
+  }
+}
+
 // ---- adjoint -----------------------------------------------------------------
 //
 // Pixel-driven gather, no atomics. A CTA owns a T x T pixel tile and a range of
@@ -165,32 +266,51 @@ __device__ __forceinline__ float onep32(uint32_t frac) {
   return __uint_as_float(0x3F800000u + (frac >> 9));
 }
 
-// kPair: factor-1 path (two bins per pixel, float2 window pairs, T = 32).
+template <bool kPair, bool kSym>
+struct AdjWin;  // staged window element: bins (k, k+1) for the pair path, rows (a, n-a) for kSym
+template <> struct AdjWin<false, false> { using T = float; };
+template <> struct AdjWin<false, true> { using T = float2; };
+template <> struct AdjWin<true, false> { using T = float2; };
+template <> struct AdjWin<true, true> { using T = float4; };
+
+// kPair: factor-1 path (two bins per pixel, T = 32).
 // T: tile side; lanes = T*T/8 threads share one angle, G = 128/lanes angle groups.
-template <bool kPair, int T>
-__global__ void __launch_bounds__(kAdjThreads, 10)
+// kSym (mirror symmetry, full angle set of even size): the grid covers the
+// left half of the image; pixel p = (col,row) at angle a has the same detector
+// bins and weights as its mirror m(p) = (n-1-col,row) at angle n-a (theta ->
+// pi-theta, x -> -x), so each weight evaluation accumulates into both pixels,
+// reading rows a and n-a from one staged window element. Angle 0 is excluded
+// (the half-open tie rule flips under the mirror) and runs through the plain
+// kernel. Angles [a_begin, a_end) are split over grid.z; plane z of `out`
+// receives this split's partial image.
+template <bool kPair, int T, bool kSym>
+__global__ void __launch_bounds__(kAdjThreads, kSym ? 6 : 8)
 k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W, int CA,
-          int a_per_split, int n_loc, int n_det, const AdjAngle* __restrict__ ang) {
+          int a_begin, int a_per_split, int a_end, int n_mirror, int n_det,
+          const AdjAngle* __restrict__ ang) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  using WinT = typename AdjWin<kPair, kSym>::T;
   constexpr int lanes = T * T / kAdjPPT;
   constexpr int G = kAdjThreads / lanes;
   constexpr int dy_step = lanes / T;  // rows between a thread's pixels
+  constexpr int NACC = kSym ? 2 : 1;
   AdjStage* st = reinterpret_cast<AdjStage*>(smem_raw);
   float* red = reinterpret_cast<float*>(st + CA);
-  float* win = red + kAdjThreads * kAdjPPT;  // CA x W floats, or CA x W float2 pairs
-  float2* win2 = reinterpret_cast<float2*>(win);
+  WinT* win = reinterpret_cast<WinT*>(red + kAdjThreads * kAdjPPT * NACC);
 
   const int tid = threadIdx.x;
   const int grp = tid / lanes;
   const int pix0 = tid % lanes;
   const int x0 = blockIdx.x * T, y0 = blockIdx.y * T;
-  const int a_lo = blockIdx.z * a_per_split;
-  const int a_hi = min(n_loc, a_lo + a_per_split);
+  const int a_lo = a_begin + blockIdx.z * a_per_split;
+  const int a_hi = min(a_end, a_lo + a_per_split);
   const int dx = pix0 % T, dy = pix0 / T;
   const int warp = tid >> 5, lane = tid & 31;
-  float acc[kAdjPPT];
+  float acc[NACC][kAdjPPT];
 #pragma unroll
-  for (int k = 0; k < kAdjPPT; ++k) acc[k] = 0.f;
+  for (int q = 0; q < NACC; ++q)
+#pragma unroll
+    for (int k = 0; k < kAdjPPT; ++k) acc[q][k] = 0.f;
 
   for (int a0 = a_lo; a0 < a_hi; a0 += CA) {
     const int na = min(CA, a_hi - a0);
@@ -213,15 +333,14 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
         s.Rk = 1.f;
         s.k1a = 0.f;
         s.k1b = 0.f;  // factor 1: the box holds one bin
-        s.nb = A.nb;
       } else {
         s.kneg = A.kneg;
         s.Rk = A.Rk;
         // factor 1: u1 = (3 - R) - onep > 0, so w1 = sat(onep * (-kneg) + Rk + kneg * (3 - R))
         s.k1a = -A.kneg;
         s.k1b = A.Rk + A.kneg * (3.0f - A.R);
-        s.nb = A.nb;
       }
+      s.nb = A.nb;
       s.jb = jb + 1;
       s.wsc = A.wsc;
       st[t] = s;
@@ -232,19 +351,26 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
       const int jb = st[t].jb;
       const float wsc = st[t].wsc;
       const float* yrow = sino + (size_t)(a0 + t) * n_det;
+      const float* mrow = sino + (size_t)(kSym ? n_mirror - (a0 + t) : 0) * n_det;
       for (int k = lane; k < W; k += 32) {
         const int j = jb + k;
-        const float v0 = (j >= 0 && j < n_det) ? __ldg(yrow + j) * wsc : 0.f;
-        if (kPair) {
-          const float v1 = (j + 1 < n_det && j + 1 >= 0) ? __ldg(yrow + j + 1) * wsc : 0.f;
-          win2[t * W + k] = make_float2(v0, v1);
+        const bool in0 = j >= 0 && j < n_det, in1 = j + 1 >= 0 && j + 1 < n_det;
+        const float v0 = in0 ? __ldg(yrow + j) * wsc : 0.f;
+        if constexpr (kPair && kSym) {
+          win[t * W + k] = make_float4(v0, in1 ? __ldg(yrow + j + 1) * wsc : 0.f,
+                                       in0 ? __ldg(mrow + j) * wsc : 0.f,
+                                       in1 ? __ldg(mrow + j + 1) * wsc : 0.f);
+        } else if constexpr (kPair) {
+          win[t * W + k] = make_float2(v0, in1 ? __ldg(yrow + j + 1) * wsc : 0.f);
+        } else if constexpr (kSym) {
+          win[t * W + k] = make_float2(v0, in0 ? __ldg(mrow + j) * wsc : 0.f);
         } else {
           win[t * W + k] = v0;
         }
       }
     }
     __syncthreads();
-    if (kPair) {
+    if constexpr (kPair) {
 #pragma unroll 2
       for (int t = 0; t < na; ++t) {
         const AdjStage s = st[t];
@@ -252,12 +378,16 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
         const Fix32 estep = fix_from(s.estep);
 #pragma unroll
         for (int k = 0; k < kAdjPPT; ++k) {
-          const float2 pr = win2[e.hi];
+          const WinT pr = win[e.hi];
           const float onep = onep32(e.lo);
           const float w0 = __saturatef(fmaf(fabsf(s.c0 - onep), s.kneg, s.Rk));
           const float w1 = __saturatef(fmaf(onep, s.k1a, s.k1b));
-          acc[k] = fmaf(w0, pr.x, acc[k]);
-          acc[k] = fmaf(w1, pr.y, acc[k]);
+          acc[0][k] = fmaf(w0, pr.x, acc[0][k]);
+          acc[0][k] = fmaf(w1, pr.y, acc[0][k]);
+          if constexpr (kSym) {
+            acc[NACC - 1][k] = fmaf(w0, pr.z, acc[NACC - 1][k]);
+            acc[NACC - 1][k] = fmaf(w1, pr.w, acc[NACC - 1][k]);
+          }
           fix_add(e, estep);
         }
       }
@@ -266,56 +396,59 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
         const AdjStage s = st[t];
         Fix32 e = fix_from(s.E0 + (long long)dx * s.Dc + (long long)dy * s.Ds);
         const Fix32 estep = fix_from(s.estep);
-        if (s.axis) {
-          // half-open box [eta - h/2, eta + h/2): nb bins of weight 1 from ceil(v)
+        // bins outer, pixels inner: independent accumulation chains
+        int base[kAdjPPT];
+        float u[kAdjPPT];
+#pragma unroll
+        for (int k = 0; k < kAdjPPT; ++k) {
+          base[k] = (int)e.hi;
+          u[k] = s.c0 - onep32(e.lo);
+          fix_add(e, estep);
+        }
+        for (int b = 0; b < s.nb; ++b) {
 #pragma unroll
           for (int k = 0; k < kAdjPPT; ++k) {
-            const float* wp = win + e.hi;
-            float part = 0.f;
-            for (int b = 0; b < s.nb; ++b) part += wp[b];
-            acc[k] += part;
-            fix_add(e, estep);
-          }
-        } else {
-          // bins outer, pixels inner: eight independent accumulation chains
-          int base[kAdjPPT];
-          float u[kAdjPPT];
-#pragma unroll
-          for (int k = 0; k < kAdjPPT; ++k) {
-            base[k] = (int)e.hi;
-            u[k] = s.c0 - onep32(e.lo);
-            fix_add(e, estep);
-          }
-          for (int b = 0; b < s.nb; ++b) {
-#pragma unroll
-            for (int k = 0; k < kAdjPPT; ++k) {
-              acc[k] = fmaf(__saturatef(fmaf(fabsf(u[k]), s.kneg, s.Rk)), win[base[k] + b], acc[k]);
-              u[k] += 1.0f;
+            const float w = __saturatef(fmaf(fabsf(u[k]), s.kneg, s.Rk));
+            const WinT v = win[base[k] + b];
+            if constexpr (kSym) {
+              acc[0][k] = fmaf(w, v.x, acc[0][k]);
+              acc[NACC - 1][k] = fmaf(w, v.y, acc[NACC - 1][k]);
+            } else {
+              acc[0][k] = fmaf(w, v, acc[0][k]);
             }
+            u[k] += 1.0f;
           }
         }
       }
     }
   }
-  float* dst = out + (size_t)blockIdx.z * n * n;  // per-split partial image when gridDim.z > 1
+  float* dst = out + (size_t)blockIdx.z * n * n;  // per-split partial image
   if (G > 1) {
     // fixed-order sum over the angle groups
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kAdjPPT; ++k) red[(grp * kAdjPPT + k) * lanes + pix0] = acc[k];
+    for (int q = 0; q < NACC; ++q)
+#pragma unroll
+      for (int k = 0; k < kAdjPPT; ++k)
+        red[((q * G + grp) * kAdjPPT + k) * lanes + pix0] = acc[q][k];
     __syncthreads();
-    for (int q = tid; q < lanes * kAdjPPT; q += kAdjThreads) {
-      const int k = q / lanes, p = q % lanes;
+    for (int i = tid; i < NACC * lanes * kAdjPPT; i += kAdjThreads) {
+      const int q = i / (lanes * kAdjPPT), r = i % (lanes * kAdjPPT);
+      const int k = r / lanes, p = r % lanes;
       float v = 0.f;
-      for (int g = 0; g < G; ++g) v += red[(g * kAdjPPT + k) * lanes + p];
-      const int row = y0 + p / T + k * dy_step, col = x0 + p % T;
-      if (row < n && col < n) dst[(size_t)row * n + col] = v;
+      for (int g = 0; g < G; ++g) v += red[((q * G + g) * kAdjPPT + k) * lanes + p];
+      const int row = y0 + p / T + k * dy_step;
+      const int col = q == 0 ? x0 + p % T : n - 1 - (x0 + p % T);
+      if (row < n && col >= 0 && col < n) dst[(size_t)row * n + col] = v;
     }
   } else {
 #pragma unroll
     for (int k = 0; k < kAdjPPT; ++k) {
       const int row = y0 + dy + k * dy_step, col = x0 + dx;
-      if (row < n && col < n) dst[(size_t)row * n + col] = acc[k];
+      if (row < n && col < n) {
+        dst[(size_t)row * n + col] = acc[0][k];
+        if constexpr (kSym) dst[(size_t)row * n + (n - 1 - col)] = acc[NACC - 1][k];
+      }
     }
   }
 }
@@ -332,15 +465,26 @@ __global__ void k_adjoint_reduce(const float* __restrict__ part, float* __restri
 
 // ---- launchers ----------------------------------------------------------
 
-cudaError_t launch_forward(const float2* P, const float2* PT, int n, const FwdAngle* ang,
-                           int n_loc, int n_det, float* sino, const SinoSaga* saga,
-                           cudaStream_t stream) {
+cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, const float2* PTM,
+                           int n, const FwdAngle* ang, int n_loc, int n_det,
+                           const int2* sym_entries, int n_entries, float* sino,
+                           const SinoSaga* saga, cudaStream_t stream) {
+  SinoSaga none{};
+  if (sym_entries) {
+    dim3 grid((n_det + 31) / 32, (n_entries + 7) / 8);
+    if (saga)
+      k_forward_sym<true><<<grid, 256, 0, stream>>>(P, PT, PM, PTM, n, pair_pitch(n), ang,
+                                                    sym_entries, n_entries, n_det, nullptr, *saga);
+    else
+      k_forward_sym<false><<<grid, 256, 0, stream>>>(P, PT, PM, PTM, n, pair_pitch(n), ang,
+                                                     sym_entries, n_entries, n_det, sino, none);
+    return cudaGetLastError();
+  }
   dim3 grid((n_det + 31) / 32, (n_loc + 7) / 8);
   if (saga) {
     k_forward<true><<<grid, 256, 0, stream>>>(P, PT, n, pair_pitch(n), ang, n_loc, n_det, nullptr,
                                               *saga);
   } else {
-    SinoSaga none{};
     k_forward<false><<<grid, 256, 0, stream>>>(P, PT, n, pair_pitch(n), ang, n_loc, n_det, sino,
                                                none);
   }
@@ -350,63 +494,124 @@ cudaError_t launch_forward(const float2* P, const float2* PT, int n, const FwdAn
 // Opt-in shared memory beyond 48 KB (called once per device at plan creation,
 // outside any stream capture).
 void init_kernel_attributes() {
-  cudaFuncSetAttribute(k_adjoint<true, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_adjoint<false, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_adjoint<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_adjoint<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+#define ADJ_ATTR(P_, T_, S_)                                                                  \
+  cudaFuncSetAttribute(k_adjoint<P_, T_, S_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                       200 * 1024)
+  ADJ_ATTR(true, 32, false);
+  ADJ_ATTR(true, 32, true);
+  ADJ_ATTR(false, 32, false);
+  ADJ_ATTR(false, 32, true);
+  ADJ_ATTR(false, 16, false);
+  ADJ_ATTR(false, 8, false);
+  ADJ_ATTR(false, 16, true);
+  ADJ_ATTR(false, 8, true);
+#undef ADJ_ATTR
 }
 
 // Tile / split choice of the adjoint at one level (shared with the plan's
-// scratch sizing): T = 32 at factors 1-2, 16 at factor 4, else 8; T shrinks
-// to the next power of two >= n (>= 8) for small images. Enough angle splits
-// that the grid has ~4 CTAs per SM.
-void adjoint_layout(int n, int factor, int n_loc, int* T_out, int* S_out) {
+// scratch sizing): T = 32 at factor 1, 32 at factor 2, 16 at factor 4, else 8;
+// T shrinks to the next power of two >= n (>= 8) for small images. The angle
+// splits S give the grid ~16-20 CTAs per SM; with mirror symmetry (sym) the
+// grid covers half the tiles and one extra partial plane holds angle 0.
+void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_out) {
   int T = factor <= 2 ? 32 : (factor == 4 ? 16 : 8);
   int np2 = 8;
   while (np2 < n) np2 <<= 1;
   if (T > np2) T = np2;
-  const int tiles = ((n + T - 1) / T) * ((n + T - 1) / T);
-  int S = 1;
-  {
-    const int target = (factor == 1 ? 20 : 16) * 148;
-    S = (target + tiles - 1) / tiles;
-    const int max_s = n_loc / 8 > 1 ? n_loc / 8 : 1;
-    if (S > max_s) S = max_s;
-    if (S < 1) S = 1;
-  }
+  int tiles = ((n + T - 1) / T) * ((n + T - 1) / T);
+  if (sym) tiles /= 2;
+  const int target = (factor == 1 ? 20 : 16) * 148;
+  int S = (target + tiles - 1) / tiles;
+  const int max_s = n_loc / 8 > 1 ? n_loc / 8 : 1;
+  if (S > max_s) S = max_s;
+  if (S < 1) S = 1;
   *T_out = T;
   *S_out = S;
 }
 
-cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n, int factor,
-                           int n_loc, int n_det, const AdjAngle* ang, cudaStream_t stream,
-                           int* launches) {
+// Mirror symmetry applies when the slab is the whole, even-sized angle set and
+// the left half of the image is a whole number of tiles (T is a power of two,
+// so n % (2T) == 0).
+bool adjoint_sym_ok(int n, int factor, int n_loc, bool full_even_set) {
   int T, S;
-  adjoint_layout(n, factor, n_loc, &T, &S);
-  const bool pair = (factor == 1 && T == 32);
-  const int W = (int)floor(1.41422 * T * factor) + 6;
+  adjoint_layout(n, factor, n_loc, false, &T, &S);
+  return full_even_set && n_loc >= 4 && n % (2 * T) == 0;
+}
+
+int adjoint_planes(int n, int factor, int n_loc, bool sym) {
+  int T, S;
+  adjoint_layout(n, factor, n_loc, sym, &T, &S);
+  return sym ? S + 1 : (S > 1 ? S : 0);
+}
+
+template <bool kPair, int T, bool kSym>
+static void adj_launch(dim3 grid, size_t smem, cudaStream_t stream, const float* sino, float* dst,
+                       int n, int W, int CA, int a_begin, int per_split, int a_end, int n_mirror,
+                       int n_det, const AdjAngle* ang) {
+  k_adjoint<kPair, T, kSym><<<grid, kAdjThreads, smem, stream>>>(
+      sino, dst, n, W, CA, a_begin, per_split, a_end, n_mirror, n_det, ang);
+}
+
+static void adj_dispatch(bool pair, int T, bool sym, dim3 grid, size_t smem, cudaStream_t stream,
+                         const float* sino, float* dst, int n, int W, int CA, int a_begin,
+                         int per_split, int a_end, int n_mirror, int n_det, const AdjAngle* ang) {
+#define ADJ_CALL(P_, T_, S_)                                                                \
+  adj_launch<P_, T_, S_>(grid, smem, stream, sino, dst, n, W, CA, a_begin, per_split, a_end, \
+                         n_mirror, n_det, ang)
+  if (pair) {
+    if (sym) ADJ_CALL(true, 32, true); else ADJ_CALL(true, 32, false);
+  } else if (T == 32) {
+    if (sym) ADJ_CALL(false, 32, true); else ADJ_CALL(false, 32, false);
+  } else if (T == 16) {
+    if (sym) ADJ_CALL(false, 16, true); else ADJ_CALL(false, 16, false);
+  } else {
+    if (sym) ADJ_CALL(false, 8, true); else ADJ_CALL(false, 8, false);
+  }
+#undef ADJ_CALL
+}
+
+static size_t adj_smem(bool pair, bool sym, int T, int W, int* CA_io) {
   const int lanes = T * T / kAdjPPT;
   const int G = kAdjThreads / lanes;
-  const int per_split = (n_loc + S - 1) / S;
   int CA = G > 32 ? G : 32;
-  const size_t elem = pair ? sizeof(float2) : sizeof(float);
+  const size_t elem = sizeof(float) * (pair ? 2 : 1) * (sym ? 2 : 1);
   while (CA > G && (size_t)CA * W * elem > 100 * 1024) CA >>= 1;
-  const size_t smem = (size_t)CA * sizeof(AdjStage) + kAdjThreads * kAdjPPT * sizeof(float) +
-                      (size_t)CA * W * elem;
+  *CA_io = CA;
+  return (size_t)CA * sizeof(AdjStage) + kAdjThreads * kAdjPPT * (sym ? 2 : 1) * sizeof(float) +
+         (size_t)CA * W * elem;
+}
+
+cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n, int factor,
+                           int n_loc, int n_det, const AdjAngle* ang, bool full_even_set,
+                           cudaStream_t stream, int* launches) {
+  const bool sym = adjoint_sym_ok(n, factor, n_loc, full_even_set);
+  int T, S;
+  adjoint_layout(n, factor, n_loc, sym, &T, &S);
+  const bool pair = (factor == 1 && T == 32);
+  const int W = (int)floor(1.41422 * T * factor) + 6;
+  int CA;
+  *launches = 0;
+  if (sym) {
+    // angles 1 .. n_loc-1 with their mirrors over the left-half tiles, S planes;
+    // angle 0 through the plain kernel into plane S; then the ordered reduction
+    const size_t smem = adj_smem(pair, true, T, W, &CA);
+    const int per_split = (n_loc - 1 + S - 1) / S;
+    dim3 grid(n / (2 * T), (n + T - 1) / T, S);
+    adj_dispatch(pair, T, true, grid, smem, stream, sino, partial, n, W, CA, 1, per_split, n_loc,
+                 n_loc, n_det, ang);
+    const size_t smem0 = adj_smem(pair, false, T, W, &CA);
+    dim3 grid0((n + T - 1) / T, (n + T - 1) / T, 1);
+    adj_dispatch(pair, T, false, grid0, smem0, stream, sino, partial + (size_t)S * n * n, n, W, CA,
+                 0, 1, 1, n_loc, n_det, ang);
+    k_adjoint_reduce<<<(n * n + 255) / 256, 256, 0, stream>>>(partial, out, n * n, S + 1);
+    *launches = 3;
+    return cudaGetLastError();
+  }
+  const size_t smem = adj_smem(pair, false, T, W, &CA);
+  const int per_split = (n_loc + S - 1) / S;
   dim3 grid((n + T - 1) / T, (n + T - 1) / T, S);
-  float* dst = S > 1 ? partial : out;
-#define ADJ_LAUNCH(P_, T_)                                                                   \
-  k_adjoint<P_, T_><<<grid, kAdjThreads, smem, stream>>>(sino, dst, n, W, CA, per_split, n_loc, \
-                                                         n_det, ang)
-  if (pair)
-    ADJ_LAUNCH(true, 32);
-  else if (T == 32)
-    ADJ_LAUNCH(false, 32);
-  else if (T == 16)
-    ADJ_LAUNCH(false, 16);
-  else
-    ADJ_LAUNCH(false, 8);
-#undef ADJ_LAUNCH
+  adj_dispatch(pair, T, false, grid, smem, stream, sino, S > 1 ? partial : out, n, W, CA, 0,
+               per_split, n_loc, n_loc, n_det, ang);
   *launches = 1;
   if (S > 1) {
     k_adjoint_reduce<<<(n * n + 255) / 256, 256, 0, stream>>>(partial, out, n * n, S);

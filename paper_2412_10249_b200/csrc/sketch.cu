@@ -84,19 +84,24 @@ k_compensate(const float* __restrict__ x, float* __restrict__ out, int side, Com
 
 // Pair layouts of the n x n image u for the forward projector, rows padded by
 // kPadC zero columns on each side (imask_common.cuh):
-//   P [R][c + 1 + kPadC]  = (u[R][c], u[R][c+1] - u[R][c])   c in [-1-kPadC, n-1+kPadC]
-//   PT[C][r + 1 + kPadC]  = (u[r][C], u[r+1][C] - u[r][C])   r in [-1-kPadC, n-1+kPadC]
+//   P  [R][c + 1 + kPadC] = (u[R][c], u[R][c+1] - u[R][c])          c in [-1-kPadC, n-1+kPadC]
+//   PT [C][r + 1 + kPadC] = (u[r][C], u[r+1][C] - u[r][C])          r in [-1-kPadC, n-1+kPadC]
+// and, for the mirror-symmetric forward (PM != nullptr), the same layouts of
+// the left-right mirrored image um[R][c] = u[R][n-1-c]:
+//   PM [R][c + 1 + kPadC] = (u[R][n-1-c], u[R][n-2-c] - u[R][n-1-c])
+//   PTM[C][.]             = PT[n-1-C][.]
 // with u = 0 outside the image. The grid tiles the padded index range in both
-// dimensions; each 32x32 tile (plus a one-element halo) is staged in shared
-// memory so both the row-major and the transposed writes are coalesced.
+// dimensions; each 32x32 tile (plus a one-element halo on each side) is staged
+// in shared memory so the row-major and the transposed writes are coalesced.
 __global__ void __launch_bounds__(256)
-k_prepare(const float* __restrict__ u, int n, float2* __restrict__ P, float2* __restrict__ PT) {
-  __shared__ float t[33][34];
+k_prepare(const float* __restrict__ u, int n, float2* __restrict__ P, float2* __restrict__ PT,
+          float2* __restrict__ PM, float2* __restrict__ PTM) {
+  __shared__ float t[33][35];  // t[rr][cc] = u[r0 + rr][c0 - 1 + cc]
   const int pitch = pair_pitch(n);
   const int r0 = blockIdx.y * 32 - 1 - kPadC, c0 = blockIdx.x * 32 - 1 - kPadC;
-  for (int e = threadIdx.x; e < 33 * 33; e += blockDim.x) {
-    const int rr = e / 33, cc = e % 33;
-    const int R = r0 + rr, C = c0 + cc;
+  for (int e = threadIdx.x; e < 33 * 34; e += blockDim.x) {
+    const int rr = e / 34, cc = e % 34;
+    const int R = r0 + rr, C = c0 - 1 + cc;
     t[rr][cc] = (R >= 0 && R < n && C >= 0 && C < n) ? __ldg(u + (size_t)R * n + C) : 0.f;
   }
   __syncthreads();
@@ -104,18 +109,25 @@ k_prepare(const float* __restrict__ u, int n, float2* __restrict__ P, float2* __
     const int rr = e / 32, cc = e % 32;
     // row-major pairs: real rows, padded column index
     {
-      const int R = r0 + rr, idx = c0 + cc + 1 + kPadC;
+      const int R = r0 + rr, C = c0 + cc, idx = C + 1 + kPadC;
       if (R >= 0 && R < n && idx < pitch) {
-        const float v = t[rr][cc];
-        P[(size_t)R * pitch + idx] = make_float2(v, t[rr][cc + 1] - v);
+        const float v = t[rr][cc + 1];
+        P[(size_t)R * pitch + idx] = make_float2(v, t[rr][cc + 2] - v);
+        if (PM) {
+          // mirrored column c' = n-1-C holds (u[C], u[C-1] - u[C])
+          const int idm = n - 1 - C + 1 + kPadC;
+          if (idm >= 0 && idm < pitch) PM[(size_t)R * pitch + idm] = make_float2(v, t[rr][cc] - v);
+        }
       }
     }
     // transposed pairs: real columns, padded row index (consecutive threads walk rows of u)
     {
       const int C = c0 + rr, idx = r0 + cc + 1 + kPadC;
       if (C >= 0 && C < n && idx < pitch) {
-        const float v = t[cc][rr];
-        PT[(size_t)C * pitch + idx] = make_float2(v, t[cc + 1][rr] - v);
+        const float v = t[cc][rr + 1];
+        const float2 pr = make_float2(v, t[cc + 1][rr + 1] - v);
+        PT[(size_t)C * pitch + idx] = pr;
+        if (PTM) PTM[(size_t)(n - 1 - C) * pitch + idx] = pr;
       }
     }
   }
@@ -252,10 +264,11 @@ cudaError_t launch_compensate(const float* x, float* out, int side, const CompPa
   return cudaGetLastError();
 }
 
-cudaError_t launch_prepare(const float* u, int n, float2* P, float2* PT, cudaStream_t s) {
+cudaError_t launch_prepare(const float* u, int n, float2* P, float2* PT, float2* PM,
+                           float2* PTM, cudaStream_t s) {
   const int tiles = (pair_pitch(n) + 31) / 32;
   dim3 grid(tiles, tiles);
-  k_prepare<<<grid, 256, 0, s>>>(u, n, P, PT);
+  k_prepare<<<grid, 256, 0, s>>>(u, n, P, PT, PM, PTM);
   return cudaGetLastError();
 }
 

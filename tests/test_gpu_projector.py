@@ -194,7 +194,9 @@ def test_slab_rows_match_full():
         b, e = ctmodel.slab_bounds(90, rank, 3)
         plan = ctmodel.Plan(geom, angle_begin=b, angle_end=e)
         part = host(plan.project(x, 2)).reshape(e - b, 91)
-        assert np.array_equal(part, full[b:e])
+        # the full plan traces mirror pairs (a, n-a) from angle a's parameters, the slab
+        # plans trace each angle from its own: equal up to float32 rounding
+        assert rel_l2(part, full[b:e]) <= 1e-6
         bp_sum += host(plan.backproject(dev(y.reshape(90, 91)[b:e]), 2))
     ref = host(ctmodel.get_plan(geom).backproject(dev(y), 2))
     assert rel_l2(bp_sum, ref) <= 1e-6
