@@ -248,7 +248,9 @@ def main():
         if world > 1:
             torch.distributed.barrier()
 
-    # warm-up
+    # warm-up; the per-level CUDA graphs are captured here, never inside the timed region
+    for lv in range(r):
+        eng.graph(st, lv, prm)
     for k in range(args.warmup):
         solvers._device_step(eng, st, int(sched[k]), prm)
     torch.cuda.synchronize()

@@ -246,7 +246,9 @@ k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
 // constant weights (kneg = 0, Rk = 1 for the h bins of the box).
 
 constexpr int kAdjThreads = 128;
-constexpr int kAdjPPT = 8;  // pixels per thread (one column of a tile)
+// pixels per thread (one column of a tile): 8 where the per-angle setup must be
+// amortised (factors 1-4), 2 at coarse factors where the bin loop dominates
+// and small angle chunks keep the large windows within shared memory
 
 struct AdjStage {
   long long E0;     // Q32.32 of v at the tile origin (minus one ulp for axis angles), integer
@@ -283,20 +285,20 @@ template <> struct AdjWin<true, true> { using T = float4; };
 // (the half-open tie rule flips under the mirror) and runs through the plain
 // kernel. Angles [a_begin, a_end) are split over grid.z; plane z of `out`
 // receives this split's partial image.
-template <bool kPair, int T, bool kSym>
+template <bool kPair, int T, bool kSym, int kPPT>
 __global__ void __launch_bounds__(kAdjThreads, kSym ? 6 : 8)
 k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W, int CA,
           int a_begin, int a_per_split, int a_end, int n_mirror, int n_det,
           const AdjAngle* __restrict__ ang) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using WinT = typename AdjWin<kPair, kSym>::T;
-  constexpr int lanes = T * T / kAdjPPT;
+  constexpr int lanes = T * T / kPPT;
   constexpr int G = kAdjThreads / lanes;
   constexpr int dy_step = lanes / T;  // rows between a thread's pixels
   constexpr int NACC = kSym ? 2 : 1;
   AdjStage* st = reinterpret_cast<AdjStage*>(smem_raw);
   float* red = reinterpret_cast<float*>(st + CA);
-  WinT* win = reinterpret_cast<WinT*>(red + kAdjThreads * kAdjPPT * NACC);
+  WinT* win = reinterpret_cast<WinT*>(red + kAdjThreads * kPPT * NACC);
 
   const int tid = threadIdx.x;
   const int grp = tid / lanes;
@@ -306,11 +308,11 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
   const int a_hi = min(a_end, a_lo + a_per_split);
   const int dx = pix0 % T, dy = pix0 / T;
   const int warp = tid >> 5, lane = tid & 31;
-  float acc[NACC][kAdjPPT];
+  float acc[NACC][kPPT];
 #pragma unroll
   for (int q = 0; q < NACC; ++q)
 #pragma unroll
-    for (int k = 0; k < kAdjPPT; ++k) acc[q][k] = 0.f;
+    for (int k = 0; k < kPPT; ++k) acc[q][k] = 0.f;
 
   for (int a0 = a_lo; a0 < a_hi; a0 += CA) {
     const int na = min(CA, a_hi - a0);
@@ -377,7 +379,7 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
         Fix32 e = fix_from(s.E0 + (long long)dx * s.Dc + (long long)dy * s.Ds);
         const Fix32 estep = fix_from(s.estep);
 #pragma unroll
-        for (int k = 0; k < kAdjPPT; ++k) {
+        for (int k = 0; k < kPPT; ++k) {
           const WinT pr = win[e.hi];
           const float onep = onep32(e.lo);
           const float w0 = __saturatef(fmaf(fabsf(s.c0 - onep), s.kneg, s.Rk));
@@ -397,17 +399,17 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
         Fix32 e = fix_from(s.E0 + (long long)dx * s.Dc + (long long)dy * s.Ds);
         const Fix32 estep = fix_from(s.estep);
         // bins outer, pixels inner: independent accumulation chains
-        int base[kAdjPPT];
-        float u[kAdjPPT];
+        int base[kPPT];
+        float u[kPPT];
 #pragma unroll
-        for (int k = 0; k < kAdjPPT; ++k) {
+        for (int k = 0; k < kPPT; ++k) {
           base[k] = (int)e.hi;
           u[k] = s.c0 - onep32(e.lo);
           fix_add(e, estep);
         }
         for (int b = 0; b < s.nb; ++b) {
 #pragma unroll
-          for (int k = 0; k < kAdjPPT; ++k) {
+          for (int k = 0; k < kPPT; ++k) {
             const float w = __saturatef(fmaf(fabsf(u[k]), s.kneg, s.Rk));
             const WinT v = win[base[k] + b];
             if constexpr (kSym) {
@@ -429,21 +431,21 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
 #pragma unroll
     for (int q = 0; q < NACC; ++q)
 #pragma unroll
-      for (int k = 0; k < kAdjPPT; ++k)
-        red[((q * G + grp) * kAdjPPT + k) * lanes + pix0] = acc[q][k];
+      for (int k = 0; k < kPPT; ++k)
+        red[((q * G + grp) * kPPT + k) * lanes + pix0] = acc[q][k];
     __syncthreads();
-    for (int i = tid; i < NACC * lanes * kAdjPPT; i += kAdjThreads) {
-      const int q = i / (lanes * kAdjPPT), r = i % (lanes * kAdjPPT);
+    for (int i = tid; i < NACC * lanes * kPPT; i += kAdjThreads) {
+      const int q = i / (lanes * kPPT), r = i % (lanes * kPPT);
       const int k = r / lanes, p = r % lanes;
       float v = 0.f;
-      for (int g = 0; g < G; ++g) v += red[((q * G + g) * kAdjPPT + k) * lanes + p];
+      for (int g = 0; g < G; ++g) v += red[((q * G + g) * kPPT + k) * lanes + p];
       const int row = y0 + p / T + k * dy_step;
       const int col = q == 0 ? x0 + p % T : n - 1 - (x0 + p % T);
       if (row < n && col >= 0 && col < n) dst[(size_t)row * n + col] = v;
     }
   } else {
 #pragma unroll
-    for (int k = 0; k < kAdjPPT; ++k) {
+    for (int k = 0; k < kPPT; ++k) {
       const int row = y0 + dy + k * dy_step, col = x0 + dx;
       if (row < n && col < n) {
         dst[(size_t)row * n + col] = acc[0][k];
@@ -451,6 +453,20 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
       }
     }
   }
+}
+
+// Many planes, few pixels (coarse levels): a warp per pixel, lane l sums
+// planes l, l+32, ... and a fixed xor tree combines the lanes (deterministic).
+__global__ void k_adjoint_reduce_warp(const float* __restrict__ part, float* __restrict__ out,
+                                      int npix, int S) {
+  const int p = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (p >= npix) return;
+  float v = 0.f;
+  for (int s = lane; s < S; s += 32) v += __ldg(part + (size_t)s * npix + p);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) out[p] = v;
 }
 
 // Sum of the per-split partial images in split order (deterministic).
@@ -494,17 +510,17 @@ cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, 
 // Opt-in shared memory beyond 48 KB (called once per device at plan creation,
 // outside any stream capture).
 void init_kernel_attributes() {
-#define ADJ_ATTR(P_, T_, S_)                                                                  \
-  cudaFuncSetAttribute(k_adjoint<P_, T_, S_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                       200 * 1024)
-  ADJ_ATTR(true, 32, false);
-  ADJ_ATTR(true, 32, true);
-  ADJ_ATTR(false, 32, false);
-  ADJ_ATTR(false, 32, true);
-  ADJ_ATTR(false, 16, false);
-  ADJ_ATTR(false, 8, false);
-  ADJ_ATTR(false, 16, true);
-  ADJ_ATTR(false, 8, true);
+#define ADJ_ATTR(P_, T_, S_, K_)                                                          \
+  cudaFuncSetAttribute(k_adjoint<P_, T_, S_, K_>,                                        \
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
+  ADJ_ATTR(true, 32, false, 8);
+  ADJ_ATTR(true, 32, true, 8);
+  ADJ_ATTR(false, 32, false, 8);
+  ADJ_ATTR(false, 32, true, 8);
+  ADJ_ATTR(false, 16, false, 8);
+  ADJ_ATTR(false, 16, true, 8);
+  ADJ_ATTR(false, 8, false, 2);
+  ADJ_ATTR(false, 8, true, 2);
 #undef ADJ_ATTR
 }
 
@@ -545,10 +561,10 @@ int adjoint_planes(int n, int factor, int n_loc, bool sym) {
 }
 
 template <bool kPair, int T, bool kSym>
-static void adj_launch(dim3 grid, size_t smem, cudaStream_t stream, const float* sino, float* dst,
+static void adj_launch_(dim3 grid, size_t smem, cudaStream_t stream, const float* sino, float* dst,
                        int n, int W, int CA, int a_begin, int per_split, int a_end, int n_mirror,
                        int n_det, const AdjAngle* ang) {
-  k_adjoint<kPair, T, kSym><<<grid, kAdjThreads, smem, stream>>>(
+  k_adjoint<kPair, T, kSym, (T >= 16 ? 8 : 2)><<<grid, kAdjThreads, smem, stream>>>(
       sino, dst, n, W, CA, a_begin, per_split, a_end, n_mirror, n_det, ang);
 }
 
@@ -556,7 +572,7 @@ static void adj_dispatch(bool pair, int T, bool sym, dim3 grid, size_t smem, cud
                          const float* sino, float* dst, int n, int W, int CA, int a_begin,
                          int per_split, int a_end, int n_mirror, int n_det, const AdjAngle* ang) {
 #define ADJ_CALL(P_, T_, S_)                                                                \
-  adj_launch<P_, T_, S_>(grid, smem, stream, sino, dst, n, W, CA, a_begin, per_split, a_end, \
+  adj_launch_<P_, T_, S_>(grid, smem, stream, sino, dst, n, W, CA, a_begin, per_split, a_end, \
                          n_mirror, n_det, ang)
   if (pair) {
     if (sym) ADJ_CALL(true, 32, true); else ADJ_CALL(true, 32, false);
@@ -571,14 +587,24 @@ static void adj_dispatch(bool pair, int T, bool sym, dim3 grid, size_t smem, cud
 }
 
 static size_t adj_smem(bool pair, bool sym, int T, int W, int* CA_io) {
-  const int lanes = T * T / kAdjPPT;
+  const int ppt = T >= 16 ? 8 : 2;
+  const int lanes = T * T / ppt;
   const int G = kAdjThreads / lanes;
-  int CA = G > 32 ? G : 32;
   const size_t elem = sizeof(float) * (pair ? 2 : 1) * (sym ? 2 : 1);
-  while (CA > G && (size_t)CA * W * elem > 100 * 1024) CA >>= 1;
+  // up to 32 angles per chunk, fewer for wide windows (keep ~4+ CTAs per SM)
+  int CA = 32;
+  while (CA > G && (size_t)CA * W * elem > 40 * 1024) CA >>= 1;
+  if (CA < G) CA = G;
   *CA_io = CA;
-  return (size_t)CA * sizeof(AdjStage) + kAdjThreads * kAdjPPT * (sym ? 2 : 1) * sizeof(float) +
+  return (size_t)CA * sizeof(AdjStage) + kAdjThreads * ppt * (sym ? 2 : 1) * sizeof(float) +
          (size_t)CA * W * elem;
+}
+
+static void adj_reduce(const float* partial, float* out, int npix, int S, cudaStream_t stream) {
+  if (S >= 32 && npix <= 65536)
+    k_adjoint_reduce_warp<<<(npix * 32 + 255) / 256, 256, 0, stream>>>(partial, out, npix, S);
+  else
+    k_adjoint_reduce<<<(npix + 255) / 256, 256, 0, stream>>>(partial, out, npix, S);
 }
 
 cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n, int factor,
@@ -603,7 +629,7 @@ cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n,
     dim3 grid0((n + T - 1) / T, (n + T - 1) / T, 1);
     adj_dispatch(pair, T, false, grid0, smem0, stream, sino, partial + (size_t)S * n * n, n, W, CA,
                  0, 1, 1, n_loc, n_det, ang);
-    k_adjoint_reduce<<<(n * n + 255) / 256, 256, 0, stream>>>(partial, out, n * n, S + 1);
+    adj_reduce(partial, out, n * n, S + 1, stream);
     *launches = 3;
     return cudaGetLastError();
   }
@@ -614,7 +640,7 @@ cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n,
                per_split, n_loc, n_loc, n_det, ang);
   *launches = 1;
   if (S > 1) {
-    k_adjoint_reduce<<<(n * n + 255) / 256, 256, 0, stream>>>(partial, out, n * n, S);
+    adj_reduce(partial, out, n * n, S, stream);
     *launches = 2;
   }
   return cudaGetLastError();
