@@ -7,11 +7,14 @@
 // caller-owned device memory.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
 #include <vector>
+
+#include <cuda.h>
 
 #include "imask_b200.h"
 #include "imask_common.cuh"
@@ -42,6 +45,13 @@ cudaError_t launch_saga_sino(const float* psi_new, size_t m, const SinoSaga& sg,
 cudaError_t launch_resum(const float* phi_tab, float* phi_sum, int side, const float* psi_tab,
                          float* psi_sum, size_t m, const ResumParams& rp, cudaStream_t s);
 void init_kernel_attributes();
+struct TmaMaps {
+  CUtensorMap row, row_m, col, col_m;
+};
+cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float2* PT,
+                               const float2* PM, const float2* PTM, int n, const FwdAngle* ang,
+                               const int2* entries, int n_entries, int row_ctas, int n_det,
+                               float* sino, const SinoSaga* saga, cudaStream_t stream);
 }  // namespace imask
 
 struct imask_graph {
@@ -65,7 +75,43 @@ int fail(int code, const std::string& msg) {
 struct LevelTables {
   FwdAngle* fwd = nullptr;  // device
   AdjAngle* adj = nullptr;  // device
+  bool tma = false;         // tensor maps of the pair images at this level are valid
+  TmaMaps maps{};
 };
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D map over a pair image of one level: {pitch, n} 8-byte elements, box of
+// kFWc columns x kFB bands (constants of projector.cu: 96 x 16).
+bool encode_pair_map(CUtensorMap* map, void* base, int n) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || !base) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)pair_pitch(n), (cuuint64_t)n};
+  const cuuint64_t strides[1] = {(cuuint64_t)pair_pitch(n) * sizeof(float2)};
+  const cuuint32_t box[2] = {96, 16};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 }  // namespace
 
@@ -84,6 +130,9 @@ struct imask_plan {
   bool sym = false;       // whole, even-sized angle set: mirror-symmetric kernels
   int2* fwd_entries = nullptr;  // (angle, mirror angle or -1) per forward warp
   int n_entries = 0;
+  int2* tma_entries = nullptr;  // same, grouped 8 per CTA by ray family (-1 = idle warp)
+  int n_tma_entries = 0;
+  int tma_row_ctas = 0;         // CTAs [0, tma_row_ctas) hold row-family entries
   float* u = nullptr;
   float* sino_tmp = nullptr;
   float* adj_partial = nullptr;  // per-split partial backprojections (coarse levels)
@@ -209,6 +258,12 @@ int get_tables(imask_plan* pl, int f, LevelTables** out) {
                       "cudaMemcpy");
       if (rc) return rc;
     }
+    static const bool no_tma = std::getenv("IMASK_NO_TMA") != nullptr;  // debugging / A-B runs
+    if (pl->sym && !no_tma) {
+      const int n = pl->side / f;
+      t.tma = encode_pair_map(&t.maps.row, pl->P, n) && encode_pair_map(&t.maps.row_m, pl->PM, n) &&
+              encode_pair_map(&t.maps.col, pl->PT, n) && encode_pair_map(&t.maps.col_m, pl->PTM, n);
+    }
     it = pl->tables.emplace(f, t).first;
   }
   *out = &it->second;
@@ -238,6 +293,20 @@ int run_adjoint(imask_plan* pl, int f, const float* sino, float* out, const AdjA
                                  ang, pl->sym, s, &launches);
   g_launches += launches;
   return cuda_check(e, "adjoint");
+}
+
+int run_forward(imask_plan* pl, int f, const LevelTables* t, float* sino, const SinoSaga* saga,
+                cudaStream_t s) {
+  const int n = pl->side / f;
+  ++g_launches;
+  cudaError_t e;
+  if (t->tma && pl->tma_entries)
+    e = launch_forward_tma(t->maps, pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->tma_entries,
+                           pl->n_tma_entries, pl->tma_row_ctas, pl->n_det, sino, saga, s);
+  else
+    e = launch_forward(pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->n_loc, pl->n_det,
+                       pl->fwd_entries, pl->n_entries, sino, saga, s);
+  return cuda_check(e, "forward");
 }
 
 int check_factor(const imask_plan* pl, int f) {
@@ -345,6 +414,24 @@ int imask_plan_create(int side, int n_angles, int n_det, int angle_begin, int an
     ent.push_back(make_int2(0, -1));             // tie rule not mirror-invariant
     ent.push_back(make_int2(n_angles / 2, -1));  // self-mirrored
     pl->n_entries = (int)ent.size();
+    // TMA forward: 8 entries of one ray family per CTA (rows vs columns of the image)
+    std::vector<int2> rowf, colf;
+    for (const int2& e2 : ent)
+      (std::fabs(cos_tab[e2.x]) >= std::fabs(sin_tab[e2.x]) ? rowf : colf).push_back(e2);
+    std::vector<int2> tent;
+    for (auto* lst : {&rowf, &colf}) {
+      for (const int2& e2 : *lst) tent.push_back(e2);
+      while (tent.size() % 8) tent.push_back(make_int2(-1, -1));
+      if (lst == &rowf) pl->tma_row_ctas = (int)tent.size() / 8;
+    }
+    pl->n_tma_entries = (int)tent.size();
+    if ((rc = cuda_check(cudaMalloc(&pl->tma_entries, sizeof(int2) * tent.size()), "cudaMalloc")) ||
+        (rc = cuda_check(cudaMemcpy(pl->tma_entries, tent.data(), sizeof(int2) * tent.size(),
+                                    cudaMemcpyHostToDevice),
+                         "cudaMemcpy"))) {
+      imask_plan_destroy(pl);
+      return rc;
+    }
     if ((rc = cuda_check(cudaMalloc(&pl->fwd_entries, sizeof(int2) * ent.size()), "cudaMalloc")) ||
         (rc = cuda_check(cudaMemcpy(pl->fwd_entries, ent.data(), sizeof(int2) * ent.size(),
                                     cudaMemcpyHostToDevice),
@@ -387,6 +474,7 @@ int imask_plan_destroy(imask_plan* pl) {
   cudaFree(pl->PM);
   cudaFree(pl->PTM);
   cudaFree(pl->fwd_entries);
+  cudaFree(pl->tma_entries);
   cudaFree(pl->u);
   cudaFree(pl->sino_tmp);
   cudaFree(pl->adj_partial);
@@ -415,9 +503,7 @@ int imask_project(imask_plan* pl, int factor, const float* u, int64_t u_len, flo
   if ((rc = get_tables(pl, factor, &t))) return rc;
   if (pl->n_loc == 0) return IMASK_OK;
   LAUNCH(launch_prepare(u, n, pl->P, pl->PT, pl->PM, pl->PTM, S(stream)), "prepare");
-  LAUNCH(launch_forward(pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->n_loc, pl->n_det,
-                        pl->fwd_entries, pl->n_entries, sino, nullptr, S(stream)),
-         "forward");
+  if ((rc = run_forward(pl, factor, t, sino, nullptr, S(stream)))) return rc;
   return IMASK_OK;
 }
 
@@ -499,9 +585,7 @@ int imask_sketch_forward(imask_plan* pl, int level, const float* x, float* sino,
     LAUNCH(launch_compensate(x, pl->u, pl->side, pl->cp, S(stream)), "compensate");
   if (pl->n_loc == 0) return IMASK_OK;
   LAUNCH(launch_prepare(pl->u, n, pl->P, pl->PT, pl->PM, pl->PTM, S(stream)), "prepare");
-  LAUNCH(launch_forward(pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->n_loc, pl->n_det,
-                        pl->fwd_entries, pl->n_entries, sino, nullptr, S(stream)),
-         "forward");
+  if ((rc = run_forward(pl, f, t, sino, nullptr, S(stream)))) return rc;
   return IMASK_OK;
 }
 
@@ -590,9 +674,7 @@ int imask_step_forward(imask_plan* pl, const imask_state* st, int level0,
   sg.p_i = (float)pl->probs[level0];
   sg.sigma = (float)prm->sigma;
   sg.inv_1ps = (float)(1.0 / (1.0 + prm->sigma));
-  LAUNCH(launch_forward(pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->n_loc, pl->n_det,
-                        pl->fwd_entries, pl->n_entries, nullptr, &sg, S(stream)),
-         "forward+saga");
+  if ((rc = run_forward(pl, f, t, nullptr, &sg, S(stream)))) return rc;
   return IMASK_OK;
 }
 

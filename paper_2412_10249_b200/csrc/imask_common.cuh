@@ -24,9 +24,10 @@ constexpr double kFix = 4294967296.0;  // 2^32
 // walking its warp's band range outside its own valid range is at most
 // 31*sqrt(2) < 48 columns from a lane inside it, so it reads zeros instead of
 // needing a predicate. Column c in [-1-kPadC, n-1+kPadC] is stored at index
-// c + 1 + kPadC of a row of pitch n + 2*kPadC + 1.
+// c + 1 + kPadC of a row of pitch >= n + 2*kPadC + 1, rounded up to an even
+// number of float2 so rows are 16-byte aligned (TMA tensor-map strides).
 constexpr int kPadC = 48;
-__host__ __device__ inline int pair_pitch(int n) { return n + 2 * kPadC + 1; }
+__host__ __device__ inline int pair_pitch(int n) { return (n + 2 * kPadC + 2) & ~1; }
 
 // Forward projector, one entry per (level factor, local angle).
 // A ray crosses `n` bands (pixel rows, or columns when |sin| > |cos|); at

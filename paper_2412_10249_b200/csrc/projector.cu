@@ -14,6 +14,10 @@
 // per angle a pixel's footprint covers nb detector bins whose weights are the
 // trapezoid the forward's chords integrate (reference operator:
 // ctmodel.py:73-154).
+#include <climits>
+#include <cstdlib>
+#include <cuda.h>
+
 #include "imask_common.cuh"
 
 namespace imask {
@@ -225,6 +229,295 @@ k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
       }
     }
   }
+}
+
+// ---- TMA-staged mirror-symmetric forward ---------------------------------------
+//
+// Same rays and arithmetic as k_forward_sym, but the image data come from
+// shared memory: a CTA (8 warps = 8 angle entries of one family, each with its
+// mirror, x 32 detectors) walks its bands in chunks of kFB; for every chunk the
+// exact window of kFWc pair columns its rays touch is fetched for the image
+// and its mirror by two cp.async.bulk.tensor.2d loads (double-buffered,
+// mbarrier full/empty pipeline; TMA zero-fills outside the tensor). The warps
+// then read the window with LDS.64 instead of L1-cached LDG, so the eight
+// neighbouring angles share one on-chip copy. A CTA whose window would exceed
+// kFWc (very wide angle spread) falls back to global loads. Window origins are
+// rounded down to an even pair index: a tensor copy must start 16-byte aligned.
+constexpr int kFB = 16;           // bands per chunk
+constexpr int kFWc = 96;          // window width in pair columns (x 8 B = 768 B per row)
+constexpr int kFMaxChunks = 512;  // side up to 8192
+
+struct TmaMaps {
+  CUtensorMap row, row_m, col, col_m;  // P, PM, PT, PTM of one level
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct FwdWarpInfo {
+  long long x0_first, x0_last, step;
+  int lo, hi;  // union of the warp's band ranges (lo >= hi: idle)
+};
+
+template <bool kSaga>
+__global__ void __launch_bounds__(256)
+k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P,
+              const float2* __restrict__ PT, const float2* __restrict__ PM,
+              const float2* __restrict__ PTM, int n, int pitch, const FwdAngle* __restrict__ ang,
+              const int2* __restrict__ entries, int n_entries, int row_ctas, int n_det,
+              float* __restrict__ sino, SinoSaga saga) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int kBox = kFB * kFWc;  // float2 per image per stage
+  float2* stage = reinterpret_cast<float2*>(smem);  // [2 stages][2 images][kFB][kFWc]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * 2 * kBox * sizeof(float2));
+  uint64_t* empty = full + 2;
+  FwdWarpInfo* info = reinterpret_cast<FwdWarpInfo*>(empty + 2);
+  int* cmin_tab = reinterpret_cast<int*>(info + 8);
+  int* ctl = cmin_tab + kFMaxChunks;  // [0] overflow, [1] first band, [2] chunks
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int e = blockIdx.y * 8 + warp;
+  const int2 ent = e < n_entries ? entries[e] : make_int2(-1, -1);
+  const int a = ent.x, am = ent.y;
+  const bool valid = a >= 0;
+  const int j = blockIdx.x * 32 + lane;
+  const int jr = min(j, n_det - 1);
+  FwdAngle A{};
+  if (valid) A = ang[a];
+  long long X0 = 0;
+  int lo = n, hi = 0;
+  if (valid) {
+    X0 = __double2ll_rn(fma((double)jr, A.xi_dj, A.xi_base) * kFix);
+    band_range(X0, A.step, A.inv_step, n, &lo, &hi);
+    if (lo >= hi) {
+      lo = n;
+      hi = 0;
+    }
+  }
+  int wlo = lo, whi = hi;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    wlo = min(wlo, __shfl_xor_sync(0xffffffffu, wlo, o));
+    whi = max(whi, __shfl_xor_sync(0xffffffffu, whi, o));
+  }
+  const long long x_last = __shfl_sync(0xffffffffu, X0, 31);
+  if (lane == 0) {
+    info[warp] = FwdWarpInfo{X0, x_last, A.step, wlo, whi};
+
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int blo = n, bhi = 0;
+    for (int w = 0; w < 8; ++w) {
+      blo = min(blo, info[w].lo);
+      bhi = max(bhi, info[w].hi);
+    }
+    ctl[0] = 0;
+    ctl[1] = blo;
+    ctl[2] = bhi > blo ? (bhi - blo + kFB - 1) / kFB : 0;
+    if (ctl[2] > kFMaxChunks) ctl[0] = 1;
+  }
+  __syncthreads();
+  const int blo = ctl[1], nch = ctl[2];
+  // window (first pair column) of every chunk: extremes of the affine positions
+  for (int t = threadIdx.x; t < nch && !ctl[0]; t += blockDim.x) {
+    const int b0 = blo + t * kFB;
+    int cmn = INT_MAX, cmx = INT_MIN;
+    for (int w = 0; w < 8; ++w) {
+      const FwdWarpInfo& I = info[w];
+      const int bs = max(b0, I.lo), be = min(b0 + kFB, I.hi) - 1;
+      if (bs > be) continue;
+      const int c[4] = {(int)((I.x0_first + bs * I.step) >> 32), (int)((I.x0_first + be * I.step) >> 32),
+                        (int)((I.x0_last + bs * I.step) >> 32), (int)((I.x0_last + be * I.step) >> 32)};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        cmn = min(cmn, c[q]);
+        cmx = max(cmx, c[q]);
+      }
+    }
+    if (cmn > cmx) cmn = cmx = 0;  // no warp walks this chunk
+    // TMA needs a 16-byte aligned start in the inner dimension: even pair index
+    const int corig = ((cmn + 1 + kPadC) & ~1) - 1 - kPadC;
+    if (cmx - corig + 1 > kFWc) atomicExch(&ctl[0], 1);
+    cmin_tab[t] = corig;
+  }
+  __syncthreads();
+  // one ray family per CTA: the host puts the row-family CTAs first, so the
+  // family (and the tensor-map pointers below) is uniform, derived from blockIdx
+  const bool trans = (int)blockIdx.y >= row_ctas;
+  float acc = 0.f, accm = 0.f;
+  const float S = A.S, B = A.B;
+
+  if (ctl[0]) {
+    // fallback: global (L1) loads, as k_forward_sym
+    const float2* __restrict__ img = trans ? PT : P;
+    const float2* __restrict__ imgm = trans ? PTM : PM;
+    if (valid) {
+      const long long dYl = A.step + ((long long)pitch << 32);
+      Fix32 Y = fix_from(X0 + (long long)wlo * dYl + ((long long)(1 + kPadC) << 32));
+      const Fix32 dY = fix_from(dYl);
+      for (int b = wlo; b < whi; ++b) {
+        const float2 v = __ldg(img + Y.hi), vm = __ldg(imgm + Y.hi);
+        const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
+        acc += v.x;
+        acc = fmaf(g, v.y, acc);
+        accm += vm.x;
+        accm = fmaf(g, vm.y, accm);
+        fix_add(Y, dY);
+      }
+    }
+  } else if (nch > 0) {
+    const CUtensorMap* mm = trans ? &maps.col : &maps.row;
+    const CUtensorMap* mmm = trans ? &maps.col_m : &maps.row_m;
+    constexpr uint32_t kTx = 2 * kBox * sizeof(float2);
+    if (threadIdx.x == 0) {
+      mbar_init(&full[0], 1);
+      mbar_init(&full[1], 1);
+      mbar_init(&empty[0], 8);
+      mbar_init(&empty[1], 8);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // producer: warp 0 enters warp-uniformly, one lane issues the bulk tensor copies
+    if (warp == 0) {
+      if (lane == 0) {
+        for (int i = 0; i < 2 && i < nch; ++i) {
+          mbar_expect_tx(&full[i], kTx);
+          const int col = cmin_tab[i] + 1 + kPadC, row = blo + i * kFB;
+          tma_load_2d(stage + (i * 2 + 0) * kBox, mm, col, row, &full[i]);
+          tma_load_2d(stage + (i * 2 + 1) * kBox, mmm, col, row, &full[i]);
+        }
+      }
+      __syncwarp();
+    }
+    const Fix32 dYw = fix_from(A.step + ((long long)kFWc << 32));
+    for (int i = 0; i < nch; ++i) {
+      const int s = i & 1;
+      const int b0 = blo + i * kFB;
+      mbar_wait(&full[s], (i >> 1) & 1);
+      const int bs = max(b0, wlo), be = min(b0 + kFB, whi);
+      if (valid && bs < be) {
+        const float2* win = stage + (s * 2 + 0) * kBox;
+        const float2* winm = stage + (s * 2 + 1) * kBox;
+        const long long X = X0 + (long long)bs * A.step;
+        Fix32 Y = fix_from(X + ((long long)((bs - b0) * kFWc - cmin_tab[i]) << 32));
+        int b = bs;
+        for (; b + 4 <= be; b += 4) {
+          float2 v[4], vm[4];
+          float g[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            v[k] = win[Y.hi];
+            vm[k] = winm[Y.hi];
+            g[k] = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
+            fix_add(Y, dYw);
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            acc += v[k].x;
+            acc = fmaf(g[k], v[k].y, acc);
+            accm += vm[k].x;
+            accm = fmaf(g[k], vm[k].y, accm);
+          }
+        }
+        for (; b < be; ++b) {
+          const float2 v = win[Y.hi], vm = winm[Y.hi];
+          const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
+          acc += v.x;
+          acc = fmaf(g, v.y, acc);
+          accm += vm.x;
+          accm = fmaf(g, vm.y, accm);
+          fix_add(Y, dYw);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (warp == 0 && i + 2 < nch) {
+        // refill this stage with chunk i+2 once all eight warps have released it
+        mbar_wait(&empty[s], (i >> 1) & 1);
+        if (lane == 0) {
+          mbar_expect_tx(&full[s], kTx);
+          const int col = cmin_tab[i + 2] + 1 + kPadC, row = blo + (i + 2) * kFB;
+          tma_load_2d(stage + (s * 2 + 0) * kBox, mm, col, row, &full[s]);
+          tma_load_2d(stage + (s * 2 + 1) * kBox, mmm, col, row, &full[s]);
+        }
+        __syncwarp();
+      }
+    }
+  }
+  if (valid && j < n_det) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int row = r == 0 ? a : am;
+      if (row < 0) break;
+      const float val = (r == 0 ? acc : accm) * A.wsc;
+      const size_t q = (size_t)row * n_det + j;
+      if (kSaga) {
+        const float po = saga.psi_tab[q];
+        const float d = val - po;
+        const float ps = saga.psi_sum[q];
+        const float zeta = d + ps;
+        saga.psi_sum[q] = fmaf(saga.p_i, d, ps);
+        saga.psi_tab[q] = val;
+        const float yv = fmaf(saga.sigma, zeta, saga.y[q]);
+        saga.y[q] = (yv - saga.sigma * saga.b[q]) * saga.inv_1ps;
+      } else {
+        sino[q] = val;
+      }
+    }
+  }
+}
+
+size_t forward_tma_smem() {
+  return 2 * 2 * kFB * kFWc * sizeof(float2) + 4 * sizeof(uint64_t) + 8 * sizeof(FwdWarpInfo) +
+         (kFMaxChunks + 4) * sizeof(int);
+}
+
+cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float2* PT,
+                               const float2* PM, const float2* PTM, int n, const FwdAngle* ang,
+                               const int2* entries, int n_entries, int row_ctas, int n_det,
+                               float* sino, const SinoSaga* saga, cudaStream_t stream) {
+  dim3 grid((n_det + 31) / 32, (n_entries + 7) / 8);
+  const size_t smem = forward_tma_smem();
+  SinoSaga none{};
+  if (saga)
+    k_forward_tma<true><<<grid, 256, smem, stream>>>(maps, P, PT, PM, PTM, n, pair_pitch(n), ang,
+                                                      entries, n_entries, row_ctas, n_det, nullptr,
+                                                      *saga);
+  else
+    k_forward_tma<false><<<grid, 256, smem, stream>>>(maps, P, PT, PM, PTM, n, pair_pitch(n), ang,
+                                                       entries, n_entries, row_ctas, n_det, sino,
+                                                       none);
+  return cudaGetLastError();
 }
 
 // ---- adjoint -----------------------------------------------------------------
@@ -510,6 +803,10 @@ cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, 
 // Opt-in shared memory beyond 48 KB (called once per device at plan creation,
 // outside any stream capture).
 void init_kernel_attributes() {
+  cudaFuncSetAttribute(k_forward_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)forward_tma_smem());
+  cudaFuncSetAttribute(k_forward_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)forward_tma_smem());
 #define ADJ_ATTR(P_, T_, S_, K_)                                                          \
   cudaFuncSetAttribute(k_adjoint<P_, T_, S_, K_>,                                        \
                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
