@@ -300,7 +300,8 @@ int run_forward(imask_plan* pl, int f, const LevelTables* t, float* sino, const 
   const int n = pl->side / f;
   ++g_launches;
   cudaError_t e;
-  if (t->tma && pl->tma_entries)
+  // TMA staging pays off where the band walks are long; coarse grids use L1 loads
+  if (t->tma && pl->tma_entries && n > 128)
     e = launch_forward_tma(t->maps, pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->tma_entries,
                            pl->n_tma_entries, pl->tma_row_ctas, pl->n_det, sino, saga, s);
   else

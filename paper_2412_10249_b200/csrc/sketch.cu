@@ -80,6 +80,138 @@ k_compensate(const float* __restrict__ x, float* __restrict__ out, int side, Com
   }
 }
 
+// Fast path (side % 32 == 0, r <= 6): 32 x 32 tile, four contiguous pixels per
+// thread with 128-bit loads/stores; the pyramid terms of levels >= 2 are shared
+// by the four pixels, so acc = (sum over levels r-1..2, coarsest first) + the
+// level-1 term, which keeps the reference's accumulation order.
+struct CompTile32 {
+  float tile[32 * 32];
+  float pyr[16 * 16 + 8 * 8 + 4 * 4 + 2 * 2 + 1];
+};
+
+__device__ __forceinline__ void comp32_build(CompTile32& sm, int r) {
+  // level j has side 32 >> j at offset off(j) = sum_{l<j} (32 >> l)^2 (level 1 at 0)
+  const float* src = sm.tile;
+  float* dst = sm.pyr;
+  int sn = 32;
+  for (int lev = 1; lev < r; ++lev) {
+    const int dn = sn >> 1;
+    if ((int)threadIdx.x < dn * dn) {
+      const int rr = threadIdx.x / dn, cc = threadIdx.x % dn;
+      const float* s0 = src + (2 * rr) * sn + 2 * cc;
+      dst[threadIdx.x] = ((s0[0] + s0[1]) + (s0[sn] + s0[sn + 1])) * 0.25f;
+    }
+    __syncthreads();
+    src = dst;
+    dst += dn * dn;
+    sn = dn;
+  }
+}
+
+// S_r of the four pixels (py, px..px+3) of the staged tile.
+__device__ __forceinline__ float4 comp32_quad(const CompTile32& sm, const CompParams& cp, int py,
+                                             int px) {
+  const float4 v = *reinterpret_cast<const float4*>(&sm.tile[py * 32 + px]);
+  if (cp.r == 1) return v;  // S_1 = I (mrsketch.py:137-138)
+  float shared_acc = 0.f;
+  bool first = true;
+  for (int i = 1; i < cp.r - 1; ++i) {  // levels j = r-1 .. 2
+    const int j = cp.r - i;
+    const int sj = 32 >> j;
+    const int off = (1024 - (1 << (12 - 2 * j))) / 3;  // sum of (32 >> l)^2, l < j
+    const float term = cp.p[i - 1] * sm.pyr[off + (py >> j) * sj + (px >> j)];
+    shared_acc = first ? term : shared_acc + term;
+    first = false;
+  }
+  const float pl = cp.p[cp.r - 2];  // level-1 term (factor 2), last in the telescoping order
+  const float t0 = pl * sm.pyr[(py >> 1) * 16 + (px >> 1)];
+  const float t1 = pl * sm.pyr[(py >> 1) * 16 + (px >> 1) + 1];
+  const float a0 = first ? t0 : shared_acc + t0;
+  const float a1 = first ? t1 : shared_acc + t1;
+  return make_float4((v.x - a0) / cp.pr, (v.y - a0) / cp.pr, (v.z - a1) / cp.pr,
+                     (v.w - a1) / cp.pr);
+}
+
+__global__ void __launch_bounds__(256)
+k_compensate32(const float* __restrict__ x, float* __restrict__ out, int side, CompParams cp) {
+  __shared__ __align__(16) CompTile32 sm;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
+  const size_t g = (size_t)(y0 + py) * side + x0 + px;
+  *reinterpret_cast<float4*>(&sm.tile[py * 32 + px]) = __ldg(reinterpret_cast<const float4*>(x + g));
+  __syncthreads();
+  comp32_build(sm, cp.r);
+  *reinterpret_cast<float4*>(out + g) = comp32_quad(sm, cp, py, px);
+}
+
+__device__ __forceinline__ float saga_px(float pn, float& tab, float& sum, float& xv,
+                                         const ImageSaga& sg) {
+  const float d = pn - tab;
+  const float xi = d + sum;
+  sum = fmaf(sg.p_i, d, sum);
+  tab = pn;
+  xv = fmaf(-sg.s, xi, xv) * sg.inv_den;
+  return d;
+}
+
+// Full level, fast path: phi_new = S_r(bp) by the 32x32 tile pyramid, then the
+// SAGA image update, all with 128-bit accesses.
+__global__ void __launch_bounds__(256)
+k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, ImageSaga sg) {
+  __shared__ __align__(16) CompTile32 sm;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
+  const size_t g = (size_t)(y0 + py) * side + x0 + px;
+  *reinterpret_cast<float4*>(&sm.tile[py * 32 + px]) = __ldg(reinterpret_cast<const float4*>(bp + g));
+  float4 tab = *reinterpret_cast<const float4*>(sg.phi_tab + g);
+  float4 sum = *reinterpret_cast<const float4*>(sg.phi_sum + g);
+  float4 xv = *reinterpret_cast<const float4*>(sg.x + g);
+  __syncthreads();
+  comp32_build(sm, cp.r);
+  const float4 pn = comp32_quad(sm, cp, py, px);
+  saga_px(pn.x, tab.x, sum.x, xv.x, sg);
+  saga_px(pn.y, tab.y, sum.y, xv.y, sg);
+  saga_px(pn.z, tab.z, sum.z, xv.z, sg);
+  saga_px(pn.w, tab.w, sum.w, xv.w, sg);
+  *reinterpret_cast<float4*>(sg.phi_tab + g) = tab;
+  *reinterpret_cast<float4*>(sg.phi_sum + g) = sum;
+  *reinterpret_cast<float4*>(sg.x + g) = xv;
+}
+
+// Coarse level, fast path (side % 32 == 0, f <= 32): 32 x 32 full-resolution
+// tile, four contiguous pixels per thread, 128-bit accesses to x / phi_sum.
+__global__ void __launch_bounds__(256)
+k_saga_image_coarse32(const float* __restrict__ bp, int side, int f, float inv_f2, ImageSaga sg) {
+  const int n = side / f;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
+  const int row = y0 + py, col = x0 + px;
+  const size_t g = (size_t)row * side + col;
+  const int qrow = (row / f) * n;
+  float4 sum = *reinterpret_cast<const float4*>(sg.phi_sum + g);
+  float4 xv = *reinterpret_cast<const float4*>(sg.x + g);
+  float pn[4], po[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int q = qrow + (col + k) / f;
+    pn[k] = __ldg(bp + q) * inv_f2;
+    po[k] = sg.phi_tab[q];
+  }
+  float d;
+  d = pn[0] - po[0]; { const float xi = d + sum.x; sum.x = fmaf(sg.p_i, d, sum.x); xv.x = fmaf(-sg.s, xi, xv.x) * sg.inv_den; }
+  d = pn[1] - po[1]; { const float xi = d + sum.y; sum.y = fmaf(sg.p_i, d, sum.y); xv.y = fmaf(-sg.s, xi, xv.y) * sg.inv_den; }
+  d = pn[2] - po[2]; { const float xi = d + sum.z; sum.z = fmaf(sg.p_i, d, sum.z); xv.z = fmaf(-sg.s, xi, xv.z) * sg.inv_den; }
+  d = pn[3] - po[3]; { const float xi = d + sum.w; sum.w = fmaf(sg.p_i, d, sum.w); xv.w = fmaf(-sg.s, xi, xv.w) * sg.inv_den; }
+  *reinterpret_cast<float4*>(sg.phi_sum + g) = sum;
+  *reinterpret_cast<float4*>(sg.x + g) = xv;
+  __syncthreads();  // every old table value of this tile's blocks has been read
+  const int tc = 32 / f;
+  if ((int)threadIdx.x < tc * tc) {
+    const int q = (y0 / f + threadIdx.x / tc) * n + x0 / f + threadIdx.x % tc;
+    sg.phi_tab[q] = __ldg(bp + q) * inv_f2;
+  }
+}
+
 // ---- projector staging ------------------------------------------------------
 
 // Pair layouts of the n x n image u for the forward projector, rows padded by
@@ -254,6 +386,10 @@ static inline int comp_tile(int r) { return (r <= 6) ? 32 : 64; }
 
 cudaError_t launch_compensate(const float* x, float* out, int side, const CompParams& cp,
                               cudaStream_t s) {
+  if (side % 32 == 0 && cp.r <= 6) {
+    k_compensate32<<<dim3(side / 32, side / 32), 256, 0, s>>>(x, out, side, cp);
+    return cudaGetLastError();
+  }
   const int TT = comp_tile(cp.r);
   const int ts = side < TT ? side : TT;
   dim3 grid(side / ts, side / ts);
@@ -274,6 +410,11 @@ cudaError_t launch_prepare(const float* u, int n, float2* P, float2* PT, float2*
 
 cudaError_t launch_saga_image_coarse(const float* bp, int side, int f, const ImageSaga& sg,
                                      cudaStream_t s) {
+  if (side % 32 == 0 && f <= 32 && 32 % f == 0) {
+    k_saga_image_coarse32<<<dim3(side / 32, side / 32), 256, 0, s>>>(bp, side, f,
+                                                                     1.0f / (float)(f * f), sg);
+    return cudaGetLastError();
+  }
   int ts = f > 32 ? f : 32;
   if (ts > side) ts = side;
   dim3 grid(side / ts, side / ts);
@@ -283,6 +424,10 @@ cudaError_t launch_saga_image_coarse(const float* bp, int side, int f, const Ima
 
 cudaError_t launch_saga_image_full(const float* bp, int side, const CompParams& cp,
                                    const ImageSaga& sg, cudaStream_t s) {
+  if (side % 32 == 0 && cp.r <= 6) {
+    k_saga_image_full32<<<dim3(side / 32, side / 32), 256, 0, s>>>(bp, side, cp, sg);
+    return cudaGetLastError();
+  }
   const int TT = comp_tile(cp.r);
   const int ts = side < TT ? side : TT;
   dim3 grid(side / ts, side / ts);

@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
 timeout 600 python tools/prof_kernels.py --factors 1 --reps 1 > gpurun_out/prof_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k k_forward_sym -c 1 -o gpurun_out/prof_fwd -f python tools/prof_kernels.py --factors 1 --reps 1 > gpurun_out/ncu_fwd.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k k_forward_tma -c 1 -o gpurun_out/prof_fwd -f python tools/prof_kernels.py --factors 1 --reps 1 > gpurun_out/ncu_fwd.log 2>&1
 echo "ncu rc=$?"
