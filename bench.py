@@ -14,8 +14,10 @@ e2e     = iterations/s through the public API solvers.run(..., record_every=1,
           x_ref=...) from host data: b copied from pinned host memory inside the
           timed region, per-iteration metric read-back (the reference run()'s
           rel_dist / psnr row), final x copied back.
-roofline = the dominant kernel (the level-1 backprojection) against measured
-          HBM bandwidth on its algorithmic bytes, plus its FP32-issue fraction.
+roofline = the dominant kernel (the slower level-1 projector) against measured
+          HBM bandwidth on its algorithmic bytes, plus an FP32-issue view (footprint
+          evaluations/s against a live FFMA-chain peak) and the HBM-bound
+          image-side SAGA kernels against HBM bandwidth (hbm_kernels).
 cpu_baseline / --impl reference = the reference algorithm (scipy CSR float64,
           oracle/ restatement) on a sampled-angle slice of config D, scaled to
           the full angle count (the full CSR needs ~130 GB).
@@ -310,7 +312,6 @@ def main():
     torch.cuda.synchronize()
     fwd_ms = float(np.mean([ev[2 * q].elapsed_time(ev[2 * q + 1]) for q in range(reps)]))
     m_loc = (end - begin) * cfg.n_det
-    alg_bytes = 4.0 * (cfg.d + m_loc)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
@@ -318,23 +319,80 @@ def main():
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured (MEASURED_PEAKS.json)" if "hbm_gbs" in peaks else "fallback 6650 GB/s"
-    achieved = alg_bytes / (adj_ms * 1e-3) / 1e9
-    # FP32-issue view: footprint evaluations (nnz of the reference CSR) per second
-    nnz = 4.0 / np.pi * (end - begin) * cfg.d
-    traffic = None
+    traffic_tab = {}
     try:
-        traffic = json.load(open(os.path.join(REPO, "profiles", "traffic.json"))).get("adjoint_f1")
+        traffic_tab = json.load(open(os.path.join(REPO, "profiles", "traffic.json")))
     except Exception:
         pass
-    roofline = {"bound": "hbm", "kernel": "k_adjoint<2> (level-1 backprojection)",
+
+    # HBM-bound kernels (SURVEY 8(d) kernel (3)+(4)): the image-side SAGA update
+    # with the fused compensation pyramid, timed alone at the full and coarsest level
+    import ctypes
+    from paper_2412_10249_b200 import _lib
+
+    cst = st.c_state(eng.b)
+    flush_sink = torch.empty((), device=device)
+
+    def time_image(level0):
+        for _ in range(3):
+            _lib.check(_lib.lib().imask_step_image(plan.handle, ctypes.byref(cst), level0,
+                                                   ctypes.byref(prm), plan.stream))
+        for q in range(reps):
+            # read-flush: evicts the working set without leaving dirty lines whose
+            # write-back would be charged to the kernel under test
+            flush_sink.copy_(flush.sum())
+            ev[2 * q].record(stream)
+            _lib.check(_lib.lib().imask_step_image(plan.handle, ctypes.byref(cst), level0,
+                                                   ctypes.byref(prm), plan.stream))
+            ev[2 * q + 1].record(stream)
+        torch.cuda.synchronize()
+        return float(np.mean([ev[2 * q].elapsed_time(ev[2 * q + 1]) for q in range(reps)]))
+
+    hbm_kernels = []
+    for level0, name in ((r - 1, "k_saga_image_full32 (f=1, compensation fused)"),
+                         (0, f"k_saga_image_coarse32 (f={2 ** (r - 1)})")):
+        f = 2 ** (r - 1 - level0)
+        di = cfg.d // (f * f)
+        nbytes = 4.0 * (7 * cfg.d) if f == 1 else 4.0 * (4 * cfg.d + 3 * di)
+        ms = time_image(level0)
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        hbm_kernels.append({"kernel": name, "algorithmic_bytes": nbytes, "avg_launch_ms": round(ms, 4),
+                            "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                            "frac": round(gbs / hbm_peak, 4),
+                            "traffic": traffic_tab.get("saga_image_full" if f == 1 else
+                                                       "saga_image_coarse")})
+
+    # dominant kernel of the step: the level-1 projector (forward or adjoint, whichever
+    # is slower). It is FP32-issue bound; the HBM figure uses its compulsory
+    # bytes 4*(d + m_slab) and is small by construction; fp32_view carries the real bound.
+    fwd_dominant = fwd_ms >= adj_ms
+    dom_ms = fwd_ms if fwd_dominant else adj_ms
+    alg_bytes = 4.0 * (cfg.d + m_loc)
+    achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
+    nnz = 4.0 / np.pi * (end - begin) * cfg.d  # footprint evaluations = nnz of the reference CSR
+    ffma = ctypes.c_double(0.0)
+    _lib.check(_lib.lib().imask_probe_ffma_peak(local, ctypes.byref(ffma)))
+    roofline = {"bound": "hbm",
+                "kernel": ("k_forward_tma<true> (level-1 projection, SAGA epilogue)" if fwd_dominant
+                           else "k_adjoint<pair,sym> (level-1 backprojection)"),
                 "achieved": round(achieved, 2), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(achieved / hbm_peak, 5), "traffic": traffic,
-                "algorithmic_bytes": alg_bytes, "avg_launch_ms": round(adj_ms, 4),
+                "frac": round(achieved / hbm_peak, 5),
+                "traffic": traffic_tab.get("forward_f1" if fwd_dominant else "adjoint_f1"),
+                "algorithmic_bytes": alg_bytes, "avg_launch_ms": round(dom_ms, 4),
                 "peak_source": peak_src,
-                "note": "projector is FP32-issue bound, not HBM bound (SURVEY 0.7); "
-                        "see fp32_view",
-                "fp32_view": {"footprint_evals_per_s": round(nnz / (adj_ms * 1e-3), 1),
-                              "forward_f1_ms": round(fwd_ms, 4), "adjoint_f1_ms": round(adj_ms, 4)}}
+                "note": "projectors are FP32-issue bound, not HBM bound (SURVEY 8(d)); "
+                        "see fp32_view; HBM-bound kernels in hbm_kernels",
+                "fp32_view": {
+                    "footprint_evals": nnz,
+                    "forward_f1_ms": round(fwd_ms, 4), "adjoint_f1_ms": round(adj_ms, 4),
+                    "forward_evals_per_s": round(nnz / (fwd_ms * 1e-3), 1),
+                    "adjoint_evals_per_s": round(nnz / (adj_ms * 1e-3), 1),
+                    "ffma_peak_per_s": round(ffma.value, 1),
+                    "evals_per_ffma_slot": round(nnz / (dom_ms * 1e-3) / ffma.value, 4),
+                    "csr_equivalent_gbs": round(8.0 * nnz / (dom_ms * 1e-3) / 1e9, 1),
+                    "csr_note": "bandwidth a float32 value + int32 index CSR SpMV would need "
+                                "to match this kernel (the reference's operator form)"},
+                "hbm_kernels": hbm_kernels}
 
     # e2e through the public API: solvers.run with host inputs
     e2e = None

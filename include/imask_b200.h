@@ -182,6 +182,11 @@ IMASK_API int imask_graph_destroy(imask_graph* graph);
  * enqueued (instrumentation for the benchmark's gpu_launches count). */
 IMASK_API int imask_last_launch_count(void);
 
+/* Measurement helper (no reference counterpart): thread-level FP32 FFMA
+ * throughput of `device` from an FFMA-chain microbenchmark, the FP32-issue
+ * denominator of bench.py's roofline. */
+IMASK_API int imask_probe_ffma_peak(int device, double* ffma_per_s);
+
 #ifdef __cplusplus
 }
 #endif

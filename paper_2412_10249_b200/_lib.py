@@ -48,6 +48,7 @@ SIGNATURES = {
     "imask_version": (ctypes.c_char_p, []),
     "imask_last_error": (ctypes.c_char_p, []),
     "imask_last_launch_count": (ctypes.c_int, []),
+    "imask_probe_ffma_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "imask_plan_create": (
         ctypes.c_int,
         [

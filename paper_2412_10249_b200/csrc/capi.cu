@@ -27,7 +27,7 @@ cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, 
                            const SinoSaga* saga, cudaStream_t stream);
 cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n, int factor,
                            int n_loc, int n_det, const AdjAngle* ang, bool full_even_set,
-                           cudaStream_t stream, int* launches);
+                           cudaStream_t stream, const SideStream& side, int* launches);
 int adjoint_planes(int n, int factor, int n_loc, bool sym);
 bool adjoint_sym_ok(int n, int factor, int n_loc, bool full_even_set);
 cudaError_t launch_restrict(const float* x, float* u, int side, int f, cudaStream_t s);
@@ -136,6 +136,7 @@ struct imask_plan {
   float* u = nullptr;
   float* sino_tmp = nullptr;
   float* adj_partial = nullptr;  // per-split partial backprojections (coarse levels)
+  SideStream aux;                // overlaps the angle-0 plane / forward staging with the adjoint
   size_t adj_partial_len = 0;
   int64_t scratch = 0;
   CompParams cp{};
@@ -290,7 +291,7 @@ int run_adjoint(imask_plan* pl, int f, const float* sino, float* out, const AdjA
                 cudaStream_t s) {
   int launches = 0;
   cudaError_t e = launch_adjoint(sino, out, pl->adj_partial, pl->side / f, f, pl->n_loc, pl->n_det,
-                                 ang, pl->sym, s, &launches);
+                                 ang, pl->sym, s, pl->aux, &launches);
   g_launches += launches;
   return cuda_check(e, "adjoint");
 }
@@ -333,6 +334,43 @@ uint64_t mix64(uint64_t z) {
 }
 
 constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+
+}  // namespace
+
+namespace {
+
+// Restriction (or compensation at the full level) of x into pl->u, then the
+// pair images of the forward projector.
+int stage_forward_input(imask_plan* pl, const float* x, int level0, cudaStream_t s) {
+  const int f = pl->factors[level0];
+  const int n = pl->side / f;
+  if (level0 < pl->r - 1)
+    LAUNCH(launch_restrict(x, pl->u, pl->side, f, s), "restrict");
+  else
+    LAUNCH(launch_compensate(x, pl->u, pl->side, pl->cp, s), "compensate");
+  if (pl->n_loc == 0) return IMASK_OK;
+  LAUNCH(launch_prepare(pl->u, n, pl->P, pl->PT, pl->PM, pl->PTM, s), "prepare");
+  return IMASK_OK;
+}
+
+// psi_new = K_i u on this slab fused with the sinogram-side SAGA update.
+int forward_saga(imask_plan* pl, const imask_state* st, int level0, const imask_step_params* prm,
+                 const LevelTables* t, cudaStream_t stream) {
+  if (pl->n_loc == 0) return IMASK_OK;
+  const int f = pl->factors[level0];
+  int rc;
+  const size_t m = (size_t)pl->n_loc * pl->n_det;
+  SinoSaga sg;
+  sg.psi_tab = st->psi_tab + (size_t)level0 * m;
+  sg.psi_sum = st->psi_sum;
+  sg.y = st->y;
+  sg.b = st->b;
+  sg.p_i = (float)pl->probs[level0];
+  sg.sigma = (float)prm->sigma;
+  sg.inv_1ps = (float)(1.0 / (1.0 + prm->sigma));
+  if ((rc = run_forward(pl, f, t, nullptr, &sg, S(stream)))) return rc;
+  return IMASK_OK;
+}
 
 }  // namespace
 
@@ -451,6 +489,13 @@ int imask_plan_create(int side, int n_angles, int n_det, int angle_begin, int an
     imask_plan_destroy(pl);
     return rc;
   }
+  if ((rc = cuda_check(cudaStreamCreateWithFlags(&pl->aux.stream, cudaStreamNonBlocking),
+                       "side stream")) ||
+      (rc = cuda_check(cudaEventCreateWithFlags(&pl->aux.fork, cudaEventDisableTiming), "event")) ||
+      (rc = cuda_check(cudaEventCreateWithFlags(&pl->aux.join, cudaEventDisableTiming), "event"))) {
+    imask_plan_destroy(pl);
+    return rc;
+  }
   pl->scratch = (int64_t)((pl->sym ? 4 : 2) * pair_bytes + img_bytes + sino_bytes);
   for (int f : pl->factors) {
     LevelTables* t;
@@ -479,6 +524,9 @@ int imask_plan_destroy(imask_plan* pl) {
   cudaFree(pl->u);
   cudaFree(pl->sino_tmp);
   cudaFree(pl->adj_partial);
+  if (pl->aux.stream) cudaStreamDestroy(pl->aux.stream);
+  if (pl->aux.fork) cudaEventDestroy(pl->aux.fork);
+  if (pl->aux.join) cudaEventDestroy(pl->aux.join);
   delete pl;
   return IMASK_OK;
 }
@@ -657,26 +705,10 @@ int imask_step_forward(imask_plan* pl, const imask_state* st, int level0,
   if (!(prm->sigma > 0.0)) return fail(IMASK_EINVAL, "sigma must be positive");
   DeviceGuard g(pl->device);
   const int f = pl->factors[level0];
-  const int n = pl->side / f;
   LevelTables* t;
   if ((rc = get_tables(pl, f, &t))) return rc;
-  if (level0 < pl->r - 1)
-    LAUNCH(launch_restrict(st->x, pl->u, pl->side, f, S(stream)), "restrict");
-  else
-    LAUNCH(launch_compensate(st->x, pl->u, pl->side, pl->cp, S(stream)), "compensate");
-  if (pl->n_loc == 0) return IMASK_OK;
-  LAUNCH(launch_prepare(pl->u, n, pl->P, pl->PT, pl->PM, pl->PTM, S(stream)), "prepare");
-  const size_t m = (size_t)pl->n_loc * pl->n_det;
-  SinoSaga sg;
-  sg.psi_tab = st->psi_tab + (size_t)level0 * m;
-  sg.psi_sum = st->psi_sum;
-  sg.y = st->y;
-  sg.b = st->b;
-  sg.p_i = (float)pl->probs[level0];
-  sg.sigma = (float)prm->sigma;
-  sg.inv_1ps = (float)(1.0 / (1.0 + prm->sigma));
-  if ((rc = run_forward(pl, f, t, nullptr, &sg, S(stream)))) return rc;
-  return IMASK_OK;
+  if ((rc = stage_forward_input(pl, st->x, level0, S(stream)))) return rc;
+  return forward_saga(pl, st, level0, prm, t, S(stream));
 }
 
 int imask_step_image(imask_plan* pl, const imask_state* st, int level0,
@@ -707,14 +739,36 @@ int imask_step_image(imask_plan* pl, const imask_state* st, int level0,
 
 int imask_sketch_step(imask_plan* pl, const imask_state* st, int level0,
                       const imask_step_params* prm, void* stream) {
-  int total = 0, rc;
-  if ((rc = imask_step_adjoint(pl, st, level0, stream))) return rc;
-  total += g_launches;
-  if ((rc = imask_step_forward(pl, st, level0, prm, stream))) return rc;
-  total += g_launches;
+  g_err.clear();
+  g_launches = 0;
+  int rc = check_level0(pl, level0);
+  if (rc) return rc;
+  if (!(prm->sigma > 0.0) || !(prm->mu_g > 0.0))
+    return fail(IMASK_EINVAL, "sigma and mu_g must be positive");
+  if (!(prm->mu > 0.0)) return fail(IMASK_EINVAL, "mu must be positive");
+  DeviceGuard g(pl->device);
+  const int f = pl->factors[level0];
+  const int n = pl->side / f;
+  LevelTables* t;
+  if ((rc = get_tables(pl, f, &t))) return rc;
+  const cudaStream_t s = S(stream);
+  if (pl->n_loc == 0) {
+    LAUNCH(cudaMemsetAsync(st->bp, 0, sizeof(float) * n * n, s), "memset");
+  } else {
+    // the forward's input staging (restriction / compensation + pair images)
+    // reads only x, so it runs on the side stream while the adjoint reads y
+    cudaEventRecord(pl->aux.fork, s);
+    cudaStreamWaitEvent(pl->aux.stream, pl->aux.fork, 0);
+    if ((rc = stage_forward_input(pl, st->x, level0, pl->aux.stream))) return rc;
+    if ((rc = run_adjoint(pl, f, st->y, st->bp, t->adj, s))) return rc;
+    cudaEventRecord(pl->aux.join, pl->aux.stream);
+    cudaStreamWaitEvent(s, pl->aux.join, 0);
+    if ((rc = cuda_check(cudaGetLastError(), "fork/join"))) return rc;
+    if ((rc = forward_saga(pl, st, level0, prm, t, s))) return rc;
+  }
+  const int launches = g_launches;
   if ((rc = imask_step_image(pl, st, level0, prm, stream))) return rc;
-  total += g_launches;
-  g_launches = total;
+  g_launches += launches;
   return IMASK_OK;
 }
 

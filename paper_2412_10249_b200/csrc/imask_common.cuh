@@ -92,6 +92,14 @@ struct SinoSaga {  // sinogram side of the SAGA step, fused into the forward epi
   float inv_1ps;  // 1 / (1 + sigma)
 };
 
+// Optional second stream for work that can overlap a kernel on the main
+// stream: fork = record on main + wait on side; join = record on side + wait on
+// main. stream == nullptr: everything stays on the main stream.
+struct SideStream {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
 struct ImageSaga {
   float* phi_tab;  // level row of the phi table (coarse, or full at the full level)
   float* phi_sum;

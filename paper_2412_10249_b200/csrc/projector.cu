@@ -578,8 +578,11 @@ template <> struct AdjWin<true, true> { using T = float4; };
 // (the half-open tie rule flips under the mirror) and runs through the plain
 // kernel. Angles [a_begin, a_end) are split over grid.z; plane z of `out`
 // receives this split's partial image.
+#ifndef IMASK_ADJ_SYM_MINB
+#define IMASK_ADJ_SYM_MINB 7
+#endif
 template <bool kPair, int T, bool kSym, int kPPT>
-__global__ void __launch_bounds__(kAdjThreads, kSym ? 6 : 8)
+__global__ void __launch_bounds__(kAdjThreads, kSym ? IMASK_ADJ_SYM_MINB : 8)
 k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W, int CA,
           int a_begin, int a_per_split, int a_end, int n_mirror, int n_det,
           const AdjAngle* __restrict__ ang) {
@@ -888,9 +891,13 @@ static size_t adj_smem(bool pair, bool sym, int T, int W, int* CA_io) {
   const int lanes = T * T / ppt;
   const int G = kAdjThreads / lanes;
   const size_t elem = sizeof(float) * (pair ? 2 : 1) * (sym ? 2 : 1);
-  // up to 32 angles per chunk, fewer for wide windows (keep ~4+ CTAs per SM)
+  // up to 32 angles per chunk, fewer for wide windows (keep ~7 CTAs per SM)
+  static const size_t cap = [] {
+    const char* e = getenv("IMASK_ADJ_WIN_KB");
+    return (size_t)(e ? atoi(e) : 20) * 1024;
+  }();
   int CA = 32;
-  while (CA > G && (size_t)CA * W * elem > 40 * 1024) CA >>= 1;
+  while (CA > G && (size_t)CA * W * elem > cap) CA >>= 1;
   if (CA < G) CA = G;
   *CA_io = CA;
   return (size_t)CA * sizeof(AdjStage) + kAdjThreads * ppt * (sym ? 2 : 1) * sizeof(float) +
@@ -906,7 +913,7 @@ static void adj_reduce(const float* partial, float* out, int npix, int S, cudaSt
 
 cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n, int factor,
                            int n_loc, int n_det, const AdjAngle* ang, bool full_even_set,
-                           cudaStream_t stream, int* launches) {
+                           cudaStream_t stream, const SideStream& side, int* launches) {
   const bool sym = adjoint_sym_ok(n, factor, n_loc, full_even_set);
   int T, S;
   adjoint_layout(n, factor, n_loc, sym, &T, &S);
@@ -916,16 +923,25 @@ cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n,
   *launches = 0;
   if (sym) {
     // angles 1 .. n_loc-1 with their mirrors over the left-half tiles, S planes;
-    // angle 0 through the plain kernel into plane S; then the ordered reduction
+    // angle 0 through the plain kernel into plane S (on the side stream, if
+    // any, concurrently with the symmetric kernel); then the ordered reduction
+    cudaStream_t s0 = stream;
+    if (side.stream) {
+      cudaEventRecord(side.fork, stream);
+      cudaStreamWaitEvent(side.stream, side.fork, 0);
+      s0 = side.stream;
+    }
+    const size_t smem0 = adj_smem(pair, false, T, W, &CA);
+    dim3 grid0((n + T - 1) / T, (n + T - 1) / T, 1);
+    adj_dispatch(pair, T, false, grid0, smem0, s0, sino, partial + (size_t)S * n * n, n, W, CA,
+                 0, 1, 1, n_loc, n_det, ang);
+    if (side.stream) cudaEventRecord(side.join, side.stream);
     const size_t smem = adj_smem(pair, true, T, W, &CA);
     const int per_split = (n_loc - 1 + S - 1) / S;
     dim3 grid(n / (2 * T), (n + T - 1) / T, S);
     adj_dispatch(pair, T, true, grid, smem, stream, sino, partial, n, W, CA, 1, per_split, n_loc,
                  n_loc, n_det, ang);
-    const size_t smem0 = adj_smem(pair, false, T, W, &CA);
-    dim3 grid0((n + T - 1) / T, (n + T - 1) / T, 1);
-    adj_dispatch(pair, T, false, grid0, smem0, stream, sino, partial + (size_t)S * n * n, n, W, CA,
-                 0, 1, 1, n_loc, n_det, ang);
+    if (side.stream) cudaStreamWaitEvent(stream, side.join, 0);
     adj_reduce(partial, out, n * n, S + 1, stream);
     *launches = 3;
     return cudaGetLastError();

@@ -144,6 +144,26 @@ k_compensate32(const float* __restrict__ x, float* __restrict__ out, int side, C
   *reinterpret_cast<float4*>(out + g) = comp32_quad(sm, cp, py, px);
 }
 
+// Restriction by a power-of-two factor f = 2^lg <= 32 (side % 32 == 0): each
+// CTA stages a 32 x 32 tile of x with 128-bit loads, builds the block-mean
+// pyramid in shared memory and writes the tile's (32/f)^2 coarse pixels.
+__global__ void __launch_bounds__(256)
+k_restrict32(const float* __restrict__ x, float* __restrict__ u, int side, int lg) {
+  __shared__ __align__(16) CompTile32 sm;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
+  *reinterpret_cast<float4*>(&sm.tile[py * 32 + px]) =
+      __ldg(reinterpret_cast<const float4*>(x + (size_t)(y0 + py) * side + x0 + px));
+  __syncthreads();
+  comp32_build(sm, lg + 1);
+  const int sj = 32 >> lg, n = side >> lg;
+  const int off = (1024 - (1 << (12 - 2 * lg))) / 3;  // pyramid offset of level lg
+  if ((int)threadIdx.x < sj * sj) {
+    const int rr = threadIdx.x / sj, cc = threadIdx.x % sj;
+    u[(size_t)((y0 >> lg) + rr) * n + (x0 >> lg) + cc] = sm.pyr[off + rr * sj + cc];
+  }
+}
+
 __device__ __forceinline__ float saga_px(float pn, float& tab, float& sum, float& xv,
                                          const ImageSaga& sg) {
   const float d = pn - tab;
@@ -368,6 +388,14 @@ static inline unsigned blocks_for(size_t n, int t) { return (unsigned)((n + t - 
 
 cudaError_t launch_restrict(const float* x, float* u, int side, int f, cudaStream_t s) {
   const int n = side / f;
+  if (side % 32 == 0 && f >= 2 && f <= 32) {
+    int lg = 0;
+    while ((1 << lg) < f) ++lg;
+    if ((1 << lg) == f) {
+      k_restrict32<<<dim3(side / 32, side / 32), 256, 0, s>>>(x, u, side, lg);
+      return cudaGetLastError();
+    }
+  }
   if (f >= 16) {
     k_restrict_warp<<<blocks_for((size_t)n * n * 32, 256), 256, 0, s>>>(x, u, side, f);
   } else {
