@@ -100,6 +100,30 @@ struct SideStream {
   cudaEvent_t fork = nullptr, join = nullptr;
 };
 
+// Inputs of the sinogram-side update of one ray, loaded before the band walk
+// so their latency hides behind it; sino_update then applies solvers.py:205-215
+// (psi row, psi_sum, dual prox) with the new projection value.
+struct SinoIn {
+  float po = 0.f, ps = 0.f, yv = 0.f, bv = 0.f;
+};
+__device__ __forceinline__ SinoIn sino_load(const SinoSaga& sg, size_t q) {
+  SinoIn in;
+  in.po = sg.psi_tab[q];
+  in.ps = sg.psi_sum[q];
+  in.yv = sg.y[q];
+  in.bv = __ldg(sg.b + q);
+  return in;
+}
+__device__ __forceinline__ void sino_update(const SinoSaga& sg, size_t q, const SinoIn& in,
+                                            float val) {
+  const float d = val - in.po;
+  const float zeta = d + in.ps;
+  sg.psi_sum[q] = fmaf(sg.p_i, d, in.ps);
+  sg.psi_tab[q] = val;
+  const float yv = fmaf(sg.sigma, zeta, in.yv);
+  sg.y[q] = (yv - sg.sigma * in.bv) * sg.inv_1ps;
+}
+
 struct ImageSaga {
   float* phi_tab;  // level row of the phi table (coarse, or full at the full level)
   float* phi_sum;

@@ -15,6 +15,7 @@
 // trapezoid the forward's chords integrate (reference operator:
 // ctmodel.py:73-154).
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cuda.h>
 
@@ -70,6 +71,8 @@ k_forward(const float2* __restrict__ P, const float2* __restrict__ PT, int n, in
   float acc = 0.f;
   // lanes past n_det trace the last detector's ray (result discarded)
   const int jr = min(j, n_det - 1);
+  SinoIn sin;
+  if (kSaga && j < n_det) sin = sino_load(saga, (size_t)a * n_det + j);
   const long long X0 = __double2ll_rn(fma((double)jr, A.xi_dj, A.xi_base) * kFix);
   int lo, hi;
   band_range(X0, A.step, A.inv_step, n, &lo, &hi);
@@ -116,14 +119,7 @@ k_forward(const float2* __restrict__ P, const float2* __restrict__ PT, int n, in
     const size_t q = (size_t)a * n_det + j;
     if (kSaga) {
       // sinogram side of sketch_step (solvers.py:205-215): psi row, psi_sum, dual prox
-      const float po = saga.psi_tab[q];
-      const float d = acc - po;
-      const float ps = saga.psi_sum[q];
-      const float zeta = d + ps;
-      saga.psi_sum[q] = fmaf(saga.p_i, d, ps);
-      saga.psi_tab[q] = acc;
-      const float yv = fmaf(saga.sigma, zeta, saga.y[q]);
-      saga.y[q] = (yv - saga.sigma * saga.b[q]) * saga.inv_1ps;
+      sino_update(saga, q, sin, acc);
     } else {
       sino[q] = acc;
     }
@@ -154,6 +150,11 @@ k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
   const float2* __restrict__ img = A.transposed ? PT : P;
   const float2* __restrict__ imgm = A.transposed ? PTM : PM;
   const int jr = min(j, n_det - 1);
+  SinoIn sin[2];
+  if (kSaga && j < n_det) {
+    sin[0] = sino_load(saga, (size_t)a * n_det + j);
+    if (am >= 0) sin[1] = sino_load(saga, (size_t)am * n_det + j);
+  }
   const long long X0 = __double2ll_rn(fma((double)jr, A.xi_dj, A.xi_base) * kFix);
   int lo, hi;
   band_range(X0, A.step, A.inv_step, n, &lo, &hi);
@@ -216,14 +217,7 @@ k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
       const float val = (r == 0 ? acc : accm) * A.wsc;
       const size_t q = (size_t)row * n_det + j;
       if (kSaga) {
-        const float po = saga.psi_tab[q];
-        const float d = val - po;
-        const float ps = saga.psi_sum[q];
-        const float zeta = d + ps;
-        saga.psi_sum[q] = fmaf(saga.p_i, d, ps);
-        saga.psi_tab[q] = val;
-        const float yv = fmaf(saga.sigma, zeta, saga.y[q]);
-        saga.y[q] = (yv - saga.sigma * saga.b[q]) * saga.inv_1ps;
+        sino_update(saga, q, sin[r], val);
       } else {
         sino[q] = val;
       }
@@ -313,6 +307,11 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   const int jr = min(j, n_det - 1);
   FwdAngle A{};
   if (valid) A = ang[a];
+  SinoIn sin[2];
+  if (kSaga && valid && j < n_det) {
+    sin[0] = sino_load(saga, (size_t)a * n_det + j);
+    if (am >= 0) sin[1] = sino_load(saga, (size_t)am * n_det + j);
+  }
   long long X0 = 0;
   int lo = n, hi = 0;
   if (valid) {
@@ -332,7 +331,6 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   const long long x_last = __shfl_sync(0xffffffffu, X0, 31);
   if (lane == 0) {
     info[warp] = FwdWarpInfo{X0, x_last, A.step, wlo, whi};
-
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -482,14 +480,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
       const float val = (r == 0 ? acc : accm) * A.wsc;
       const size_t q = (size_t)row * n_det + j;
       if (kSaga) {
-        const float po = saga.psi_tab[q];
-        const float d = val - po;
-        const float ps = saga.psi_sum[q];
-        const float zeta = d + ps;
-        saga.psi_sum[q] = fmaf(saga.p_i, d, ps);
-        saga.psi_tab[q] = val;
-        const float yv = fmaf(saga.sigma, zeta, saga.y[q]);
-        saga.y[q] = (yv - saga.sigma * saga.b[q]) * saga.inv_1ps;
+        sino_update(saga, q, sin[r], val);
       } else {
         sino[q] = val;
       }
@@ -831,6 +822,15 @@ void init_kernel_attributes() {
 // grid covers half the tiles and one extra partial plane holds angle 0.
 void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_out) {
   int T = factor <= 2 ? 32 : (factor == 4 ? 16 : 8);
+  if (const char* e = getenv("IMASK_ADJ_TILE")) {  // tuning: "f:T,f:T,..."
+    for (const char* q = e; *q;) {
+      int ff = 0, tt = 0;
+      if (sscanf(q, "%d:%d", &ff, &tt) == 2 && ff == factor && (tt == 8 || tt == 16 || tt == 32))
+        T = tt;
+      while (*q && *q != ',') ++q;
+      if (*q) ++q;
+    }
+  }
   int np2 = 8;
   while (np2 < n) np2 <<= 1;
   if (T > np2) T = np2;

@@ -109,6 +109,12 @@ def test_cost_ledger_and_run_report():
     assert rel_l2(host(rep.x), ost.x) <= 1e-3
     rel_ref = float(np.dot(ost.x - x_true, ost.x - x_true) / np.dot(x_true, x_true))
     assert abs(rep.rows[-1][3] - rel_ref) <= 1e-3 * rel_ref
+    # device-recorded rows: psnr as _metrics computes it, time stamps in order
+    import torch
+    x_t = torch.as_tensor(x_true, dtype=torch.float32, device=rep.x.device)
+    assert abs(rep.rows[-1][4] - solvers.psnr(rep.x, x_t)) <= 1e-9 * abs(rep.rows[-1][4]) + 1e-9
+    secs = [row[5] for row in rep.rows]
+    assert all(b >= a for a, b in zip(secs, secs[1:]))
     assert rep.to_csv().startswith("k,cost,level,rel_dist,psnr,seconds\n0,0,0,")
 
 
