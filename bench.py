@@ -251,8 +251,7 @@ def main():
             torch.distributed.barrier()
 
     # warm-up; the per-level CUDA graphs are captured here, never inside the timed region
-    for lv in range(r):
-        eng.graph(st, lv, prm)
+    eng.capture_all(st, prm)
     for k in range(args.warmup):
         solvers._device_step(eng, st, int(sched[k]), prm)
     torch.cuda.synchronize()

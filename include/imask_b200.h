@@ -48,7 +48,8 @@ typedef struct imask_plan imask_plan; /* opaque; owns per-angle tables + scratch
  *                          values replicated to full resolution)
  *   y, b, psi_sum        : n_loc*n_det (this rank's slab)
  *   psi_tab              : r * n_loc*n_det, level i at offset (i-1)*n_loc*n_det
- *   bp                   : side*side scratch for the (partial) backprojection */
+ *   bp                   : side*side scratch for the (partial) backprojection
+ *   y_next               : n_loc*n_det or NULL (see below) */
 typedef struct imask_state {
   float* x;
   float* y;
@@ -58,6 +59,11 @@ typedef struct imask_state {
   float* phi_tab;
   float* psi_tab;
   float* bp;
+  /* Optional second dual buffer (n_loc*n_det). When set, the forward writes
+   * y^{k+1} here instead of updating y in place, so imask_sketch_step runs
+   * the forward concurrently with the adjoint (which reads y^k); the caller
+   * swaps y and y_next after each step. NULL: in-place update. */
+  float* y_next;
 } imask_state;
 
 /* Per-iteration scalars of sketch_step (solvers.py:194-221) with the ridge
@@ -145,15 +151,19 @@ IMASK_API double imask_uniform_at(uint64_t seed, int64_t k);
 /* One parallel ImaSk iteration at 0-based level index `level0` (the value
  * draw_level returns) on one GPU: replaces sketch_step (solvers.py:194-221)
  * minus the host bookkeeping (k, cost, resum cadence stay on the host).
- * Equivalent to step_adjoint + step_forward + step_image below. */
+ * Equivalent to step_adjoint + step_forward + step_image below; with
+ * st->y_next set, the forward chain runs on a plan-owned side stream
+ * concurrently with the adjoint (fork/join with events, so the call stays
+ * stream-ordered and graph-capturable). */
 IMASK_API int imask_sketch_step(imask_plan* plan, const imask_state* st, int level0,
                                 const imask_step_params* prm, void* stream);
 /* The three phases of one iteration, for angle-sharded multi-GPU runs:
  *  step_adjoint : st->bp = partial (this slab) coarse backprojection R_f^T y
  *                 (or K^T y at the full level), reads y^k.
  *  step_forward : psi_new = K_i x^k on this slab, fused with the sinogram-
- *                 side SAGA update (psi table row, psi_sum, y prox). Must be
- *                 enqueued after step_adjoint (it overwrites y).
+ *                 side SAGA update (psi table row, psi_sum, y prox) writing
+ *                 y^{k+1} to st->y_next (or in place when it is NULL, in
+ *                 which case it must be enqueued after step_adjoint).
  *  step_image   : after st->bp has been all-reduced over ranks: phi_new,
  *                 phi table row, phi_sum and the x prox (x^k -> x^{k+1}).
  *                 Must be enqueued after step_forward's image read. */

@@ -37,6 +37,7 @@ class ImaskState(ctypes.Structure):
         ("phi_tab", _vp),
         ("psi_tab", _vp),
         ("bp", _vp),
+        ("y_next", _vp),
     ]
 
 

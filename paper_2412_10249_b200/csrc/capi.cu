@@ -41,7 +41,6 @@ cudaError_t launch_saga_image_coarse(const float* bp, int side, int f, const Ima
                                      cudaStream_t s);
 cudaError_t launch_saga_image_full(const float* bp, int side, const CompParams& cp,
                                    const ImageSaga& sg, cudaStream_t s);
-cudaError_t launch_saga_sino(const float* psi_new, size_t m, const SinoSaga& sg, cudaStream_t s);
 cudaError_t launch_resum(const float* phi_tab, float* phi_sum, int side, const float* psi_tab,
                          float* psi_sum, size_t m, const ResumParams& rp, cudaStream_t s);
 void init_kernel_attributes();
@@ -136,7 +135,9 @@ struct imask_plan {
   float* u = nullptr;
   float* sino_tmp = nullptr;
   float* adj_partial = nullptr;  // per-split partial backprojections (coarse levels)
-  SideStream aux;                // overlaps the angle-0 plane / forward staging with the adjoint
+  SideStream aux;                // angle-0 plane of the symmetric adjoint
+  SideStream aux2;               // forward chain of imask_sketch_step, concurrent with the adjoint
+  cudaEvent_t ev_staged = nullptr;  // aux2: x has been read (restriction / compensation done)
   size_t adj_partial_len = 0;
   int64_t scratch = 0;
   CompParams cp{};
@@ -363,7 +364,8 @@ int forward_saga(imask_plan* pl, const imask_state* st, int level0, const imask_
   SinoSaga sg;
   sg.psi_tab = st->psi_tab + (size_t)level0 * m;
   sg.psi_sum = st->psi_sum;
-  sg.y = st->y;
+  sg.y_in = st->y;
+  sg.y = st->y_next ? st->y_next : st->y;
   sg.b = st->b;
   sg.p_i = (float)pl->probs[level0];
   sg.sigma = (float)prm->sigma;
@@ -492,7 +494,12 @@ int imask_plan_create(int side, int n_angles, int n_det, int angle_begin, int an
   if ((rc = cuda_check(cudaStreamCreateWithFlags(&pl->aux.stream, cudaStreamNonBlocking),
                        "side stream")) ||
       (rc = cuda_check(cudaEventCreateWithFlags(&pl->aux.fork, cudaEventDisableTiming), "event")) ||
-      (rc = cuda_check(cudaEventCreateWithFlags(&pl->aux.join, cudaEventDisableTiming), "event"))) {
+      (rc = cuda_check(cudaEventCreateWithFlags(&pl->aux.join, cudaEventDisableTiming), "event")) ||
+      (rc = cuda_check(cudaStreamCreateWithFlags(&pl->aux2.stream, cudaStreamNonBlocking),
+                       "side stream")) ||
+      (rc = cuda_check(cudaEventCreateWithFlags(&pl->aux2.fork, cudaEventDisableTiming), "event")) ||
+      (rc = cuda_check(cudaEventCreateWithFlags(&pl->aux2.join, cudaEventDisableTiming), "event")) ||
+      (rc = cuda_check(cudaEventCreateWithFlags(&pl->ev_staged, cudaEventDisableTiming), "event"))) {
     imask_plan_destroy(pl);
     return rc;
   }
@@ -527,6 +534,10 @@ int imask_plan_destroy(imask_plan* pl) {
   if (pl->aux.stream) cudaStreamDestroy(pl->aux.stream);
   if (pl->aux.fork) cudaEventDestroy(pl->aux.fork);
   if (pl->aux.join) cudaEventDestroy(pl->aux.join);
+  if (pl->aux2.stream) cudaStreamDestroy(pl->aux2.stream);
+  if (pl->aux2.fork) cudaEventDestroy(pl->aux2.fork);
+  if (pl->aux2.join) cudaEventDestroy(pl->aux2.join);
+  if (pl->ev_staged) cudaEventDestroy(pl->ev_staged);
   delete pl;
   return IMASK_OK;
 }
@@ -754,6 +765,23 @@ int imask_sketch_step(imask_plan* pl, const imask_state* st, int level0,
   const cudaStream_t s = S(stream);
   if (pl->n_loc == 0) {
     LAUNCH(cudaMemsetAsync(st->bp, 0, sizeof(float) * n * n, s), "memset");
+  } else if (st->y_next) {
+    // double-buffered dual: the whole forward chain (staging + projection +
+    // sinogram-side update into y_next) overlaps the adjoint of y^k; the image
+    // update waits for the adjoint and for the staging's read of x
+    cudaEventRecord(pl->aux2.fork, s);
+    cudaStreamWaitEvent(pl->aux2.stream, pl->aux2.fork, 0);
+    if ((rc = stage_forward_input(pl, st->x, level0, pl->aux2.stream))) return rc;
+    cudaEventRecord(pl->ev_staged, pl->aux2.stream);
+    if ((rc = forward_saga(pl, st, level0, prm, t, pl->aux2.stream))) return rc;
+    cudaEventRecord(pl->aux2.join, pl->aux2.stream);
+    if ((rc = run_adjoint(pl, f, st->y, st->bp, t->adj, s))) return rc;
+    cudaStreamWaitEvent(s, pl->ev_staged, 0);
+    const int launches = g_launches;
+    if ((rc = imask_step_image(pl, st, level0, prm, stream))) return rc;
+    g_launches += launches;
+    cudaStreamWaitEvent(s, pl->aux2.join, 0);
+    return cuda_check(cudaGetLastError(), "fork/join");
   } else {
     // the forward's input staging (restriction / compensation + pair images)
     // reads only x, so it runs on the side stream while the adjoint reads y

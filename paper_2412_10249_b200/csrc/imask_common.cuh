@@ -85,7 +85,8 @@ __device__ __forceinline__ float onep_from_frac(uint32_t frac) {
 struct SinoSaga {  // sinogram side of the SAGA step, fused into the forward epilogue
   float* psi_tab;        // level row of the psi table
   float* psi_sum;
-  float* y;
+  const float* y_in;  // y^k
+  float* y;           // y^{k+1} (== y_in for the in-place update)
   const float* b;
   float p_i;
   float sigma;
@@ -110,7 +111,7 @@ __device__ __forceinline__ SinoIn sino_load(const SinoSaga& sg, size_t q) {
   SinoIn in;
   in.po = sg.psi_tab[q];
   in.ps = sg.psi_sum[q];
-  in.yv = sg.y[q];
+  in.yv = sg.y_in[q];
   in.bv = __ldg(sg.b + q);
   return in;
 }

@@ -134,7 +134,7 @@ k_forward(const float2* __restrict__ P, const float2* __restrict__ PT, int n, in
 // angle 0 is traced alone (its tie rule is not mirror-invariant) and so is
 // the self-mirrored angle n/2.
 template <bool kSaga>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 8)
 k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
               const float2* __restrict__ PM, const float2* __restrict__ PTM, int n, int pitch,
               const FwdAngle* __restrict__ ang, const int2* __restrict__ entries, int n_entries,

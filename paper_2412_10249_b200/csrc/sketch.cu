@@ -340,20 +340,6 @@ k_saga_image_full(const float* __restrict__ bp, int side, CompParams cp, ImageSa
   }
 }
 
-// Standalone sinogram-side update (used when the forward is not fused).
-__global__ void k_saga_sino(const float* __restrict__ psi_new, size_t m, SinoSaga sg) {
-  const size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= m) return;
-  const float pn = psi_new[q];
-  const float d = pn - sg.psi_tab[q];
-  const float ps = sg.psi_sum[q];
-  const float zeta = d + ps;
-  sg.psi_sum[q] = fmaf(sg.p_i, d, ps);
-  sg.psi_tab[q] = pn;
-  const float yv = fmaf(sg.sigma, zeta, sg.y[q]);
-  sg.y[q] = (yv - sg.sigma * sg.b[q]) * sg.inv_1ps;
-}
-
 // ---- resum (solvers.py:184-191) --------------------------------------------
 
 __global__ void k_resum_image(const float* __restrict__ phi_tab, float* __restrict__ phi_sum,
@@ -463,11 +449,6 @@ cudaError_t launch_saga_image_full(const float* bp, int side, const CompParams& 
     k_saga_image_full<32><<<grid, 256, 0, s>>>(bp, side, cp, sg);
   else
     k_saga_image_full<64><<<grid, 256, 0, s>>>(bp, side, cp, sg);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_saga_sino(const float* psi_new, size_t m, const SinoSaga& sg, cudaStream_t s) {
-  k_saga_sino<<<blocks_for(m, 256), 256, 0, s>>>(psi_new, m, sg);
   return cudaGetLastError();
 }
 

@@ -91,7 +91,7 @@ class Engine:
         self.use_graphs = True
 
     def graph(self, state: "SaddleState", level0: int, prm) -> tuple:
-        key = (id(state), level0, prm.sigma, prm.mu)
+        key = (id(state), state.y.data_ptr(), level0, prm.sigma, prm.mu)
         hit = self._graphs.get(key)
         if hit is None:
             h = ctypes.c_void_p()
@@ -102,6 +102,13 @@ class Engine:
             hit = (h, n.value, state)  # keep the state alive while its graph exists
             self._graphs[key] = hit
         return hit
+
+    def capture_all(self, state: "SaddleState", prm) -> None:
+        """Capture the graphs of every level for both dual buffers (outside timing)."""
+        for _ in range(2 if state.y_alt is not None else 1):
+            for lv in range(self.family.r):
+                self.graph(state, lv, prm)
+            state.swap_dual()
 
     def release_graphs(self, state: Optional["SaddleState"] = None) -> None:
         for key in list(self._graphs):
@@ -203,7 +210,8 @@ class SaddleState:
     phi_tab: Optional[torch.Tensor] = None
     psi_tab: Optional[torch.Tensor] = None
     bp: Optional[torch.Tensor] = None
-    _cstate: Any = field(default=None, repr=False)
+    y_alt: Optional[torch.Tensor] = None  # second dual buffer: y^{k+1} is written here, then swapped
+    _cstates: dict = field(default_factory=dict, repr=False)
 
     def phi_full(self, i: int, family: SketchFamily) -> torch.Tensor:
         """Row i (0-based) in the reference's full-resolution layout."""
@@ -216,13 +224,22 @@ class SaddleState:
         return upsample(self.phi[i].reshape(low, low), f).reshape(-1)
 
     def c_state(self, b: torch.Tensor) -> _lib.ImaskState:
-        if self._cstate is None:
-            self._cstate = _lib.ImaskState(
+        """The C view of this state for the current dual buffer."""
+        key = (self.y.data_ptr(), b.data_ptr())
+        cs = self._cstates.get(key)
+        if cs is None:
+            cs = _lib.ImaskState(
                 self.x.data_ptr(), self.y.data_ptr(), b.data_ptr(), self.phi_sum.data_ptr(),
                 self.psi_sum.data_ptr(), self.phi_tab.data_ptr(), self.psi_tab.data_ptr(),
-                self.bp.data_ptr(),
+                self.bp.data_ptr(), None if self.y_alt is None else self.y_alt.data_ptr(),
             )
-        return self._cstate
+            self._cstates[key] = cs
+        return cs
+
+    def swap_dual(self) -> None:
+        """After a step that wrote y^{k+1} into y_alt: make it the current y."""
+        if self.y_alt is not None:
+            self.y, self.y_alt = self.y_alt, self.y
 
 
 def _require_engine(prob: Problem) -> Engine:
@@ -252,6 +269,7 @@ def init_state(prob: Problem, seed: int = 0, x0=None, y0=None, exact_memory: boo
         x=x, y=y, phi=phi, psi=psi, phi_sum=torch.zeros(d, device=dev),
         psi_sum=torch.zeros(m, device=dev), seed=seed, xbar=x.clone(), resum_every=resum_every,
         phi_tab=phi_tab, psi_tab=psi_tab, bp=torch.empty(d, device=dev),
+        y_alt=torch.empty(m, device=dev),
     )
     if exact_memory:
         for i in range(r):
@@ -299,10 +317,12 @@ def _device_step(eng: Engine, state: SaddleState, level0: int, prm: _lib.ImaskSt
     if eng.shard.world == 1 and eng.use_graphs:
         g, launches, _ = eng.graph(state, level0, prm)
         _lib.check(L.imask_graph_launch(g, s))
+        state.swap_dual()
         return launches
     cst = ctypes.byref(state.c_state(eng.b))
     if eng.shard.world == 1:
         _lib.check(L.imask_sketch_step(h, cst, level0, ctypes.byref(prm), s))
+        state.swap_dual()
         return _lib.last_launch_count()
     # angle-sharded: adjoint -> all-reduce (NCCL stream) || forward -> image update
     n = (eng.geom.side // eng.plan.factors[level0]) ** 2
@@ -313,6 +333,7 @@ def _device_step(eng: Engine, state: SaddleState, level0: int, prm: _lib.ImaskSt
     launches += _lib.last_launch_count()
     work.wait()
     _lib.check(L.imask_step_image(h, cst, level0, ctypes.byref(prm), s))
+    state.swap_dual()
     return launches + _lib.last_launch_count()
 
 

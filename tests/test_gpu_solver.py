@@ -75,6 +75,27 @@ def test_single_steps_tables_vs_oracle():
         assert rel_l2(host(st.y), ost.y) <= 1e-4
 
 
+@pytest.mark.parametrize("graphs", [True, False])
+def test_double_buffered_dual_matches_in_place(graphs):
+    """y_next (forward concurrent with the adjoint on a side stream) and the
+    in-place update give the same iterates, through graphs and eager calls."""
+    side, na, nd, probs = 64, 90, 91, [0.3, 0.3, 0.2, 0.2]
+    orc = so.SketchedCT(side, na, nd, probs)
+    b = orc.proj[1].apply(np.random.default_rng(4).random(side * side))
+    prob = build(side, na, nd, probs, b)
+    prob.engine.use_graphs = graphs
+    st_db = solvers.init_state(prob, seed=3)
+    st_ip = solvers.init_state(prob, seed=3)
+    st_ip.y_alt = None
+    for _ in range(12):
+        solvers.sketch_step(st_db, prob, 2e-4, 1e-2)
+        solvers.sketch_step(st_ip, prob, 2e-4, 1e-2)
+    prob.engine.release_graphs()
+    for a, c in ((st_db.x, st_ip.x), (st_db.y, st_ip.y), (st_db.phi_sum, st_ip.phi_sum),
+                 (st_db.psi_sum, st_ip.psi_sum)):
+        assert np.array_equal(host(a), host(c))
+
+
 def test_resum_matches_direct_sums():
     side, na, nd, probs = 32, 36, 47, [0.3, 0.3, 0.2, 0.2]
     orc = so.SketchedCT(side, na, nd, probs)

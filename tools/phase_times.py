@@ -53,5 +53,10 @@ for lv in range(r):
     tf = timed(lambda: _lib.check(L.imask_step_forward(h, ctypes.byref(cst), lv, ctypes.byref(prm), s)))
     ti = timed(lambda: _lib.check(L.imask_step_image(h, ctypes.byref(cst), lv, ctypes.byref(prm), s)))
     tall = timed(lambda: _lib.check(L.imask_sketch_step(h, ctypes.byref(cst), lv, ctypes.byref(prm), s)))
-    print(f"f={f:3d} adjoint {ta:8.1f}us forward {tf:8.1f}us image {ti:7.1f}us  step {tall:8.1f}us",
-          flush=True)
+    n = cfg.side // f
+    u = torch.rand(n * n, device="cuda")
+    sino = torch.empty(eng.m_loc, device="cuda")
+    tp = timed(lambda: eng.plan.project(u, f, sino))
+    tb = timed(lambda: eng.plan.backproject(st.y, f, u))
+    print(f"f={f:3d} adjoint {ta:8.1f}us forward {tf:8.1f}us image {ti:7.1f}us  step {tall:8.1f}us"
+          f"  | project {tp:8.1f}us backproject {tb:8.1f}us", flush=True)
