@@ -569,6 +569,27 @@ template <> struct AdjWin<true, true> { using T = float4; };
 // (the half-open tie rule flips under the mirror) and runs through the plain
 // kernel. Angles [a_begin, a_end) are split over grid.z; plane z of `out`
 // receives this split's partial image.
+// Pixel k of thread slot p (0 <= p < lanes) within a T x T tile. The lanes of
+// a warp cover a compact 8 x 4 pixel block at every k, so one window read
+// touches few distinct bins (ideally ~8|cos| + 4|sin| + 1 slots, many lanes
+// broadcast) instead of a 32-pixel row's ~32:
+//   T = 32 (lanes 128): fixed column 8*warp + p%8, rows p%32/8 + 4k
+//   T = 16 (lanes 32) : columns p%8 + 8*(k&1), rows p/8 + 4*(k>>1)
+//   T = 8  (lanes 32) : column p%8, rows p/8 + 4k
+template <int T>
+__device__ __forceinline__ void adj_pixel(int p, int k, int& dx, int& dy) {
+  if constexpr (T == 32) {
+    dx = ((p >> 5) << 3) + (p & 7);
+    dy = ((p & 31) >> 3) + 4 * k;
+  } else if constexpr (T == 16) {
+    dx = (p & 7) + 8 * (k & 1);
+    dy = (p >> 3) + 4 * (k >> 1);
+  } else {
+    dx = p & 7;
+    dy = (p >> 3) + 4 * k;
+  }
+}
+
 #ifndef IMASK_ADJ_SYM_MINB
 #define IMASK_ADJ_SYM_MINB 7
 #endif
@@ -581,7 +602,7 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
   using WinT = typename AdjWin<kPair, kSym>::T;
   constexpr int lanes = T * T / kPPT;
   constexpr int G = kAdjThreads / lanes;
-  constexpr int dy_step = lanes / T;  // rows between a thread's pixels
+  static_assert(lanes == (T == 32 ? 128 : 32), "adj_pixel layout");
   constexpr int NACC = kSym ? 2 : 1;
   AdjStage* st = reinterpret_cast<AdjStage*>(smem_raw);
   float* red = reinterpret_cast<float*>(st + CA);
@@ -593,7 +614,8 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
   const int x0 = blockIdx.x * T, y0 = blockIdx.y * T;
   const int a_lo = a_begin + blockIdx.z * a_per_split;
   const int a_hi = min(a_end, a_lo + a_per_split);
-  const int dx = pix0 % T, dy = pix0 / T;
+  int dx, dy;
+  adj_pixel<T>(pix0, 0, dx, dy);
   const int warp = tid >> 5, lane = tid & 31;
   float acc[NACC][kPPT];
 #pragma unroll
@@ -614,7 +636,7 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
              ((long long)(t * W) << 32);
       s.Dc = A.Dc;
       s.Ds = A.Ds;
-      s.estep = (long long)dy_step * A.Ds;
+      s.estep = 4 * A.Ds;  // next pixel of a thread: 4 rows down (T = 16: see estep2)
       s.c0 = 2.0f - A.R;
       s.axis = A.axis;
       if (A.axis) {
@@ -684,7 +706,9 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
       for (int t = grp; t < na; t += G) {
         const AdjStage s = st[t];
         Fix32 e = fix_from(s.E0 + (long long)dx * s.Dc + (long long)dy * s.Ds);
-        const Fix32 estep = fix_from(s.estep);
+        // T = 16 alternates +8 columns / (-8 columns, +4 rows) between pixels
+        const Fix32 estep = fix_from(T == 16 ? 8 * s.Dc : s.estep);
+        const Fix32 estep2 = fix_from(s.estep - 8 * s.Dc);
         // bins outer, pixels inner: independent accumulation chains
         int base[kPPT];
         float u[kPPT];
@@ -692,7 +716,7 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
         for (int k = 0; k < kPPT; ++k) {
           base[k] = (int)e.hi;
           u[k] = s.c0 - onep32(e.lo);
-          fix_add(e, estep);
+          fix_add(e, (T == 16 && (k & 1)) ? estep2 : estep);
         }
         for (int b = 0; b < s.nb; ++b) {
 #pragma unroll
@@ -726,14 +750,18 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
       const int k = r / lanes, p = r % lanes;
       float v = 0.f;
       for (int g = 0; g < G; ++g) v += red[((q * G + g) * kPPT + k) * lanes + p];
-      const int row = y0 + p / T + k * dy_step;
-      const int col = q == 0 ? x0 + p % T : n - 1 - (x0 + p % T);
+      int px, py;
+      adj_pixel<T>(p, k, px, py);
+      const int row = y0 + py;
+      const int col = q == 0 ? x0 + px : n - 1 - (x0 + px);
       if (row < n && col >= 0 && col < n) dst[(size_t)row * n + col] = v;
     }
   } else {
 #pragma unroll
     for (int k = 0; k < kPPT; ++k) {
-      const int row = y0 + dy + k * dy_step, col = x0 + dx;
+      int px, py;
+      adj_pixel<T>(pix0, k, px, py);
+      const int row = y0 + py, col = x0 + px;
       if (row < n && col < n) {
         dst[(size_t)row * n + col] = acc[0][k];
         if constexpr (kSym) dst[(size_t)row * n + (n - 1 - col)] = acc[NACC - 1][k];
