@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--config", default=CONFIG_KEY)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--steps-only", action="store_true",
+                    help="skip the post-run kernel measurements (launch-list profiling runs)")
     return ap.parse_args()
 
 
@@ -288,7 +290,16 @@ def main():
     per_level_ms = {f"f{2 ** (r - 1 - i)}": round(float(step_ms[lev == i].mean()), 4)
                     for i in range(r) if np.any(lev == i)}
 
-    # dominant kernel: level-1 (f = 1) backprojection, timed alone with events
+    if args.steps_only:
+        if rank == 0:
+            print(json.dumps(dict(base, value=ips, ms_per_step=total_ms / args.steps,
+                                  gpu_launches=launches, per_level_ms=per_level_ms,
+                                  note="--steps-only: no roofline / e2e / cpu_baseline")))
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    # dominant kernel: level-1 (f = 1) projector, timed alone with events
     plan = eng.plan
     ybuf = st.y.clone()
     out = torch.empty(cfg.d, device=device)
@@ -407,10 +418,14 @@ def main():
         b_dev = b_host.to(device, non_blocking=True)
         xref_dev = xref_host.to(device, non_blocking=True)
         prob2 = dist_mod.make_sharded_problem(geom, b_dev, fam, cfg.mu_g)
+        t1 = time.perf_counter()
         rep = solvers.run(prob2, "sketch", SIGMA, cfg.mu_g, e2e_steps, record_every=1,
                           seed=SEED, x_ref=xref_dev)
+        t2 = time.perf_counter()
         x_out = rep.x.cpu()
         dt = time.perf_counter() - t0
+        print(f"[bench] e2e: setup {1e3 * (t1 - t0):.1f} ms, run {1e3 * (t2 - t1):.1f} ms, "
+              f"read-back {1e3 * (time.perf_counter() - t2):.1f} ms", file=sys.stderr)
         e2e = {"value": e2e_steps / dt, "unit": "iter/s",
                "h2d_bytes_per_step": round((b_host.numel() + xref_host.numel()) * 4 / e2e_steps),
                "d2h_bytes_per_step": round(16 + x_out.numel() * 4 / e2e_steps),
