@@ -193,7 +193,8 @@ def main():
                             f"(factors 1..{2 ** (cfg.levels - 1)}), uniform level probabilities",
                 "side": cfg.side, "n_angles": cfg.n_angles, "n_det": cfg.n_det,
                 "levels": cfg.levels, "seed": SEED, "sigma": SIGMA, "mu_g": cfg.mu_g,
-                "parallelism": f"angle-sharded x{n_gpus}" if n_gpus > 1 else "single GPU"}
+                "parallelism": (f"mirror-closed angle shards x{n_gpus}, NCCL all-reduce of the "
+                                "coarse backprojection" if n_gpus > 1 else "single GPU")}
 
     if args.impl == "reference":
         if world > 1 and rank != 0:
@@ -229,7 +230,6 @@ def main():
     r = cfg.levels
     probs = [1.0 / r] * r
     geom = ctmodel.Geometry(cfg.side, cfg.n_angles, cfg.n_det)
-    begin, end = ctmodel.slab_bounds(cfg.n_angles, rank, world)
     x_true = ellipse_phantom(cfg.side, 0)
     # data: b = K x_true + 1% noise, built with the device projector (the CSR oracle needs
     # ~130 GB at this size); the same seeded arrays on every rank
@@ -238,7 +238,7 @@ def main():
     sino_h = sino.double().cpu().numpy()
     noise = np.random.default_rng(1).standard_normal(sino_h.size)
     b_full = sino_h + cfg.kappa * np.abs(sino_h).max() * noise
-    b_loc = b_full.reshape(cfg.n_angles, cfg.n_det)[begin:end].ravel()
+    b_loc = dist_mod.local_rows(geom, b_full, rank, world)  # mirror-closed shard rows
 
     fam = mrsketch.make_family(r, cfg.side, probs, mode="coarse")
     prob = dist_mod.make_sharded_problem(geom, b_loc, fam, cfg.mu_g, rank, world, group)
@@ -321,7 +321,8 @@ def main():
         ev[2 * q + 1].record(stream)
     torch.cuda.synchronize()
     fwd_ms = float(np.mean([ev[2 * q].elapsed_time(ev[2 * q + 1]) for q in range(reps)]))
-    m_loc = (end - begin) * cfg.n_det
+    n_loc = len(ctmodel.shard_angles(cfg.n_angles, rank, world))
+    m_loc = n_loc * cfg.n_det
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
@@ -379,7 +380,7 @@ def main():
     dom_ms = fwd_ms if fwd_dominant else adj_ms
     alg_bytes = 4.0 * (cfg.d + m_loc)
     achieved = alg_bytes / (dom_ms * 1e-3) / 1e9
-    nnz = 4.0 / np.pi * (end - begin) * cfg.d  # footprint evaluations = nnz of the reference CSR
+    nnz = 4.0 / np.pi * n_loc * cfg.d  # footprint evaluations = nnz of the reference CSR
     ffma = ctypes.c_double(0.0)
     _lib.check(_lib.lib().imask_probe_ffma_peak(local, ctypes.byref(ffma)))
     roofline = {"bound": "hbm",

@@ -99,7 +99,20 @@ IMASK_API int imask_plan_create(int side, int n_angles, int n_det, int angle_beg
                                 int angle_end, const double* cos_tab, const double* sin_tab,
                                 int r, const double* probs, double scale, int device,
                                 imask_plan** out);
+/* Same, for an arbitrary set of angles: local sinogram row i holds global
+ * angle angle_idx[i] (distinct, in [0, n_angles)); cos_tab / sin_tab are in
+ * local row order. Mirror-symmetric kernels are used when the rows are
+ * [angle 0 (optional)] followed by a list whose row i is the mirror
+ * (n_angles - a) of row (first + last - i), as the full set and the
+ * mirror-closed multi-GPU shards are (paper_2412_10249_b200.ctmodel.shard_angles). */
+IMASK_API int imask_plan_create_list(int side, int n_angles, int n_det, int n_loc,
+                                     const int* angle_idx, const double* cos_tab,
+                                     const double* sin_tab, int r, const double* probs,
+                                     double scale, int device, imask_plan** out);
 IMASK_API int imask_plan_destroy(imask_plan* plan);
+/* 1 if the plan's angle rows have the mirror layout above (symmetric kernels
+ * in use), else 0. */
+IMASK_API int imask_plan_symmetric(const imask_plan* plan);
 /* Scratch bytes the plan owns on the device (for memory accounting). */
 IMASK_API int64_t imask_plan_scratch_bytes(const imask_plan* plan);
 

@@ -61,7 +61,17 @@ SIGNATURES = {
             ctypes.POINTER(_vp),
         ],
     ),
+    "imask_plan_create_list": (
+        ctypes.c_int,
+        [
+            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+            ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), ctypes.c_int,
+            ctypes.POINTER(ctypes.c_double), ctypes.c_double, ctypes.c_int,
+            ctypes.POINTER(ctypes.c_void_p),
+        ],
+    ),
     "imask_plan_destroy": (ctypes.c_int, [_vp]),
+    "imask_plan_symmetric": (ctypes.c_int, [_vp]),
     "imask_plan_scratch_bytes": (ctypes.c_int64, [_vp]),
     "imask_project": (
         ctypes.c_int, [_vp, ctypes.c_int, _vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp]

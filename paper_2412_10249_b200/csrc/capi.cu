@@ -26,9 +26,9 @@ cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, 
                            const int2* sym_entries, int n_entries, float* sino,
                            const SinoSaga* saga, cudaStream_t stream);
 cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n, int factor,
-                           int n_loc, int n_det, const AdjAngle* ang, bool full_even_set,
+                           int n_loc, int n_det, const AdjAngle* ang, int sym_s,
                            cudaStream_t stream, const SideStream& side, int* launches);
-int adjoint_planes(int n, int factor, int n_loc, bool sym);
+int adjoint_planes(int n, int factor, int n_loc, bool sym, int sym_s);
 bool adjoint_sym_ok(int n, int factor, int n_loc, bool full_even_set);
 cudaError_t launch_restrict(const float* x, float* u, int side, int f, cudaStream_t s);
 cudaError_t launch_prolong(const float* u, float* x, int side, int f, float alpha,
@@ -115,7 +115,10 @@ bool encode_pair_map(CUtensorMap* map, void* base, int n) {
 }  // namespace
 
 struct imask_plan {
-  int side, n_angles, n_det, a_begin, a_end, n_loc, r, device;
+  int side, n_angles, n_det, n_loc, r, device;
+  std::vector<int> angle_idx;  // global angle index of every local sinogram row
+  int sym_s = 0;               // symmetric layout: rows [0, sym_s) unpaired (angle 0),
+                               // rows [sym_s, n_loc) mirror-paired as i <-> sym_s + n_loc - 1 - i
   double scale;
   std::vector<double> probs, cosv, sinv;
   std::vector<int> factors;        // factor of level i (0-based)
@@ -275,7 +278,7 @@ int get_tables(imask_plan* pl, int f, LevelTables** out) {
 int ensure_partial(imask_plan* pl, int f) {
   const int n = pl->side / f;
   const bool sym = adjoint_sym_ok(n, f, pl->n_loc, pl->sym);
-  const size_t need = (size_t)adjoint_planes(n, f, pl->n_loc, sym) * n * n;
+  const size_t need = (size_t)adjoint_planes(n, f, pl->n_loc, sym, pl->sym_s) * n * n;
   if (need > pl->adj_partial_len) {
     if (pl->adj_partial) cudaFree(pl->adj_partial);
     pl->adj_partial = nullptr;
@@ -292,7 +295,7 @@ int run_adjoint(imask_plan* pl, int f, const float* sino, float* out, const AdjA
                 cudaStream_t s) {
   int launches = 0;
   cudaError_t e = launch_adjoint(sino, out, pl->adj_partial, pl->side / f, f, pl->n_loc, pl->n_det,
-                                 ang, pl->sym, s, pl->aux, &launches);
+                                 ang, pl->sym ? pl->sym_s : -1, s, pl->aux, &launches);
   g_launches += launches;
   return cuda_check(e, "adjoint");
 }
@@ -386,15 +389,39 @@ int imask_plan_create(int side, int n_angles, int n_det, int angle_begin, int an
                       const double* cos_tab, const double* sin_tab, int r, const double* probs,
                       double scale, int device, imask_plan** out) {
   g_err.clear();
+  if (angle_begin < 0 || angle_end > n_angles || angle_begin > angle_end) {
+    if (out) *out = nullptr;
+    return fail(IMASK_EINVAL, "angle slab [" + std::to_string(angle_begin) + ", " +
+                                  std::to_string(angle_end) + ") outside 0.." +
+                                  std::to_string(n_angles));
+  }
+  std::vector<int> idx;
+  for (int a = angle_begin; a < angle_end; ++a) idx.push_back(a);
+  return imask_plan_create_list(side, n_angles, n_det, (int)idx.size(), idx.data(), cos_tab,
+                                sin_tab, r, probs, scale, device, out);
+}
+
+int imask_plan_create_list(int side, int n_angles, int n_det, int n_loc, const int* angle_idx,
+                           const double* cos_tab, const double* sin_tab, int r,
+                           const double* probs, double scale, int device, imask_plan** out) {
+  g_err.clear();
   g_launches = 0;
   if (!out) return fail(IMASK_EINVAL, "out must not be null");
   *out = nullptr;
   if (side < 1) return fail(IMASK_EINVAL, "side must be positive");
   if (n_angles < 1 || n_det < 1) return fail(IMASK_EINVAL, "n_angles and n_det must be positive");
-  if (angle_begin < 0 || angle_end > n_angles || angle_begin > angle_end)
-    return fail(IMASK_EINVAL, "angle slab [" + std::to_string(angle_begin) + ", " +
-                                  std::to_string(angle_end) + ") outside 0.." +
-                                  std::to_string(n_angles));
+  if (n_loc < 0 || n_loc > n_angles || (n_loc > 0 && !angle_idx))
+    return fail(IMASK_EINVAL, "bad angle list");
+  {
+    std::vector<char> seen(n_angles, 0);
+    for (int i = 0; i < n_loc; ++i) {
+      const int a = angle_idx[i];
+      if (a < 0 || a >= n_angles || seen[a])
+        return fail(IMASK_EINVAL, "angle list entry " + std::to_string(a) +
+                                      " out of range or repeated");
+      seen[a] = 1;
+    }
+  }
   if (r < 1 || r > 7) return fail(IMASK_EINVAL, "levels r must be in 1..7");
   const int coarsest = 1 << (r - 1);
   if (side % coarsest != 0)
@@ -407,7 +434,6 @@ int imask_plan_create(int side, int n_angles, int n_det, int angle_begin, int an
   }
   if (std::fabs(psum - 1.0) > 1e-12)
     return fail(IMASK_EINVAL, "probabilities sum to " + std::to_string(psum) + ", expected 1");
-  const int n_loc = angle_end - angle_begin;
   if ((n_loc > 0) && (!cos_tab || !sin_tab)) return fail(IMASK_EINVAL, "angle tables missing");
   for (int a = 0; a < n_loc; ++a)
     if (cos_tab[a] == 0.0 && sin_tab[a] == 0.0)
@@ -419,8 +445,7 @@ int imask_plan_create(int side, int n_angles, int n_det, int angle_begin, int an
   pl->side = side;
   pl->n_angles = n_angles;
   pl->n_det = n_det;
-  pl->a_begin = angle_begin;
-  pl->a_end = angle_end;
+  pl->angle_idx.assign(angle_idx, angle_idx + n_loc);
   pl->n_loc = n_loc;
   pl->r = r;
   pl->device = device;
@@ -448,12 +473,32 @@ int imask_plan_create(int side, int n_angles, int n_det, int angle_begin, int an
   const size_t img_bytes = sizeof(float) * (size_t)side * side;
   const size_t sino_bytes = sizeof(float) * (size_t)n_loc * n_det;
   int rc = IMASK_OK;
-  pl->sym = (angle_begin == 0 && angle_end == n_angles && n_angles % 2 == 0 && n_angles >= 4);
+  // Mirror symmetry (theta -> pi - theta is angle a -> n_angles - a): usable when
+  // the local rows are [angle 0 (optional)] + a list whose row i holds the
+  // mirror of row sym_s + n_loc - 1 - i (the full set 0..n-1 and the
+  // mirror-closed shards of shard_angles both have this layout).
+  pl->sym = false;
+  for (int s0 = 0; s0 <= 1 && !pl->sym; ++s0) {
+    if (n_loc - s0 < 2 || (s0 == 1 && angle_idx[0] != 0)) continue;
+    bool ok = true;
+    for (int i = s0; i < n_loc && ok; ++i) {
+      const int a = angle_idx[i], am = angle_idx[s0 + n_loc - 1 - i];
+      ok = a != 0 && am == n_angles - a;
+    }
+    if (ok) {
+      pl->sym = true;
+      pl->sym_s = s0;
+    }
+  }
   if (pl->sym) {
-    std::vector<int2> ent;
-    for (int a = 1; a < n_angles / 2; ++a) ent.push_back(make_int2(a, n_angles - a));
-    ent.push_back(make_int2(0, -1));             // tie rule not mirror-invariant
-    ent.push_back(make_int2(n_angles / 2, -1));  // self-mirrored
+    std::vector<int2> ent;  // local rows (row, mirror row or -1)
+    for (int i = 0; i < pl->sym_s; ++i) ent.push_back(make_int2(i, -1));  // angle 0 alone:
+                                                                         // tie rule not mirror-invariant
+    for (int i = pl->sym_s; i < n_loc; ++i) {
+      const int im = pl->sym_s + n_loc - 1 - i;
+      if (i < im) ent.push_back(make_int2(i, im));
+      else if (i == im) ent.push_back(make_int2(i, -1));  // self-mirrored (pi/2)
+    }
     pl->n_entries = (int)ent.size();
     // TMA forward: 8 entries of one ray family per CTA (rows vs columns of the image)
     std::vector<int2> rowf, colf;
@@ -543,6 +588,7 @@ int imask_plan_destroy(imask_plan* pl) {
 }
 
 int64_t imask_plan_scratch_bytes(const imask_plan* pl) { return pl ? pl->scratch : 0; }
+int imask_plan_symmetric(const imask_plan* pl) { return pl && pl->sym ? 1 : 0; }
 
 int imask_project(imask_plan* pl, int factor, const float* u, int64_t u_len, float* sino,
                   int64_t sino_len, void* stream) {

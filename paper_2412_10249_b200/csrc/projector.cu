@@ -876,16 +876,17 @@ void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_o
 // Mirror symmetry applies when the slab is the whole, even-sized angle set and
 // the left half of the image is a whole number of tiles (T is a power of two,
 // so n % (2T) == 0).
-bool adjoint_sym_ok(int n, int factor, int n_loc, bool full_even_set) {
+bool adjoint_sym_ok(int n, int factor, int n_loc, bool mirror_layout) {
   int T, S;
   adjoint_layout(n, factor, n_loc, false, &T, &S);
-  return full_even_set && n_loc >= 4 && n % (2 * T) == 0;
+  return mirror_layout && n_loc >= 2 && n % (2 * T) == 0;
 }
 
-int adjoint_planes(int n, int factor, int n_loc, bool sym) {
+int adjoint_planes(int n, int factor, int n_loc, bool sym, int sym_s) {
   int T, S;
   adjoint_layout(n, factor, n_loc, sym, &T, &S);
-  return sym ? S + 1 : (S > 1 ? S : 0);
+  const int planes = sym ? S + sym_s : S;
+  return planes > 1 ? planes : 0;
 }
 
 template <bool kPair, int T, bool kSym>
@@ -940,9 +941,9 @@ static void adj_reduce(const float* partial, float* out, int npix, int S, cudaSt
 }
 
 cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n, int factor,
-                           int n_loc, int n_det, const AdjAngle* ang, bool full_even_set,
+                           int n_loc, int n_det, const AdjAngle* ang, int sym_s,
                            cudaStream_t stream, const SideStream& side, int* launches) {
-  const bool sym = adjoint_sym_ok(n, factor, n_loc, full_even_set);
+  const bool sym = adjoint_sym_ok(n, factor, n_loc, sym_s >= 0);
   int T, S;
   adjoint_layout(n, factor, n_loc, sym, &T, &S);
   const bool pair = (factor == 1 && T == 32);
@@ -950,28 +951,36 @@ cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n,
   int CA;
   *launches = 0;
   if (sym) {
-    // angles 1 .. n_loc-1 with their mirrors over the left-half tiles, S planes;
-    // angle 0 through the plain kernel into plane S (on the side stream, if
-    // any, concurrently with the symmetric kernel); then the ordered reduction
-    cudaStream_t s0 = stream;
-    if (side.stream) {
-      cudaEventRecord(side.fork, stream);
-      cudaStreamWaitEvent(side.stream, side.fork, 0);
-      s0 = side.stream;
+    // rows [sym_s, n_loc) with their mirrors over the left-half tiles, S planes;
+    // the unpaired rows [0, sym_s) (angle 0) through the plain kernel into plane
+    // S (on the side stream, if any, concurrently with the symmetric kernel);
+    // then the ordered reduction
+    const int planes = S + sym_s;
+    if (sym_s > 0) {
+      cudaStream_t s0 = stream;
+      if (side.stream) {
+        cudaEventRecord(side.fork, stream);
+        cudaStreamWaitEvent(side.stream, side.fork, 0);
+        s0 = side.stream;
+      }
+      const size_t smem0 = adj_smem(pair, false, T, W, &CA);
+      dim3 grid0((n + T - 1) / T, (n + T - 1) / T, 1);
+      adj_dispatch(pair, T, false, grid0, smem0, s0, sino, partial + (size_t)S * n * n, n, W,
+                   CA, 0, sym_s, sym_s, n_loc, n_det, ang);
+      if (side.stream) cudaEventRecord(side.join, side.stream);
+      ++*launches;
     }
-    const size_t smem0 = adj_smem(pair, false, T, W, &CA);
-    dim3 grid0((n + T - 1) / T, (n + T - 1) / T, 1);
-    adj_dispatch(pair, T, false, grid0, smem0, s0, sino, partial + (size_t)S * n * n, n, W, CA,
-                 0, 1, 1, n_loc, n_det, ang);
-    if (side.stream) cudaEventRecord(side.join, side.stream);
     const size_t smem = adj_smem(pair, true, T, W, &CA);
-    const int per_split = (n_loc - 1 + S - 1) / S;
+    const int per_split = (n_loc - sym_s + S - 1) / S;
     dim3 grid(n / (2 * T), (n + T - 1) / T, S);
-    adj_dispatch(pair, T, true, grid, smem, stream, sino, partial, n, W, CA, 1, per_split, n_loc,
-                 n_loc, n_det, ang);
-    if (side.stream) cudaStreamWaitEvent(stream, side.join, 0);
-    adj_reduce(partial, out, n * n, S + 1, stream);
-    *launches = 3;
+    adj_dispatch(pair, T, true, grid, smem, stream, sino, planes > 1 ? partial : out, n, W, CA,
+                 sym_s, per_split, n_loc, sym_s + n_loc - 1, n_det, ang);
+    ++*launches;
+    if (sym_s > 0 && side.stream) cudaStreamWaitEvent(stream, side.join, 0);
+    if (planes > 1) {
+      adj_reduce(partial, out, n * n, planes, stream);
+      ++*launches;
+    }
     return cudaGetLastError();
   }
   const size_t smem = adj_smem(pair, false, T, W, &CA);

@@ -59,14 +59,18 @@ class Geometry:
         n = self.n_detectors
         return np.arange(n, dtype=float) - (n - 1) / 2.0
 
-    def cos_sin(self, begin: int = 0, end: Optional[int] = None):
-        """float64 cos/sin of angles [begin, end), snapped below 1e-14 (ctmodel.py:88-93).
+    def cos_sin(self, begin: int = 0, end: Optional[int] = None, angles=None):
+        """float64 cos/sin of angles [begin, end) (or of the index list ``angles``),
+        snapped below 1e-14 (ctmodel.py:88-93).
 
         The snap is decided here, in float64, and passed to the device, so the
         axis-parallel tie rule never depends on float32 rounding.
         """
-        end = self.n_angles if end is None else end
-        th = self.angles[begin:end]
+        if angles is not None:
+            th = self.angles[np.asarray(angles, dtype=np.int64)]
+        else:
+            end = self.n_angles if end is None else end
+            th = self.angles[begin:end]
         c = np.array([math.cos(t) for t in th])
         s = np.array([math.sin(t) for t in th])
         c[np.abs(c) < AXIS_SNAP] = 0.0
@@ -83,6 +87,34 @@ def slab_bounds(n_angles: int, rank: int, world: int) -> tuple[int, int]:
     return begin, begin + base + (1 if rank < extra else 0)
 
 
+def shard_angles(n_angles: int, rank: int, world: int) -> tuple:
+    """Mirror-closed angle shard of one rank (global indices, local row order).
+
+    Angle a and its mirror n_angles - a (theta -> pi - theta) always land on the
+    same rank, so every rank runs the mirror-symmetric kernels. The base angles
+    1..floor(n_angles/2) are split contiguously, balancing the row count (two
+    rows per base, one for the self-mirrored pi/2 and for angle 0, which rank 0
+    takes). Row order: [0 on rank 0] + bases ascending + mirrors ascending,
+    the layout imask_plan_create_list detects. world = 1 gives 0..n_angles-1.
+    """
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of world {world}")
+    if world == 1:
+        return tuple(range(n_angles))
+    bases = list(range(1, n_angles // 2 + 1))
+    weight = [1 if 2 * a == n_angles else 2 for a in bases]
+    cum = np.concatenate([[1], 1 + np.cumsum(weight)])  # rows up to and including base i (+ angle 0)
+    # rank k takes the bases whose cumulative row count falls in (k, k+1] * n_angles / world
+    edges = [0] + [int(np.searchsorted(cum[1:], (k + 1) * n_angles / world - 0.5)) + 1
+                   for k in range(world - 1)] + [len(bases)]
+    edges = [min(max(e, 0), len(bases)) for e in edges]
+    for k in range(1, len(edges)):
+        edges[k] = max(edges[k], edges[k - 1])
+    mine = bases[edges[rank]:edges[rank + 1]]
+    mirrors = sorted(n_angles - a for a in mine if 2 * a != n_angles)
+    return tuple(([0] if rank == 0 else []) + mine + mirrors)
+
+
 def _stream_ptr(device: torch.device) -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
@@ -91,8 +123,21 @@ def _ptr(t: torch.Tensor) -> ctypes.c_void_p:
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _angle_list(geom: Geometry, angles=None, angle_begin: int = 0,
+                angle_end: Optional[int] = None) -> tuple:
+    if angles is not None:
+        return tuple(int(a) for a in angles)
+    angle_end = geom.n_angles if angle_end is None else angle_end
+    return tuple(range(angle_begin, angle_end))
+
+
 class Plan:
-    """Native plan of one geometry, angle slab, sketch family and scale on one device."""
+    """Native plan of one geometry, angle set, sketch family and scale on one device.
+
+    ``angles`` (global indices, local row order) selects this rank's sinogram
+    rows; the default is all angles. ``angle_begin`` / ``angle_end`` select a
+    contiguous slab instead.
+    """
 
     def __init__(
         self,
@@ -103,27 +148,29 @@ class Plan:
         angle_begin: int = 0,
         angle_end: Optional[int] = None,
         device: Optional[torch.device] = None,
+        angles=None,
     ):
         self.geom = geom
         self.device = device or default_device()
-        self.angle_begin = angle_begin
-        self.angle_end = geom.n_angles if angle_end is None else angle_end
-        self.n_loc = self.angle_end - self.angle_begin
+        self.angles = _angle_list(geom, angles, angle_begin, angle_end)
+        self.n_loc = len(self.angles)
         self.m_loc = self.n_loc * geom.n_detectors
         self.r = int(r)
         self.probs = np.asarray(probs, dtype=float)
         self.scale = float(scale)
         self.factors = tuple(2 ** (self.r - i) for i in range(1, self.r + 1))
-        c, s = geom.cos_sin(self.angle_begin, self.angle_end)
+        c, s = geom.cos_sin(angles=self.angles)
         self._c = np.ascontiguousarray(c)
         self._s = np.ascontiguousarray(s)
+        self._idx = np.ascontiguousarray(np.asarray(self.angles, dtype=np.int32))
         dp = ctypes.POINTER(ctypes.c_double)
         handle = ctypes.c_void_p()
         L = _lib.lib()
         with torch.cuda.device(self.device):
             _lib.check(
-                L.imask_plan_create(
-                    geom.side, geom.n_angles, geom.n_detectors, self.angle_begin, self.angle_end,
+                L.imask_plan_create_list(
+                    geom.side, geom.n_angles, geom.n_detectors, self.n_loc,
+                    self._idx.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
                     self._c.ctypes.data_as(dp), self._s.ctypes.data_as(dp), self.r,
                     self.probs.ctypes.data_as(dp), self.scale, self.device.index, ctypes.byref(handle),
                 )
@@ -144,6 +191,11 @@ class Plan:
             except Exception:
                 pass
             self.handle = None
+
+    @property
+    def symmetric(self) -> bool:
+        """True when the mirror-symmetric kernels serve this plan's angle rows."""
+        return bool(_lib.lib().imask_plan_symmetric(self.handle))
 
     @property
     def stream(self) -> ctypes.c_void_p:
@@ -192,17 +244,15 @@ _plan_cache: dict = {}
 _plan_lock = threading.Lock()
 
 
-def get_plan(geom: Geometry, r=1, probs=(1.0,), scale=1.0, angle_begin=0, angle_end=None,
-             device=None) -> Plan:
-    """Cached plan per (geometry, family, scale, slab, device), like _projector_pair."""
+def get_plan(geom: Geometry, r=1, probs=(1.0,), scale=1.0, angles=None, device=None) -> Plan:
+    """Cached plan per (geometry, family, scale, angle set, device), like _projector_pair."""
     device = device or default_device()
-    angle_end = geom.n_angles if angle_end is None else angle_end
-    key = (geom, int(r), tuple(float(p) for p in probs), float(scale), angle_begin, angle_end,
-           str(device))
+    angles = _angle_list(geom, angles)
+    key = (geom, int(r), tuple(float(p) for p in probs), float(scale), angles, str(device))
     with _plan_lock:
         plan = _plan_cache.get(key)
         if plan is None:
-            plan = Plan(geom, r, probs, scale, angle_begin, angle_end, device)
+            plan = Plan(geom, r, probs, scale, device=device, angles=angles)
             _plan_cache[key] = plan
     return plan
 
@@ -214,30 +264,32 @@ class ProjectorMeta:
     geom: Geometry
     factor: int
     scale: float = 1.0
-    angle_begin: int = 0
-    angle_end: Optional[int] = None
+    angles: Optional[tuple] = None  # global angle indices of the rows (None: all)
 
     def scaled(self, alpha: float) -> "ProjectorMeta":
-        return ProjectorMeta(self.geom, self.factor, self.scale * alpha, self.angle_begin,
-                             self.angle_end)
+        return ProjectorMeta(self.geom, self.factor, self.scale * alpha, self.angles)
+
+    @property
+    def angle_list(self) -> tuple:
+        return _angle_list(self.geom, self.angles)
 
 
-def _projector_linop(geom: Geometry, factor: int, scale: float = 1.0, angle_begin: int = 0,
-                     angle_end: Optional[int] = None) -> LinOp:
-    """R_f restricted to the angle slab [angle_begin, angle_end) (all angles by default).
+def _projector_linop(geom: Geometry, factor: int, scale: float = 1.0, angles=None) -> LinOp:
+    """R_f restricted to the rows of ``angles`` (all angles by default).
 
     The plan is resolved at first apply (after the caller has picked its CUDA device).
     """
-    angle_end = geom.n_angles if angle_end is None else angle_end
+    angles = None if angles is None else tuple(int(a) for a in angles)
+    n_rows = geom.n_angles if angles is None else len(angles)
     low = geom.side // factor
-    meta = ProjectorMeta(geom, factor, scale, angle_begin, angle_end)
+    meta = ProjectorMeta(geom, factor, scale, angles)
 
     def plan():
-        return get_plan(geom, scale=scale, angle_begin=angle_begin, angle_end=angle_end)
+        return get_plan(geom, scale=scale, angles=angles)
 
     return LinOp(
         low * low,
-        (angle_end - angle_begin) * geom.n_detectors,
+        n_rows * geom.n_detectors,
         lambda x: plan().project(to_device(x), factor),
         lambda y: plan().backproject(to_device(y), factor),
         meta,

@@ -32,7 +32,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .ctmodel import Geometry, get_plan, slab_bounds
+from .ctmodel import Geometry, get_plan, shard_angles
 from .linops import LinOp, to_device
 from .mrsketch import SketchFamily, SketchedMeta, cost_fraction, forward_family
 from .proxlib import ProxFn
@@ -66,7 +66,8 @@ def draw_level(seed: int, k: int, cum_probs: np.ndarray) -> int:
 
 @dataclass(frozen=True)
 class Shard:
-    """This rank's angle slab and the process group the backprojection is reduced over."""
+    """This rank's angle shard (ctmodel.shard_angles) and the process group the
+    backprojection is reduced over."""
 
     rank: int = 0
     world: int = 1
@@ -77,11 +78,11 @@ class Engine:
     """Native state of the fused sketch_step for one problem on one device."""
 
     def __init__(self, geom: Geometry, family: SketchFamily, scale: float, mu_g: float,
-                 b: torch.Tensor, shard: Shard, begin: int, end: int):
+                 b: torch.Tensor, shard: Shard, angles: tuple):
         self.geom = geom
         self.family = family
         self.shard = shard
-        self.plan = get_plan(geom, family.r, tuple(family.probs), scale, begin, end)
+        self.plan = get_plan(geom, family.r, tuple(family.probs), scale, angles)
         self.device = self.plan.device
         self.mu_g = float(mu_g)
         self.b = b
@@ -170,13 +171,12 @@ class Problem:
             return None
         if self.g.kind != "ridge" or self.f_conj.kind != "quadratic_conjugate":
             return None
-        begin = proj.angle_begin
-        end = proj.geom.n_angles if proj.angle_end is None else proj.angle_end
-        if self.shard.world > 1 and (begin, end) != slab_bounds(
+        angles = proj.angle_list
+        if self.shard.world > 1 and angles != shard_angles(
                 proj.geom.n_angles, self.shard.rank, self.shard.world):
-            raise ValueError("projector angle slab does not match this rank's shard")
+            raise ValueError("projector angle set does not match this rank's shard")
         return Engine(proj.geom, self.family, proj.scale, self.g.param, self.f_conj.param,
-                      self.shard, begin, end)
+                      self.shard, angles)
 
 
 def make_problem(K: LinOp, b, family: SketchFamily, g: ProxFn, f_conj: ProxFn,

@@ -1,12 +1,15 @@
 """Angle-sharded multi-rank logic on CPU (world_size 2, gloo).
 
-The B200 path shards projection angles: each rank backprojects its slab and
-the partial images are summed by one all-reduce. These tests
-check, with the float64 oracle standing in for the device kernels, that
-slab-partial backprojections all-reduce to the full backprojection, that
-slab forward projections concatenate to the full sinogram, that every rank
-draws the identical level schedule from the C library, and that a sharded
-ImaSk iteration equals the unsharded one.
+The B200 path shards projection angles into mirror-closed shards
+(ctmodel.shard_angles: a and n - a on the same rank, so every rank runs the
+symmetric kernels): each rank backprojects its shard and the partial images
+are summed by one all-reduce. These tests check, with the
+float64 oracle standing in for the device kernels and the product's own
+sharding helpers (shard_angles, dist.local_rows), that shard-partial
+backprojections all-reduce to the full backprojection, that shard forward
+projections scatter back to the full sinogram, that every rank draws the
+identical level schedule from the C library, and that a sharded ImaSk
+iteration equals the unsharded one.
 """
 
 import os
@@ -19,7 +22,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import ct_oracle, sketch_oracle
-from paper_2412_10249_b200.ctmodel import slab_bounds
+from paper_2412_10249_b200 import dist as dist_mod
+from paper_2412_10249_b200.ctmodel import Geometry, shard_angles
 
 
 def _free_port():
@@ -30,32 +34,37 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, q):
+def _scatter_rows(part, idx, n_angles, n_det):
+    """This rank's rows placed into a zero full sinogram (summed over ranks)."""
+    full = np.zeros((n_angles, n_det))
+    full[np.asarray(idx)] = np.asarray(part).reshape(len(idx), n_det)
+    return torch.from_numpy(full.ravel())
+
+
+def _worker(rank, world, port, q, n_angles):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2412_10249_b200.solvers import draw_levels
 
-        side, n_angles, n_det, r = 32, 30, 47, 3
+        side, n_det, r = 32, 47, 3
         probs = [1 / 3] * 3
-        begin, end = slab_bounds(n_angles, rank, world)
+        idx = shard_angles(n_angles, rank, world)
         rng = np.random.default_rng(5)
         x = rng.standard_normal(side * side)
         y = rng.standard_normal(n_angles * n_det)
-        y_loc = y.reshape(n_angles, n_det)[begin:end].ravel()
+        y_loc = dist_mod.local_rows(Geometry(side, n_angles, n_det), y, rank, world)
         res = {}
         for f in (1, 2, 4):
-            op = ct_oracle.ProjectorOracle(side, n_angles, n_det, f, angle_idx=range(begin, end))
+            op = ct_oracle.ProjectorOracle(side, n_angles, n_det, f, angle_idx=idx)
             bp = torch.from_numpy(op.adjoint_apply(y_loc))
             dist.all_reduce(bp)
             res[f"bp{f}"] = bp.numpy()
             xl = sketch_oracle.decimate(x.reshape(side, side), f).ravel()
-            part = torch.from_numpy(op.apply(xl))
-            parts = [torch.zeros(n_det * (e - b), dtype=part.dtype)
-                     for b, e in (slab_bounds(n_angles, k, world) for k in range(world))]
-            dist.all_gather(parts, part)
-            res[f"fw{f}"] = torch.cat(parts).numpy()
+            full = _scatter_rows(op.apply(xl), idx, n_angles, n_det)
+            dist.all_reduce(full)
+            res[f"fw{f}"] = full.numpy()
         sched = torch.from_numpy(draw_levels(99, 0, 256, np.cumsum(probs)).astype(np.int64))
         all_s = [torch.zeros_like(sched) for _ in range(world)]
         dist.all_gather(all_s, sched)
@@ -67,19 +76,21 @@ def _worker(rank, world, port, q):
 
 
 @pytest.mark.timeout(300)
-def test_sharded_projections_world2():
+@pytest.mark.parametrize("n_angles", [30, 31])
+def test_sharded_projections_world2(n_angles):
     world = 2
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, n_angles))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = q.get(timeout=240)
     for p in procs:
         p.join(60)
         assert p.exitcode == 0
-    side, n_angles, n_det = 32, 30, 47
+    side, n_det = 32, 47
     rng = np.random.default_rng(5)
     x = rng.standard_normal(side * side)
     y = rng.standard_normal(n_angles * n_det)
@@ -100,11 +111,11 @@ def _step_worker(rank, world, port, q):
         from oracle import solver_oracle as so
 
         side, n_angles, n_det, probs = 32, 30, 47, [1 / 3] * 3
-        begin, end = slab_bounds(n_angles, rank, world)
-        ops = so.SketchedCT(side, n_angles, n_det, probs, angle_idx=range(begin, end))
+        idx = shard_angles(n_angles, rank, world)
+        ops = so.SketchedCT(side, n_angles, n_det, probs, angle_idx=idx)
         rng = np.random.default_rng(8)
         b_full = rng.standard_normal(n_angles * n_det)
-        b = b_full.reshape(n_angles, n_det)[begin:end].ravel()
+        b = dist_mod.local_rows(Geometry(side, n_angles, n_det), b_full, rank, world)
         st = so.init_state(ops, seed=4)
         sigma, mu, mu_g = 1e-3, 1e-2, 1e-2
         cum = np.cumsum(probs)
@@ -123,11 +134,10 @@ def _step_worker(rank, world, port, q):
             st.x = (st.x - s * xi) / (1 + s * mu_g)
             st.y = ((st.y + sigma * zeta) - sigma * b) / (1 + sigma)
             st.k += 1
-        ys = [torch.zeros(n_det * (e - bb), dtype=torch.float64)
-              for bb, e in (slab_bounds(n_angles, k, world) for k in range(world))]
-        dist.all_gather(ys, torch.from_numpy(st.y))
+        y_full = _scatter_rows(st.y, idx, n_angles, n_det)
+        dist.all_reduce(y_full)
         if rank == 0:
-            q.put({"x": st.x, "y": torch.cat(ys).numpy()})
+            q.put({"x": st.x, "y": y_full.numpy()})
     finally:
         dist.destroy_process_group()
 

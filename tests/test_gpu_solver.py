@@ -96,6 +96,59 @@ def test_double_buffered_dual_matches_in_place(graphs):
         assert np.array_equal(host(a), host(c))
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_phases_match_single_gpu(world):
+    """The multi-GPU step emulated in one process: every rank's
+    mirror-closed shard runs step_adjoint on its own plan, the partial coarse
+    backprojections are summed (the NCCL all-reduce), then step_forward and
+    step_image; x stays identical across ranks and matches the single-GPU run."""
+    import ctypes
+
+    from paper_2412_10249_b200 import _lib
+    from paper_2412_10249_b200 import dist as dist_mod
+
+    side, na, nd, probs, mu_g = 64, 90, 91, [0.3, 0.3, 0.2, 0.2], 1e-2
+    geom = ctmodel.Geometry(side, na, nd)
+    orc = so.SketchedCT(side, na, nd, probs)
+    b = orc.proj[1].apply(np.random.default_rng(6).random(side * side))
+    fam = mrsketch.make_family(4, side, probs, mode="coarse")
+    single = dist_mod.make_sharded_problem(geom, b, fam, mu_g)
+    st1 = solvers.init_state(single, seed=2)
+    ranks = []
+    for rank in range(world):
+        pr = dist_mod.make_sharded_problem(geom, dist_mod.local_rows(geom, b, rank, world), fam,
+                                           mu_g, rank, world)
+        assert pr.engine.plan.symmetric
+        ranks.append((pr, solvers.init_state(pr, seed=2)))
+    prm = solvers._params(2e-4, 1e-2, mu_g)
+    L = _lib.lib()
+    sched = solvers.draw_levels(2, 0, 10, single.cum_probs)
+    for lv in (int(v) for v in sched):
+        solvers._device_step(single.engine, st1, lv, prm)
+        n = (side // single.engine.plan.factors[lv]) ** 2
+        for pr, st in ranks:
+            _lib.check(L.imask_step_adjoint(pr.engine.plan.handle,
+                                            ctypes.byref(st.c_state(pr.engine.b)), lv,
+                                            pr.engine.plan.stream))
+        total = sum(st.bp[:n].clone() for _, st in ranks)
+        for pr, st in ranks:
+            st.bp[:n].copy_(total)
+            cst = ctypes.byref(st.c_state(pr.engine.b))
+            _lib.check(L.imask_step_forward(pr.engine.plan.handle, cst, lv, ctypes.byref(prm),
+                                            pr.engine.plan.stream))
+            _lib.check(L.imask_step_image(pr.engine.plan.handle, cst, lv, ctypes.byref(prm),
+                                          pr.engine.plan.stream))
+            st.swap_dual()
+    x0 = host(ranks[0][1].x)
+    for _, st in ranks[1:]:
+        assert np.array_equal(host(st.x), x0)
+    assert rel_l2(x0, host(st1.x)) <= 1e-5
+    y1 = host(st1.y).reshape(na, nd)
+    for rank, (_, st) in enumerate(ranks):
+        idx = list(ctmodel.shard_angles(na, rank, world))
+        assert rel_l2(host(st.y).reshape(len(idx), nd), y1[idx]) <= 1e-5
+
+
 def test_resum_matches_direct_sums():
     side, na, nd, probs = 32, 36, 47, [0.3, 0.3, 0.2, 0.2]
     orc = so.SketchedCT(side, na, nd, probs)

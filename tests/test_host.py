@@ -8,7 +8,7 @@ import pytest
 
 from oracle import ct_oracle
 from paper_2412_10249_b200 import mrsketch
-from paper_2412_10249_b200.ctmodel import Geometry, slab_bounds
+from paper_2412_10249_b200.ctmodel import Geometry, shard_angles, slab_bounds
 from paper_2412_10249_b200.synth import CONFIGS, ellipse_phantom
 
 
@@ -40,6 +40,24 @@ def test_slabs_partition_angles(n, world):
         assert e0 == b1
     sizes = [e - b for b, e in bounds]
     assert max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.parametrize("n,world", [(180, 8), (1440, 8), (1440, 3), (90, 4), (7, 3), (9, 2),
+                                     (2048, 2), (5, 1), (6, 4)])
+def test_shards_partition_angles_mirror_closed(n, world):
+    shards = [shard_angles(n, r, world) for r in range(world)]
+    flat = [a for sh in shards for a in sh]
+    assert sorted(flat) == list(range(n))  # a partition of all angles
+    sizes = [len(sh) for sh in shards]
+    assert max(sizes) - min(sizes) <= 3
+    for rank, sh in enumerate(shards):
+        # the row layout imask_plan_create_list turns into mirror-symmetric kernels:
+        # [0 on rank 0] + rows i <-> s + n_loc - 1 - i holding a and n - a
+        s0 = 1 if rank == 0 else 0
+        assert (0 in sh) == (rank == 0) and (rank != 0 or sh[0] == 0)
+        rows = sh[s0:]
+        for i, a in enumerate(rows):
+            assert rows[len(rows) - 1 - i] == n - a
 
 
 def test_family_validation_messages():
