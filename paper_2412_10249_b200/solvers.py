@@ -104,6 +104,12 @@ class Engine:
             self._graphs[key] = hit
         return hit
 
+    def side_stream(self) -> torch.cuda.Stream:
+        """Stream of the forward chain in angle-sharded steps (created on first use)."""
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        return self._side
+
     def capture_all(self, state: "SaddleState", prm) -> None:
         """Capture the graphs of every level for both dual buffers (outside timing)."""
         for _ in range(2 if state.y_alt is not None else 1):
@@ -324,14 +330,27 @@ def _device_step(eng: Engine, state: SaddleState, level0: int, prm: _lib.ImaskSt
         _lib.check(L.imask_sketch_step(h, cst, level0, ctypes.byref(prm), s))
         state.swap_dual()
         return _lib.last_launch_count()
-    # angle-sharded: adjoint -> all-reduce (NCCL stream) || forward -> image update
+    # angle-sharded: adjoint -> all-reduce of the coarse partial (NCCL stream); the
+    # forward chain overlaps both (side stream when the dual is double-buffered,
+    # else after the adjoint on this stream); then the replicated image update
     n = (eng.geom.side // eng.plan.factors[level0]) ** 2
+    main = torch.cuda.current_stream(eng.device)
+    side = eng.side_stream() if state.y_alt is not None else None
+    launches = 0
+    if side is not None:
+        side.wait_stream(main)
+        _lib.check(L.imask_step_forward(h, cst, level0, ctypes.byref(prm),
+                                        ctypes.c_void_p(side.cuda_stream)))
+        launches += _lib.last_launch_count()
     _lib.check(L.imask_step_adjoint(h, cst, level0, s))
-    launches = _lib.last_launch_count()
-    work = _allreduce(eng, state.bp[:n], async_op=True)
-    _lib.check(L.imask_step_forward(h, cst, level0, ctypes.byref(prm), s))
     launches += _lib.last_launch_count()
+    work = _allreduce(eng, state.bp[:n], async_op=True)
+    if side is None:
+        _lib.check(L.imask_step_forward(h, cst, level0, ctypes.byref(prm), s))
+        launches += _lib.last_launch_count()
     work.wait()
+    if side is not None:
+        main.wait_stream(side)
     _lib.check(L.imask_step_image(h, cst, level0, ctypes.byref(prm), s))
     state.swap_dual()
     return launches + _lib.last_launch_count()

@@ -149,6 +149,42 @@ def test_sharded_phases_match_single_gpu(world):
         assert rel_l2(host(st.y).reshape(len(idx), nd), y1[idx]) <= 1e-5
 
 
+def test_sharded_device_step_stream_ordering(monkeypatch):
+    """solvers._device_step's multi-GPU branch (forward chain on a side stream,
+    adjoint + all-reduce on the main stream) on rank 0 of a 2-rank shard, with
+    the collective stubbed out, equals the three phases run back to back."""
+    import ctypes
+
+    from paper_2412_10249_b200 import _lib
+    from paper_2412_10249_b200 import dist as dist_mod
+
+    class _Done:
+        def wait(self):
+            pass
+
+    monkeypatch.setattr(solvers, "_allreduce", lambda eng, t, async_op=False: _Done())
+    side, na, nd, probs, mu_g = 64, 90, 91, [0.3, 0.3, 0.2, 0.2], 1e-2
+    geom = ctmodel.Geometry(side, na, nd)
+    b = np.random.default_rng(7).standard_normal(geom.m)
+    fam = mrsketch.make_family(4, side, probs, mode="coarse")
+    pr = dist_mod.make_sharded_problem(geom, dist_mod.local_rows(geom, b, 0, 2), fam, mu_g, 0, 2)
+    st_a = solvers.init_state(pr, seed=9)
+    st_b = solvers.init_state(pr, seed=9)
+    st_b.y_alt = None  # in-place reference: phases strictly in order
+    prm = solvers._params(2e-4, 1e-2, mu_g)
+    L = _lib.lib()
+    h, s = pr.engine.plan.handle, pr.engine.plan.stream
+    for lv in (3, 0, 2, 1, 3, 3, 0):
+        solvers._device_step(pr.engine, st_a, lv, prm)
+        cst = ctypes.byref(st_b.c_state(pr.engine.b))
+        _lib.check(L.imask_step_adjoint(h, cst, lv, s))
+        _lib.check(L.imask_step_forward(h, cst, lv, ctypes.byref(prm), s))
+        _lib.check(L.imask_step_image(h, cst, lv, ctypes.byref(prm), s))
+    for a, c in ((st_a.x, st_b.x), (st_a.y, st_b.y), (st_a.phi_sum, st_b.phi_sum),
+                 (st_a.psi_sum, st_b.psi_sum)):
+        assert np.array_equal(host(a), host(c))
+
+
 def test_resum_matches_direct_sums():
     side, na, nd, probs = 32, 36, 47, [0.3, 0.3, 0.2, 0.2]
     orc = so.SketchedCT(side, na, nd, probs)
