@@ -228,8 +228,9 @@ k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
 // ---- TMA-staged mirror-symmetric forward ---------------------------------------
 //
 // Same rays and arithmetic as k_forward_sym, but the image data come from
-// shared memory: a CTA (8 warps = 8 angle entries of one family, each with its
-// mirror, x 32 detectors) walks its bands in chunks of kFB; for every chunk the
+// shared memory: a CTA (8 angle entries of one family, each with its mirror,
+// x 32 detectors; a warp takes 4 entries x 8 detectors) walks its bands in
+// chunks of kFB; for every chunk the
 // exact window of kFWc pair columns its rays touch is fetched for the image
 // and its mirror by two cp.async.bulk.tensor.2d loads (double-buffered,
 // mbarrier full/empty pipeline; TMA zero-fills outside the tensor). The warps
@@ -279,7 +280,7 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 
 struct FwdWarpInfo {
   long long x0_first, x0_last, step;
-  int lo, hi;  // union of the warp's band ranges (lo >= hi: idle)
+  int lo, hi;  // union of the lockstep band ranges (lo >= hi: idle)
 };
 
 template <bool kSaga>
@@ -296,14 +297,19 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   uint64_t* empty = full + 2;
   FwdWarpInfo* info = reinterpret_cast<FwdWarpInfo*>(empty + 2);
   int* cmin_tab = reinterpret_cast<int*>(info + 8);
-  int* ctl = cmin_tab + kFMaxChunks;  // [0] overflow, [1] first band, [2] chunks
+  int* ctl = cmin_tab + kFMaxChunks;  // [0] overflow, [1] first band, [2] chunks, then cmax_tab
 
+  // A warp holds 4 angles x 8 consecutive detectors (lane = 8 q + d): each
+  // half-warp's 8-byte window reads then span ~10 pair columns of one band,
+  // never two slots 16 apart (the bank period), so a read is 2 wavefronts
+  // where 32 detectors of one angle (up to 45 columns) cost up to 4.
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int e = blockIdx.y * 8 + warp;
+  const int q4 = lane >> 3;
+  const int e = blockIdx.y * 8 + (warp >> 2) * 4 + q4;
   const int2 ent = e < n_entries ? entries[e] : make_int2(-1, -1);
   const int a = ent.x, am = ent.y;
   const bool valid = a >= 0;
-  const int j = blockIdx.x * 32 + lane;
+  const int j = blockIdx.x * 32 + (warp & 3) * 8 + (lane & 7);
   const int jr = min(j, n_det - 1);
   FwdAngle A{};
   if (valid) A = ang[a];
@@ -328,9 +334,26 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
     wlo = min(wlo, __shfl_xor_sync(0xffffffffu, wlo, o));
     whi = max(whi, __shfl_xor_sync(0xffffffffu, whi, o));
   }
-  const long long x_last = __shfl_sync(0xffffffffu, X0, 31);
-  if (lane == 0) {
-    info[warp] = FwdWarpInfo{X0, x_last, A.step, wlo, whi};
+  // per angle slot (8 per CTA): positions of its first and last detector and the
+  // union of the lockstep band ranges of the four warps holding it (every lane
+  // walks its warp's whole range)
+  int* cmax_tab = ctl + 4;  // [kFMaxChunks]
+  if (threadIdx.x < 8) {
+    info[threadIdx.x] = FwdWarpInfo{0, 0, 0, n, 0};
+    ctl[0] = 0;
+  }
+  __syncthreads();
+  const int slot = (warp >> 2) * 4 + q4;
+  if ((lane & 7) == 0 && valid) {
+    FwdWarpInfo& I = info[slot];
+    if ((warp & 3) == 0) I.x0_first = X0;
+    if ((warp & 3) == 0) I.step = A.step;
+    atomicMin(&I.lo, wlo);
+    atomicMax(&I.hi, whi);
+  }
+  {
+    const long long x_last = __shfl_sync(0xffffffffu, X0, lane | 7);
+    if ((lane & 7) == 0 && valid && (warp & 3) == 3) info[slot].x0_last = x_last;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -339,34 +362,40 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
       blo = min(blo, info[w].lo);
       bhi = max(bhi, info[w].hi);
     }
-    ctl[0] = 0;
     ctl[1] = blo;
     ctl[2] = bhi > blo ? (bhi - blo + kFB - 1) / kFB : 0;
     if (ctl[2] > kFMaxChunks) ctl[0] = 1;
   }
   __syncthreads();
   const int blo = ctl[1], nch = ctl[2];
-  // window (first pair column) of every chunk: extremes of the affine positions
-  for (int t = threadIdx.x; t < nch && !ctl[0]; t += blockDim.x) {
-    const int b0 = blo + t * kFB;
-    int cmn = INT_MAX, cmx = INT_MIN;
-    for (int w = 0; w < 8; ++w) {
-      const FwdWarpInfo& I = info[w];
+  // window (first pair column) of every chunk: extremes of the affine positions,
+  // one (chunk, angle slot) item per thread
+  if (!ctl[0]) {
+    for (int t = threadIdx.x; t < nch; t += blockDim.x) {
+      cmin_tab[t] = INT_MAX;
+      cmax_tab[t] = INT_MIN;
+    }
+    __syncthreads();
+    for (int it = threadIdx.x; it < nch * 8; it += blockDim.x) {
+      const int t = it >> 3;
+      const FwdWarpInfo& I = info[it & 7];
+      const int b0 = blo + t * kFB;
       const int bs = max(b0, I.lo), be = min(b0 + kFB, I.hi) - 1;
       if (bs > be) continue;
-      const int c[4] = {(int)((I.x0_first + bs * I.step) >> 32), (int)((I.x0_first + be * I.step) >> 32),
-                        (int)((I.x0_last + bs * I.step) >> 32), (int)((I.x0_last + be * I.step) >> 32)};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        cmn = min(cmn, c[q]);
-        cmx = max(cmx, c[q]);
-      }
+      const int c0 = (int)((I.x0_first + bs * I.step) >> 32), c1 = (int)((I.x0_first + be * I.step) >> 32),
+                c2 = (int)((I.x0_last + bs * I.step) >> 32), c3 = (int)((I.x0_last + be * I.step) >> 32);
+      atomicMin(&cmin_tab[t], min(min(c0, c1), min(c2, c3)));
+      atomicMax(&cmax_tab[t], max(max(c0, c1), max(c2, c3)));
     }
-    if (cmn > cmx) cmn = cmx = 0;  // no warp walks this chunk
-    // TMA needs a 16-byte aligned start in the inner dimension: even pair index
-    const int corig = ((cmn + 1 + kPadC) & ~1) - 1 - kPadC;
-    if (cmx - corig + 1 > kFWc) atomicExch(&ctl[0], 1);
-    cmin_tab[t] = corig;
+    __syncthreads();
+    for (int t = threadIdx.x; t < nch; t += blockDim.x) {
+      int cmn = cmin_tab[t], cmx = cmax_tab[t];
+      if (cmn > cmx) cmn = cmx = 0;  // no warp walks this chunk
+      // TMA needs a 16-byte aligned start in the inner dimension: even pair index
+      const int corig = ((cmn + 1 + kPadC) & ~1) - 1 - kPadC;
+      if (cmx - corig + 1 > kFWc) atomicExch(&ctl[0], 1);
+      cmin_tab[t] = corig;
+    }
   }
   __syncthreads();
   // one ray family per CTA: the host puts the row-family CTAs first, so the
@@ -490,7 +519,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
 
 size_t forward_tma_smem() {
   return 2 * 2 * kFB * kFWc * sizeof(float2) + 4 * sizeof(uint64_t) + 8 * sizeof(FwdWarpInfo) +
-         (kFMaxChunks + 4) * sizeof(int);
+         (2 * kFMaxChunks + 4) * sizeof(int);
 }
 
 cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float2* PT,
@@ -864,7 +893,16 @@ void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_o
   if (T > np2) T = np2;
   int tiles = ((n + T - 1) / T) * ((n + T - 1) / T);
   if (sym) tiles /= 2;
-  const int target = (factor == 1 ? 20 : 16) * 148;
+  int per_sm = factor == 1 ? 20 : 16;
+  if (const char* e = getenv("IMASK_ADJ_CTAS")) {  // tuning: "f:ctas_per_sm,..."
+    for (const char* q = e; *q;) {
+      int ff = 0, cc = 0;
+      if (sscanf(q, "%d:%d", &ff, &cc) == 2 && ff == factor && cc > 0) per_sm = cc;
+      while (*q && *q != ',') ++q;
+      if (*q) ++q;
+    }
+  }
+  const int target = per_sm * 148;
   int S = (target + tiles - 1) / tiles;
   const int max_s = n_loc / 8 > 1 ? n_loc / 8 : 1;
   if (S > max_s) S = max_s;
