@@ -306,7 +306,11 @@ int run_forward(imask_plan* pl, int f, const LevelTables* t, float* sino, const 
   ++g_launches;
   cudaError_t e;
   // TMA staging pays off where the band walks are long; coarse grids use L1 loads
-  if (t->tma && pl->tma_entries && n > 128)
+  static const int tma_min_n = [] {
+    const char* e = std::getenv("IMASK_TMA_MIN_N");  // tuning / A-B runs
+    return e ? std::atoi(e) : 128;
+  }();
+  if (t->tma && pl->tma_entries && n >= tma_min_n)
     e = launch_forward_tma(t->maps, pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->tma_entries,
                            pl->n_tma_entries, pl->tma_row_ctas, pl->n_det, sino, saga, s);
   else

@@ -82,6 +82,28 @@ __device__ __forceinline__ float onep_from_frac(uint32_t frac) {
   return __uint_as_float((frac >> 9) | 0x3F800000u);
 }
 
+// Packed FP32 (FADD2 / FFMA2, sm_100): both lanes of a float2 in one
+// instruction, each rounded exactly like the scalar fadd / fmaf.
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+  return r;
+}
+// c + g * b with the scalar g broadcast
+__device__ __forceinline__ float2 ffma2(float g, float2 b, float2 c) {
+  float2 r;
+  const float2 gg = make_float2(g, g);
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&gg)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&c)));
+  return r;
+}
+
 struct SinoSaga {  // sinogram side of the SAGA step, fused into the forward epilogue
   float* psi_tab;        // level row of the psi table
   float* psi_sum;

@@ -168,47 +168,35 @@ k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
   Fix32 Y = fix_from(X0 + (long long)wlo * dYl + ((long long)(1 + kPadC) << 32));
   const Fix32 dY = fix_from(dYl);
   const float S = A.S, B = A.B;
-  float acc = 0.f, accm = 0.f;
+  // img holds value pairs (u, um), imgm difference pairs (d, dm) (k_prepare):
+  // (acc, accm) += (u, um) + g * (d, dm) with packed FP32 ops
+  float2 acc2 = make_float2(0.f, 0.f);
   int b = wlo;
-  if (am >= 0) {
 #pragma unroll 1
-    for (; b + 4 <= whi; b += 4) {
-      float2 v[4], vm[4];
-      float g[4];
+  for (; b + 4 <= whi; b += 4) {
+    float2 v[4], vd[4];
+    float g[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        v[k] = __ldg(img + Y.hi);
-        vm[k] = __ldg(imgm + Y.hi);
-        g[k] = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
-        fix_add(Y, dY);
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        acc += v[k].x;
-        acc = fmaf(g[k], v[k].y, acc);
-        accm += vm[k].x;
-        accm = fmaf(g[k], vm[k].y, accm);
-      }
-    }
-    for (; b < whi; ++b) {
-      const float2 v = __ldg(img + Y.hi), vm = __ldg(imgm + Y.hi);
-      const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
-      acc += v.x;
-      acc = fmaf(g, v.y, acc);
-      accm += vm.x;
-      accm = fmaf(g, vm.y, accm);
+    for (int k = 0; k < 4; ++k) {
+      v[k] = __ldg(img + Y.hi);
+      vd[k] = __ldg(imgm + Y.hi);
+      g[k] = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
       fix_add(Y, dY);
     }
-  } else {
-#pragma unroll 4
-    for (; b < whi; ++b) {
-      const float2 v = __ldg(img + Y.hi);
-      const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
-      acc += v.x;
-      acc = fmaf(g, v.y, acc);
-      fix_add(Y, dY);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      acc2 = fadd2(acc2, v[k]);
+      acc2 = ffma2(g[k], vd[k], acc2);
     }
   }
+  for (; b < whi; ++b) {
+    const float2 v = __ldg(img + Y.hi), vd = __ldg(imgm + Y.hi);
+    const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
+    acc2 = fadd2(acc2, v);
+    acc2 = ffma2(g, vd, acc2);
+    fix_add(Y, dY);
+  }
+  const float acc = acc2.x, accm = acc2.y;
   if (j < n_det) {
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
@@ -401,7 +389,9 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   // one ray family per CTA: the host puts the row-family CTAs first, so the
   // family (and the tensor-map pointers below) is uniform, derived from blockIdx
   const bool trans = (int)blockIdx.y >= row_ctas;
-  float acc = 0.f, accm = 0.f;
+  // value pairs (u, um) and difference pairs (d, dm) (k_prepare's symmetric
+  // layout): (acc, accm) += (u, um) + g * (d, dm) with packed FP32 ops
+  float2 acc2 = make_float2(0.f, 0.f);
   const float S = A.S, B = A.B;
 
   if (ctl[0]) {
@@ -413,12 +403,10 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
       Fix32 Y = fix_from(X0 + (long long)wlo * dYl + ((long long)(1 + kPadC) << 32));
       const Fix32 dY = fix_from(dYl);
       for (int b = wlo; b < whi; ++b) {
-        const float2 v = __ldg(img + Y.hi), vm = __ldg(imgm + Y.hi);
+        const float2 v = __ldg(img + Y.hi), vd = __ldg(imgm + Y.hi);
         const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
-        acc += v.x;
-        acc = fmaf(g, v.y, acc);
-        accm += vm.x;
-        accm = fmaf(g, vm.y, accm);
+        acc2 = fadd2(acc2, v);
+        acc2 = ffma2(g, vd, acc2);
         fix_add(Y, dY);
       }
     }
@@ -453,36 +441,33 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
       mbar_wait(&full[s], (i >> 1) & 1);
       const int bs = max(b0, wlo), be = min(b0 + kFB, whi);
       if (valid && bs < be) {
-        const float2* win = stage + (s * 2 + 0) * kBox;
-        const float2* winm = stage + (s * 2 + 1) * kBox;
+        // the stage's value window, with the difference window kBox elements on;
+        // the stage offset rides in the position's integer word
+        const float2* win = stage;
         const long long X = X0 + (long long)bs * A.step;
-        Fix32 Y = fix_from(X + ((long long)((bs - b0) * kFWc - cmin_tab[i]) << 32));
+        Fix32 Y = fix_from(X + ((long long)((bs - b0) * kFWc - cmin_tab[i] + s * 2 * kBox) << 32));
         int b = bs;
         for (; b + 4 <= be; b += 4) {
-          float2 v[4], vm[4];
+          float2 v[4], vd[4];
           float g[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             v[k] = win[Y.hi];
-            vm[k] = winm[Y.hi];
+            vd[k] = win[Y.hi + kBox];
             g[k] = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
             fix_add(Y, dYw);
           }
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            acc += v[k].x;
-            acc = fmaf(g[k], v[k].y, acc);
-            accm += vm[k].x;
-            accm = fmaf(g[k], vm[k].y, accm);
+            acc2 = fadd2(acc2, v[k]);
+            acc2 = ffma2(g[k], vd[k], acc2);
           }
         }
         for (; b < be; ++b) {
-          const float2 v = win[Y.hi], vm = winm[Y.hi];
+          const float2 v = win[Y.hi], vd = win[Y.hi + kBox];
           const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
-          acc += v.x;
-          acc = fmaf(g, v.y, acc);
-          accm += vm.x;
-          accm = fmaf(g, vm.y, accm);
+          acc2 = fadd2(acc2, v);
+          acc2 = ffma2(g, vd, acc2);
           fix_add(Y, dYw);
         }
       }
@@ -506,7 +491,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
     for (int r = 0; r < 2; ++r) {
       const int row = r == 0 ? a : am;
       if (row < 0) break;
-      const float val = (r == 0 ? acc : accm) * A.wsc;
+      const float val = (r == 0 ? acc2.x : acc2.y) * A.wsc;
       const size_t q = (size_t)row * n_det + j;
       if (kSaga) {
         sino_update(saga, q, sin[r], val);

@@ -238,10 +238,12 @@ k_saga_image_coarse32(const float* __restrict__ bp, int side, int f, float inv_f
 // kPadC zero columns on each side (imask_common.cuh):
 //   P  [R][c + 1 + kPadC] = (u[R][c], u[R][c+1] - u[R][c])          c in [-1-kPadC, n-1+kPadC]
 //   PT [C][r + 1 + kPadC] = (u[r][C], u[r+1][C] - u[r][C])          r in [-1-kPadC, n-1+kPadC]
-// and, for the mirror-symmetric forward (PM != nullptr), the same layouts of
-// the left-right mirrored image um[R][c] = u[R][n-1-c]:
-//   PM [R][c + 1 + kPadC] = (u[R][n-1-c], u[R][n-2-c] - u[R][n-1-c])
-//   PTM[C][.]             = PT[n-1-C][.]
+// For the mirror-symmetric forward (PM != nullptr) the pairs of u and of the
+// left-right mirrored image um[R][c] = u[R][n-1-c] (whose transposed layout is
+// PT with its bands reversed) are regrouped as value and difference planes,
+// so one 8-byte read feeds a ray and its mirror with packed FP32 adds:
+//   P  [R][i] = (P_u[R][i].x,  P_um[R][i].x)    PM [R][i] = (P_u[R][i].y,  P_um[R][i].y)
+//   PT [C][i] = (PT[C][i].x, PT[n-1-C][i].x)    PTM[C][i] = (PT[C][i].y, PT[n-1-C][i].y)
 // with u = 0 outside the image. The grid tiles the padded index range in both
 // dimensions; each 32x32 tile (plus a one-element halo on each side) is staged
 // in shared memory so the row-major and the transposed writes are coalesced.
@@ -264,11 +266,20 @@ k_prepare(const float* __restrict__ u, int n, float2* __restrict__ P, float2* __
       const int R = r0 + rr, C = c0 + cc, idx = C + 1 + kPadC;
       if (R >= 0 && R < n && idx < pitch) {
         const float v = t[rr][cc + 1];
-        P[(size_t)R * pitch + idx] = make_float2(v, t[rr][cc + 2] - v);
-        if (PM) {
-          // mirrored column c' = n-1-C holds (u[C], u[C-1] - u[C])
+        if (!PM) {
+          P[(size_t)R * pitch + idx] = make_float2(v, t[rr][cc + 2] - v);
+        } else {
+          // value planes (u, um) in P and difference planes (d, dm) in PM; the
+          // mirrored column c' = n-1-C holds (um, dm) = (u[C], u[C-1] - u[C])
+          float* pu = reinterpret_cast<float*>(P + (size_t)R * pitch);
+          float* pd = reinterpret_cast<float*>(PM + (size_t)R * pitch);
+          pu[2 * idx] = v;
+          pd[2 * idx] = t[rr][cc + 2] - v;
           const int idm = n - 1 - C + 1 + kPadC;
-          if (idm >= 0 && idm < pitch) PM[(size_t)R * pitch + idm] = make_float2(v, t[rr][cc] - v);
+          if (idm >= 0 && idm < pitch) {
+            pu[2 * idm + 1] = v;
+            pd[2 * idm + 1] = t[rr][cc] - v;
+          }
         }
       }
     }
@@ -277,9 +288,16 @@ k_prepare(const float* __restrict__ u, int n, float2* __restrict__ P, float2* __
       const int C = c0 + rr, idx = r0 + cc + 1 + kPadC;
       if (C >= 0 && C < n && idx < pitch) {
         const float v = t[cc][rr + 1];
-        const float2 pr = make_float2(v, t[cc + 1][rr + 1] - v);
-        PT[(size_t)C * pitch + idx] = pr;
-        if (PTM) PTM[(size_t)(n - 1 - C) * pitch + idx] = pr;
+        const float dv = t[cc + 1][rr + 1] - v;
+        if (!PTM) {
+          PT[(size_t)C * pitch + idx] = make_float2(v, dv);
+        } else {
+          // band C of the transposed image and band n-1-C of its mirror
+          reinterpret_cast<float*>(PT + (size_t)C * pitch)[2 * idx] = v;
+          reinterpret_cast<float*>(PTM + (size_t)C * pitch)[2 * idx] = dv;
+          reinterpret_cast<float*>(PT + (size_t)(n - 1 - C) * pitch)[2 * idx + 1] = v;
+          reinterpret_cast<float*>(PTM + (size_t)(n - 1 - C) * pitch)[2 * idx + 1] = dv;
+        }
       }
     }
   }
