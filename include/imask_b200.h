@@ -198,6 +198,13 @@ typedef struct imask_graph imask_graph;
 IMASK_API int imask_step_graph_create(imask_plan* plan, const imask_state* st, int level0,
                                       const imask_step_params* prm, imask_graph** out,
                                       int* launches);
+/* Re-target an existing step graph to another state / step parameters of the
+ * same plan and level (new kernel arguments, same topology): the graph is
+ * re-captured and the executable graph patched in place (cudaGraphExecUpdate),
+ * which costs a fraction of a fresh instantiation. */
+IMASK_API int imask_step_graph_update(imask_graph* graph, imask_plan* plan,
+                                      const imask_state* st, int level0,
+                                      const imask_step_params* prm);
 IMASK_API int imask_graph_launch(imask_graph* graph, void* stream);
 IMASK_API int imask_graph_destroy(imask_graph* graph);
 

@@ -116,6 +116,10 @@ SIGNATURES = {
     ),
     "imask_graph_launch": (ctypes.c_int, [_vp, _vp]),
     "imask_graph_destroy": (ctypes.c_int, [_vp]),
+    "imask_step_graph_update": (
+        ctypes.c_int,
+        [_vp, _vp, ctypes.POINTER(ImaskState), ctypes.c_int, ctypes.POINTER(ImaskStepParams)],
+    ),
 }
 
 _lib: Optional[ctypes.CDLL] = None

@@ -850,6 +850,35 @@ int imask_sketch_step(imask_plan* pl, const imask_state* st, int level0,
   return IMASK_OK;
 }
 
+namespace {
+
+// Capture one imask_sketch_step into a new graph (not instantiated).
+int capture_step(imask_plan* pl, const imask_state* st, int level0, const imask_step_params* prm,
+                 cudaGraph_t* graph, int* launches) {
+  cudaStream_t s;
+  int rc;
+  if ((rc = cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create")))
+    return rc;
+  *graph = nullptr;
+  rc = cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+  int step_rc = IMASK_OK;
+  if (!rc) step_rc = imask_sketch_step(pl, st, level0, prm, s);
+  const int n_launch = g_launches;
+  const std::string step_err = g_err;
+  cudaError_t end = rc ? cudaSuccess : cudaStreamEndCapture(s, graph);
+  if (!rc && step_rc) rc = fail(step_rc, step_err);
+  if (!rc) rc = cuda_check(end, "end capture");
+  cudaStreamDestroy(s);
+  if (rc && *graph) {
+    cudaGraphDestroy(*graph);
+    *graph = nullptr;
+  }
+  if (launches) *launches = n_launch;
+  return rc;
+}
+
+}  // namespace
+
 int imask_step_graph_create(imask_plan* pl, const imask_state* st, int level0,
                             const imask_step_params* prm, imask_graph** out, int* launches) {
   g_err.clear();
@@ -857,27 +886,45 @@ int imask_step_graph_create(imask_plan* pl, const imask_state* st, int level0,
   if (rc) return rc;
   if (!out) return fail(IMASK_EINVAL, "out must not be null");
   DeviceGuard g(pl->device);
-  cudaStream_t s;
-  if ((rc = cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create")))
-    return rc;
   imask_graph* gr = new imask_graph();
   gr->device = pl->device;
-  rc = cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
-  int step_rc = IMASK_OK;
-  if (!rc) step_rc = imask_sketch_step(pl, st, level0, prm, s);
-  const int n_launch = g_launches;
-  const std::string step_err = g_err;
-  cudaError_t end = rc ? cudaSuccess : cudaStreamEndCapture(s, &gr->graph);
-  if (!rc && step_rc) rc = fail(step_rc, step_err);
-  if (!rc) rc = cuda_check(end, "end capture");
+  int n_launch = 0;
+  rc = capture_step(pl, st, level0, prm, &gr->graph, &n_launch);
   if (!rc) rc = cuda_check(cudaGraphInstantiate(&gr->exec, gr->graph, 0), "graph instantiate");
-  cudaStreamDestroy(s);
   if (rc) {
     imask_graph_destroy(gr);
     return rc;
   }
   *out = gr;
   if (launches) *launches = n_launch;
+  g_launches = 0;
+  return IMASK_OK;
+}
+
+int imask_step_graph_update(imask_graph* gr, imask_plan* pl, const imask_state* st, int level0,
+                            const imask_step_params* prm) {
+  g_err.clear();
+  if (!gr) return fail(IMASK_EINVAL, "null graph");
+  int rc = check_level0(pl, level0);
+  if (rc) return rc;
+  DeviceGuard g(pl->device);
+  cudaGraph_t fresh = nullptr;
+  if ((rc = capture_step(pl, st, level0, prm, &fresh, nullptr))) return rc;
+  // same topology, new kernel arguments: patch the executable graph in place
+  cudaGraphExecUpdateResultInfo info;
+  if (cudaGraphExecUpdate(gr->exec, fresh, &info) != cudaSuccess) {
+    cudaGetLastError();  // clear the update failure; instantiate afresh
+    cudaGraphExec_t exec = nullptr;
+    rc = cuda_check(cudaGraphInstantiate(&exec, fresh, 0), "graph instantiate");
+    if (rc) {
+      cudaGraphDestroy(fresh);
+      return rc;
+    }
+    cudaGraphExecDestroy(gr->exec);
+    gr->exec = exec;
+  }
+  if (gr->graph) cudaGraphDestroy(gr->graph);
+  gr->graph = fresh;
   g_launches = 0;
   return IMASK_OK;
 }

@@ -176,6 +176,7 @@ class Plan:
                 )
             )
         self.handle = handle
+        self.graph_cache: dict = {}  # step graphs of solvers.Engine (destroyed with the plan)
         self.phi_offsets = []
         off = 0
         for f in self.factors:
@@ -184,6 +185,11 @@ class Plan:
         self.phi_tab_len = off
 
     def __del__(self):
+        for g in getattr(self, "graph_cache", {}).values():
+            try:
+                _lib.lib().imask_graph_destroy(g[0])
+            except Exception:
+                pass
         h = getattr(self, "handle", None)
         if h is not None and h.value:
             try:

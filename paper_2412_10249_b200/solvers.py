@@ -88,21 +88,43 @@ class Engine:
         self.b = b
         self.m_loc = self.plan.m_loc
         self.d = geom.side * geom.side
-        self._graphs: dict = {}  # (state id, level, sigma, mu) -> (graph handle, launches)
+        # step graphs live with the (cached) plan, so every problem built on the
+        # same geometry and family shares them: (level, sigma, mu, mu_g, parity)
+        # -> [handle, launches, pointers it was captured for]
+        self._graphs: dict = self.plan.graph_cache
         self.use_graphs = True
 
     def graph(self, state: "SaddleState", level0: int, prm) -> tuple:
-        key = (id(state), state.y.data_ptr(), level0, prm.sigma, prm.mu)
+        """(graph handle, kernels per replay) of one step at ``level0`` on ``state``.
+
+        Graphs are cached per (level, step scalars, dual-buffer parity), not per
+        state: when another state (other buffers) uses one, it is re-targeted in
+        place (imask_step_graph_update), so a new solve pays no instantiation.
+        A graph is only launched after its pointers were checked against the
+        state's, so it never holds the state alive.
+        """
+        key = (level0, prm.sigma, prm.mu, prm.mu_g, state.parity)
+        cst = state.c_state(self.b)
+        ptrs = tuple(getattr(cst, name) for name, _ in cst._fields_)
         hit = self._graphs.get(key)
         if hit is None:
             h = ctypes.c_void_p()
             n = ctypes.c_int(0)
             _lib.check(_lib.lib().imask_step_graph_create(
-                self.plan.handle, ctypes.byref(state.c_state(self.b)), level0, ctypes.byref(prm),
+                self.plan.handle, ctypes.byref(cst), level0, ctypes.byref(prm),
                 ctypes.byref(h), ctypes.byref(n)))
-            hit = (h, n.value, state)  # keep the state alive while its graph exists
+            hit = [h, n.value, ptrs]
             self._graphs[key] = hit
-        return hit
+        elif hit[2] != ptrs:
+            _lib.check(_lib.lib().imask_step_graph_update(
+                hit[0], self.plan.handle, ctypes.byref(cst), level0, ctypes.byref(prm)))
+            hit[2] = ptrs
+        return hit[0], hit[1]
+
+    def release_graphs(self, state: Optional["SaddleState"] = None) -> None:
+        """Destroy the cached step graphs (``state`` is accepted for compatibility)."""
+        for key in list(self._graphs):
+            _lib.lib().imask_graph_destroy(self._graphs.pop(key)[0])
 
     def side_stream(self) -> torch.cuda.Stream:
         """Stream of the forward chain in angle-sharded steps (created on first use)."""
@@ -117,16 +139,6 @@ class Engine:
                 self.graph(state, lv, prm)
             state.swap_dual()
 
-    def release_graphs(self, state: Optional["SaddleState"] = None) -> None:
-        for key in list(self._graphs):
-            if state is None or key[0] == id(state):
-                _lib.lib().imask_graph_destroy(self._graphs.pop(key)[0])
-
-    def __del__(self):
-        try:
-            self.release_graphs()
-        except Exception:
-            pass
 
 
 @dataclass(frozen=True)
@@ -217,6 +229,7 @@ class SaddleState:
     psi_tab: Optional[torch.Tensor] = None
     bp: Optional[torch.Tensor] = None
     y_alt: Optional[torch.Tensor] = None  # second dual buffer: y^{k+1} is written here, then swapped
+    parity: int = 0  # how many dual swaps mod 2 (which buffer is current)
     _cstates: dict = field(default_factory=dict, repr=False)
 
     def phi_full(self, i: int, family: SketchFamily) -> torch.Tensor:
@@ -246,6 +259,7 @@ class SaddleState:
         """After a step that wrote y^{k+1} into y_alt: make it the current y."""
         if self.y_alt is not None:
             self.y, self.y_alt = self.y_alt, self.y
+            self.parity ^= 1
 
 
 def _require_engine(prob: Problem) -> Engine:
@@ -321,7 +335,7 @@ def _device_step(eng: Engine, state: SaddleState, level0: int, prm: _lib.ImaskSt
     L = _lib.lib()
     h, s = eng.plan.handle, eng.plan.stream
     if eng.shard.world == 1 and eng.use_graphs:
-        g, launches, _ = eng.graph(state, level0, prm)
+        g, launches = eng.graph(state, level0, prm)
         _lib.check(L.imask_graph_launch(g, s))
         state.swap_dual()
         return launches
@@ -516,6 +530,5 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
         if k % record_every == 0 or k == iters:
             record(k, state.cost, state.last_level, state.x)
     rows = rec.rows()
-    eng.release_graphs(state)
     return SolveReport(rows=rows, x=state.x, y=state.y, algorithm=algorithm, seed=seed,
                        snapshots=snapshots)

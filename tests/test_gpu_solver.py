@@ -185,6 +185,28 @@ def test_sharded_device_step_stream_ordering(monkeypatch):
         assert np.array_equal(host(a), host(c))
 
 
+def test_graphs_retargeted_across_solves():
+    """A second solve on the same problem reuses the cached step graphs
+    (re-targeted to the new state's buffers when they differ) and reproduces
+    the first solve bit for bit; so does an eager run."""
+    side, na, nd, probs = 64, 90, 91, [0.3, 0.3, 0.2, 0.2]
+    orc = so.SketchedCT(side, na, nd, probs)
+    b = orc.proj[1].apply(np.random.default_rng(9).random(side * side))
+    prob = build(side, na, nd, probs, b)
+    n0 = len(prob.engine._graphs)  # the cache lives with the (shared) plan
+    rep1 = solvers.run(prob, "sketch", 2e-4, 1e-2, 25, record_every=5, seed=4)
+    n_graphs = len(prob.engine._graphs)
+    assert n0 < n_graphs <= n0 + 2 * 4
+    keep = rep1.x.clone()  # hold the first state's x so the second gets new buffers
+    rep2 = solvers.run(prob, "sketch", 2e-4, 1e-2, 25, record_every=5, seed=4)
+    assert len(prob.engine._graphs) == n_graphs
+    assert np.array_equal(host(rep2.x), host(keep))
+    prob.engine.use_graphs = False
+    rep3 = solvers.run(prob, "sketch", 2e-4, 1e-2, 25, record_every=5, seed=4)
+    assert np.array_equal(host(rep3.x), host(keep))
+    assert [r[:3] for r in rep1.rows] == [r[:3] for r in rep2.rows] == [r[:3] for r in rep3.rows]
+
+
 def test_resum_matches_direct_sums():
     side, na, nd, probs = 32, 36, 47, [0.3, 0.3, 0.2, 0.2]
     orc = so.SketchedCT(side, na, nd, probs)
