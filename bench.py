@@ -59,6 +59,32 @@ def parse():
 
 # ---------------------------------------------------------------- reference arm
 
+def ray_band_count(side: int, n_angles: int, n_det: int, angles=None) -> float:
+    """Ray-band visits of the factor-1 forward (the bands whose left chord partner
+    lies in [-1, n-1], as band_range in projector.cu), summed over all rays."""
+    th = np.arange(n_angles) * (np.pi / n_angles)
+    if angles is not None:
+        th = th[np.asarray(angles)]
+    c, s = np.cos(th), np.sin(th)
+    c[np.abs(c) < 1e-14] = 0.0
+    s[np.abs(s) < 1e-14] = 0.0
+    n, half, t0 = side, side / 2.0, -(n_det - 1) / 2.0
+    row = np.abs(c) >= np.abs(s)
+    a_, b_ = np.where(row, c, s), np.where(row, s, c)  # band-normal / along-band cosines
+    xi_dj = 1.0 / a_
+    xi_base = t0 / a_ + (half - 0.5) * b_ / a_ + half - 0.5
+    step = -b_ / a_
+    x0 = xi_base[:, None] + np.arange(n_det)[None, :] * xi_dj[:, None]
+    st = np.broadcast_to(step[:, None], x0.shape)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        e1 = (-1.0 - x0) / st
+        e2 = (n - x0) / st
+    lo = np.clip(np.ceil(np.minimum(e1, e2)), 0, n)
+    hi = np.clip(np.ceil(np.maximum(e1, e2)), 0, n)
+    cnt = np.where(st == 0, np.where((x0 >= -1) & (x0 < n), n, 0), np.maximum(hi - lo, 0))
+    return float(cnt.sum())
+
+
 def cpu_reference(cfg, steps: int, warmup: int, sample: int = CPU_SAMPLE_ANGLES):
     """Reference algorithm (scipy CSR, float64) on `sample` evenly spaced angles of cfg.
 
@@ -383,16 +409,34 @@ def main():
     nnz = 4.0 / np.pi * n_loc * cfg.d  # footprint evaluations = nnz of the reference CSR
     ffma = ctypes.c_double(0.0)
     _lib.check(_lib.lib().imask_probe_ffma_peak(local, ctypes.byref(ffma)))
+    smem = ctypes.c_double(0.0)
+    _lib.check(_lib.lib().imask_probe_smem_peak(local, ctypes.byref(smem)))
+    smem_peak = smem.value / 1e9
+    # shared-memory bytes the kernels must read: the forward one 8-byte value
+    # pair and one difference pair per band for a ray and its mirror (8 B per
+    # ray-band); the adjoint one 16-byte window element per pixel and angle pair
+    # (8 B per pixel-angle)
+    shard = ctmodel.shard_angles(cfg.n_angles, rank, world)
+    fwd_smem = 8.0 * ray_band_count(cfg.side, cfg.n_angles, cfg.n_det, shard)
+    adj_smem = 8.0 * cfg.d * n_loc
+    smem_view = {
+        "peak": round(smem_peak, 1), "unit": "GB/s",
+        "peak_source": "live probe (imask_probe_smem_peak: conflict-free LDS.128 on every SM)",
+        "forward_f1": {"bytes": fwd_smem, "achieved": round(fwd_smem / (fwd_ms * 1e-3) / 1e9, 1),
+                       "frac": round(fwd_smem / (fwd_ms * 1e-3) / 1e9 / smem_peak, 4)},
+        "adjoint_f1": {"bytes": adj_smem, "achieved": round(adj_smem / (adj_ms * 1e-3) / 1e9, 1),
+                       "frac": round(adj_smem / (adj_ms * 1e-3) / 1e9 / smem_peak, 4)}}
     roofline = {"bound": "hbm",
-                "kernel": ("k_forward_tma<true> (level-1 projection, SAGA epilogue)" if fwd_dominant
+                "kernel": ("k_forward_tma<false> (level-1 projection)" if fwd_dominant
                            else "k_adjoint<pair,sym> (level-1 backprojection)"),
                 "achieved": round(achieved, 2), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 5),
                 "traffic": traffic_tab.get("forward_f1" if fwd_dominant else "adjoint_f1"),
                 "algorithmic_bytes": alg_bytes, "avg_launch_ms": round(dom_ms, 4),
                 "peak_source": peak_src,
-                "note": "projectors are FP32-issue bound, not HBM bound (SURVEY 8(d)); "
-                        "see fp32_view; HBM-bound kernels in hbm_kernels",
+                "note": "projectors are bound by shared-memory bandwidth and instruction issue, "
+                        "not HBM (SURVEY 8(d)): see smem_view and fp32_view; HBM-bound kernels "
+                        "in hbm_kernels",
                 "fp32_view": {
                     "footprint_evals": nnz,
                     "forward_f1_ms": round(fwd_ms, 4), "adjoint_f1_ms": round(adj_ms, 4),
@@ -403,6 +447,7 @@ def main():
                     "csr_equivalent_gbs": round(8.0 * nnz / (dom_ms * 1e-3) / 1e9, 1),
                     "csr_note": "bandwidth a float32 value + int32 index CSR SpMV would need "
                                 "to match this kernel (the reference's operator form)"},
+                "smem_view": smem_view,
                 "hbm_kernels": hbm_kernels}
 
     # e2e through the public API: solvers.run with host inputs

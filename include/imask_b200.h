@@ -224,6 +224,10 @@ IMASK_API int imask_sq_dist(const float* x, const float* ref, int64_t n, double*
  * throughput of `device` from an FFMA-chain microbenchmark, the FP32-issue
  * denominator of bench.py's roofline. */
 IMASK_API int imask_probe_ffma_peak(int device, double* ffma_per_s);
+/* Measurement helper: aggregate shared-memory read bandwidth of `device`
+ * (conflict-free 128-bit loads on every SM), the denominator of the
+ * projectors' shared-memory roofline in bench.py. */
+IMASK_API int imask_probe_smem_peak(int device, double* bytes_per_s);
 
 #ifdef __cplusplus
 }
