@@ -49,8 +49,8 @@ struct TmaMaps {
 };
 cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float2* PT,
                                const float2* PM, const float2* PTM, int n, const FwdAngle* ang,
-                               const int2* entries, int n_entries, int row_ctas, int n_det,
-                               float* sino, const SinoSaga* saga, cudaStream_t stream);
+                               const int4* entries, int n_entries, int row_ctas, bool quad,
+                               int n_det, float* sino, const SinoSaga* saga, cudaStream_t stream);
 }  // namespace imask
 
 struct imask_graph {
@@ -75,7 +75,7 @@ struct LevelTables {
   FwdAngle* fwd = nullptr;  // device
   AdjAngle* adj = nullptr;  // device
   bool tma = false;         // tensor maps of the pair images at this level are valid
-  TmaMaps maps{};
+  TmaMaps maps{};           // boxes of 96 x 16 (pair mode) or 96 x 8 bands (quad mode)
 };
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
@@ -99,13 +99,13 @@ EncodeTiledFn encode_fn() {
 }
 
 // 2-D map over a pair image of one level: {pitch, n} 8-byte elements, box of
-// kFWc columns x kFB bands (constants of projector.cu: 96 x 16).
-bool encode_pair_map(CUtensorMap* map, void* base, int n) {
+// kFWc columns x box_h bands (projector.cu: 96 x 16 in pair mode, 96 x 8 in quad mode).
+bool encode_pair_map(CUtensorMap* map, void* base, int n, unsigned box_h) {
   EncodeTiledFn fn = encode_fn();
   if (!fn || !base) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)pair_pitch(n), (cuuint64_t)n};
   const cuuint64_t strides[1] = {(cuuint64_t)pair_pitch(n) * sizeof(float2)};
-  const cuuint32_t box[2] = {96, 16};
+  const cuuint32_t box[2] = {96, box_h};
   const cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, base, dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -132,9 +132,12 @@ struct imask_plan {
   bool sym = false;       // whole, even-sized angle set: mirror-symmetric kernels
   int2* fwd_entries = nullptr;  // (angle, mirror angle or -1) per forward warp
   int n_entries = 0;
-  int2* tma_entries = nullptr;  // same, grouped 8 per CTA by ray family (-1 = idle warp)
+  int4* tma_entries = nullptr;  // TMA forward entries, 8 per CTA (-1 = none):
+                                // quad mode (a, n-a, n/2-a, n/2+a); pair mode (a, n-a, -1, -1)
+                                // grouped by ray family
   int n_tma_entries = 0;
-  int tma_row_ctas = 0;         // CTAs [0, tma_row_ctas) hold row-family entries
+  int tma_row_ctas = 0;         // pair mode: CTAs [0, tma_row_ctas) hold row-family entries
+  bool tma_quad = false;        // the local rows are closed under a -> n/2 - a as well
   float* u = nullptr;
   float* sino_tmp = nullptr;
   float* adj_partial = nullptr;  // per-split partial backprojections (coarse levels)
@@ -266,8 +269,11 @@ int get_tables(imask_plan* pl, int f, LevelTables** out) {
     static const bool no_tma = std::getenv("IMASK_NO_TMA") != nullptr;  // debugging / A-B runs
     if (pl->sym && !no_tma) {
       const int n = pl->side / f;
-      t.tma = encode_pair_map(&t.maps.row, pl->P, n) && encode_pair_map(&t.maps.row_m, pl->PM, n) &&
-              encode_pair_map(&t.maps.col, pl->PT, n) && encode_pair_map(&t.maps.col_m, pl->PTM, n);
+      const unsigned bh = pl->tma_quad ? 8 : 16;
+      t.tma = encode_pair_map(&t.maps.row, pl->P, n, bh) &&
+              encode_pair_map(&t.maps.row_m, pl->PM, n, bh) &&
+              encode_pair_map(&t.maps.col, pl->PT, n, bh) &&
+              encode_pair_map(&t.maps.col_m, pl->PTM, n, bh);
     }
     it = pl->tables.emplace(f, t).first;
   }
@@ -312,7 +318,8 @@ int run_forward(imask_plan* pl, int f, const LevelTables* t, float* sino, const 
   }();
   if (t->tma && pl->tma_entries && n >= tma_min_n)
     e = launch_forward_tma(t->maps, pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->tma_entries,
-                           pl->n_tma_entries, pl->tma_row_ctas, pl->n_det, sino, saga, s);
+                           pl->n_tma_entries, pl->tma_row_ctas, pl->tma_quad, pl->n_det, sino,
+                           saga, s);
   else
     e = launch_forward(pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->n_loc, pl->n_det,
                        pl->fwd_entries, pl->n_entries, sino, saga, s);
@@ -514,9 +521,55 @@ int imask_plan_create_list(int side, int n_angles, int n_det, int n_loc, const i
       while (tent.size() % 8) tent.push_back(make_int2(-1, -1));
       if (lst == &rowf) pl->tma_row_ctas = (int)tent.size() / 8;
     }
-    pl->n_tma_entries = (int)tent.size();
-    if ((rc = cuda_check(cudaMalloc(&pl->tma_entries, sizeof(int2) * tent.size()), "cudaMalloc")) ||
-        (rc = cuda_check(cudaMemcpy(pl->tma_entries, tent.data(), sizeof(int2) * tent.size(),
+    // quad mode when every row's transpose partner n/2 - a (pi/2 - theta) is local
+    // too: the singles 0 and n/2 (a transposed-family entry), entries
+    // (a, n-a, n/2-a, n/2+a) for 0 < a < n/4, then the pair (n/4, 3n/4)
+    std::vector<int4> qent;
+    static const bool no_quad = std::getenv("IMASK_NO_QUAD") != nullptr;  // A-B runs
+    if (n_angles % 4 == 0 && !no_quad) {
+      std::vector<int> loc(n_angles, -1);
+      for (int i = 0; i < n_loc; ++i) loc[angle_idx[i]] = i;
+      const int h = n_angles / 2, qn = n_angles / 4;
+      int covered = 0;
+      bool ok = true;
+      // the axis singles first, beside the near-axis quads (a CTA's lanes walk
+      // one lockstep band range, so its entries must be geometrically close)
+      if (loc[0] >= 0) {
+        qent.push_back(make_int4(loc[0], -1, -1, -1));
+        ++covered;
+      }
+      if (loc[h] >= 0) {
+        qent.push_back(make_int4(-1, -1, loc[h], -1));
+        ++covered;
+      }
+      for (int a = 1; a < qn && ok; ++a) {
+        const int r0 = loc[a], r1 = loc[n_angles - a], r2 = loc[h - a], r3 = loc[h + a];
+        const int have = (r0 >= 0) + (r1 >= 0) + (r2 >= 0) + (r3 >= 0);
+        if (have == 0) continue;
+        if (have != 4) ok = false;
+        qent.push_back(make_int4(r0, r1, r2, r3));
+        covered += 4;
+      }
+      if (ok && loc[qn] >= 0 && loc[3 * qn] >= 0) {
+        qent.push_back(make_int4(loc[qn], loc[3 * qn], -1, -1));
+        covered += 2;
+      } else if (loc[qn] >= 0 || loc[3 * qn] >= 0) {
+        ok = false;
+      }
+      if (!ok || covered != n_loc) qent.clear();
+    }
+    std::vector<int4> tent4;
+    if (!qent.empty()) {
+      pl->tma_quad = true;
+      tent4 = qent;
+      while (tent4.size() % 8) tent4.push_back(make_int4(-1, -1, -1, -1));
+      pl->tma_row_ctas = (int)tent4.size() / 8;
+    } else {
+      for (const int2& e2 : tent) tent4.push_back(make_int4(e2.x, e2.y, -1, -1));
+    }
+    pl->n_tma_entries = (int)tent4.size();
+    if ((rc = cuda_check(cudaMalloc(&pl->tma_entries, sizeof(int4) * tent4.size()), "cudaMalloc")) ||
+        (rc = cuda_check(cudaMemcpy(pl->tma_entries, tent4.data(), sizeof(int4) * tent4.size(),
                                     cudaMemcpyHostToDevice),
                          "cudaMemcpy"))) {
       imask_plan_destroy(pl);

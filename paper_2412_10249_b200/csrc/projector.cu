@@ -226,9 +226,10 @@ k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
 // neighbouring angles share one on-chip copy. A CTA whose window would exceed
 // kFWc (very wide angle spread) falls back to global loads. Window origins are
 // rounded down to an even pair index: a tensor copy must start 16-byte aligned.
-constexpr int kFB = 16;           // bands per chunk
+constexpr int kFB = 16;           // bands per chunk (pair mode)
+constexpr int kFBQuad = 8;        // bands per chunk (quad mode: twice the images)
 constexpr int kFWc = 96;          // window width in pair columns (x 8 B = 768 B per row)
-constexpr int kFMaxChunks = 512;  // side up to 8192
+constexpr int kFMaxChunks = 1024;  // side up to 8192
 
 struct TmaMaps {
   CUtensorMap row, row_m, col, col_m;  // P, PM, PT, PTM of one level
@@ -271,40 +272,51 @@ struct FwdWarpInfo {
   int lo, hi;  // union of the lockstep band ranges (lo >= hi: idle)
 };
 
-template <bool kSaga>
+// kQuad: each entry is up to four rays at the same fixed-point positions --
+// angle a (row family), its mirror n-a, its transpose partner n/2-a (column
+// family: the ray through u at pi/2 - theta is the ray through u^T at theta)
+// and that one's mirror n/2+a -- so a CTA stages four windows per chunk (the
+// value and difference planes of P and of PT) and every position, weight and
+// address is computed once for four rays. Pair mode (kQuad = false): entries
+// (a, n-a), one ray family per CTA.
+template <bool kSaga, bool kQuad>
 __global__ void __launch_bounds__(256)
 k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P,
               const float2* __restrict__ PT, const float2* __restrict__ PM,
               const float2* __restrict__ PTM, int n, int pitch, const FwdAngle* __restrict__ ang,
-              const int2* __restrict__ entries, int n_entries, int row_ctas, int n_det,
+              const int4* __restrict__ entries, int n_entries, int row_ctas, int n_det,
               float* __restrict__ sino, SinoSaga saga) {
+  constexpr int FB = kQuad ? kFBQuad : kFB;  // bands per chunk
+  constexpr int NI = kQuad ? 4 : 2;          // staged images per chunk
+  constexpr int kBox = FB * kFWc;            // float2 per image per stage
   extern __shared__ __align__(128) unsigned char smem[];
-  constexpr int kBox = kFB * kFWc;  // float2 per image per stage
-  float2* stage = reinterpret_cast<float2*>(smem);  // [2 stages][2 images][kFB][kFWc]
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * 2 * kBox * sizeof(float2));
+  float2* stage = reinterpret_cast<float2*>(smem);  // [2 stages][NI images][FB][kFWc]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * NI * kBox * sizeof(float2));
   uint64_t* empty = full + 2;
   FwdWarpInfo* info = reinterpret_cast<FwdWarpInfo*>(empty + 2);
   int* cmin_tab = reinterpret_cast<int*>(info + 8);
   int* ctl = cmin_tab + kFMaxChunks;  // [0] overflow, [1] first band, [2] chunks, then cmax_tab
 
-  // A warp holds 4 angles x 8 consecutive detectors (lane = 8 q + d): each
+  // A warp holds 4 entries x 8 consecutive detectors (lane = 8 q + d): each
   // half-warp's 8-byte window reads then span ~10 pair columns of one band,
   // never two slots 16 apart (the bank period), so a read is 2 wavefronts
   // where 32 detectors of one angle (up to 45 columns) cost up to 4.
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q4 = lane >> 3;
   const int e = blockIdx.y * 8 + (warp >> 2) * 4 + q4;
-  const int2 ent = e < n_entries ? entries[e] : make_int2(-1, -1);
-  const int a = ent.x, am = ent.y;
-  const bool valid = a >= 0;
+  const int4 ent = e < n_entries ? entries[e] : make_int4(-1, -1, -1, -1);
+  const int rows[4] = {ent.x, ent.y, ent.z, ent.w};
+  const int tab = ent.x >= 0 ? ent.x : ent.z;  // the entry's parameter row
+  const bool valid = tab >= 0;
   const int j = blockIdx.x * 32 + (warp & 3) * 8 + (lane & 7);
   const int jr = min(j, n_det - 1);
   FwdAngle A{};
-  if (valid) A = ang[a];
-  SinoIn sin[2];
+  if (valid) A = ang[tab];
+  SinoIn sin[NI];
   if (kSaga && valid && j < n_det) {
-    sin[0] = sino_load(saga, (size_t)a * n_det + j);
-    if (am >= 0) sin[1] = sino_load(saga, (size_t)am * n_det + j);
+#pragma unroll
+    for (int r = 0; r < NI; ++r)
+      if (rows[r] >= 0) sin[r] = sino_load(saga, (size_t)rows[r] * n_det + j);
   }
   long long X0 = 0;
   int lo = n, hi = 0;
@@ -322,7 +334,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
     wlo = min(wlo, __shfl_xor_sync(0xffffffffu, wlo, o));
     whi = max(whi, __shfl_xor_sync(0xffffffffu, whi, o));
   }
-  // per angle slot (8 per CTA): positions of its first and last detector and the
+  // per entry slot (8 per CTA): positions of its first and last detector and the
   // union of the lockstep band ranges of the four warps holding it (every lane
   // walks its warp's whole range)
   int* cmax_tab = ctl + 4;  // [kFMaxChunks]
@@ -351,13 +363,13 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
       bhi = max(bhi, info[w].hi);
     }
     ctl[1] = blo;
-    ctl[2] = bhi > blo ? (bhi - blo + kFB - 1) / kFB : 0;
+    ctl[2] = bhi > blo ? (bhi - blo + FB - 1) / FB : 0;
     if (ctl[2] > kFMaxChunks) ctl[0] = 1;
   }
   __syncthreads();
   const int blo = ctl[1], nch = ctl[2];
   // window (first pair column) of every chunk: extremes of the affine positions,
-  // one (chunk, angle slot) item per thread
+  // one (chunk, entry slot) item per thread
   if (!ctl[0]) {
     for (int t = threadIdx.x; t < nch; t += blockDim.x) {
       cmin_tab[t] = INT_MAX;
@@ -367,8 +379,8 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
     for (int it = threadIdx.x; it < nch * 8; it += blockDim.x) {
       const int t = it >> 3;
       const FwdWarpInfo& I = info[it & 7];
-      const int b0 = blo + t * kFB;
-      const int bs = max(b0, I.lo), be = min(b0 + kFB, I.hi) - 1;
+      const int b0 = blo + t * FB;
+      const int bs = max(b0, I.lo), be = min(b0 + FB, I.hi) - 1;
       if (bs > be) continue;
       const int c0 = (int)((I.x0_first + bs * I.step) >> 32), c1 = (int)((I.x0_first + be * I.step) >> 32),
                 c2 = (int)((I.x0_last + bs * I.step) >> 32), c3 = (int)((I.x0_last + be * I.step) >> 32);
@@ -386,34 +398,38 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
     }
   }
   __syncthreads();
-  // one ray family per CTA: the host puts the row-family CTAs first, so the
-  // family (and the tensor-map pointers below) is uniform, derived from blockIdx
-  const bool trans = (int)blockIdx.y >= row_ctas;
+  // pair mode: one ray family per CTA, the row-family CTAs first, so the family
+  // (and the tensor-map pointers below) is uniform, derived from blockIdx
+  const bool trans = !kQuad && (int)blockIdx.y >= row_ctas;
   // value pairs (u, um) and difference pairs (d, dm) (k_prepare's symmetric
-  // layout): (acc, accm) += (u, um) + g * (d, dm) with packed FP32 ops
-  float2 acc2 = make_float2(0.f, 0.f);
+  // layout): (acc, accm) += (u, um) + g * (d, dm) with packed FP32 ops; accT
+  // the same for the transpose partners (kQuad)
+  float2 acc2 = make_float2(0.f, 0.f), accT = make_float2(0.f, 0.f);
   const float S = A.S, B = A.B;
 
   if (ctl[0]) {
     // fallback: global (L1) loads, as k_forward_sym
-    const float2* __restrict__ img = trans ? PT : P;
-    const float2* __restrict__ imgm = trans ? PTM : PM;
     if (valid) {
+      const float2* __restrict__ img = trans ? PT : P;
+      const float2* __restrict__ imgd = trans ? PTM : PM;
       const long long dYl = A.step + ((long long)pitch << 32);
       Fix32 Y = fix_from(X0 + (long long)wlo * dYl + ((long long)(1 + kPadC) << 32));
       const Fix32 dY = fix_from(dYl);
       for (int b = wlo; b < whi; ++b) {
-        const float2 v = __ldg(img + Y.hi), vd = __ldg(imgm + Y.hi);
         const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
-        acc2 = fadd2(acc2, v);
-        acc2 = ffma2(g, vd, acc2);
+        acc2 = fadd2(acc2, __ldg(img + Y.hi));
+        acc2 = ffma2(g, __ldg(imgd + Y.hi), acc2);
+        if (kQuad) {
+          accT = fadd2(accT, __ldg(PT + Y.hi));
+          accT = ffma2(g, __ldg(PTM + Y.hi), accT);
+        }
         fix_add(Y, dY);
       }
     }
   } else if (nch > 0) {
-    const CUtensorMap* mm = trans ? &maps.col : &maps.row;
-    const CUtensorMap* mmm = trans ? &maps.col_m : &maps.row_m;
-    constexpr uint32_t kTx = 2 * kBox * sizeof(float2);
+    const CUtensorMap* mp[4] = {trans ? &maps.col : &maps.row, trans ? &maps.col_m : &maps.row_m,
+                                &maps.col, &maps.col_m};
+    constexpr uint32_t kTx = NI * kBox * sizeof(float2);
     if (threadIdx.x == 0) {
       mbar_init(&full[0], 1);
       mbar_init(&full[1], 1);
@@ -427,9 +443,10 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
       if (lane == 0) {
         for (int i = 0; i < 2 && i < nch; ++i) {
           mbar_expect_tx(&full[i], kTx);
-          const int col = cmin_tab[i] + 1 + kPadC, row = blo + i * kFB;
-          tma_load_2d(stage + (i * 2 + 0) * kBox, mm, col, row, &full[i]);
-          tma_load_2d(stage + (i * 2 + 1) * kBox, mmm, col, row, &full[i]);
+          const int col = cmin_tab[i] + 1 + kPadC, row = blo + i * FB;
+#pragma unroll
+          for (int k = 0; k < NI; ++k)
+            tma_load_2d(stage + (i * NI + k) * kBox, mp[k], col, row, &full[i]);
         }
       }
       __syncwarp();
@@ -437,23 +454,27 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
     const Fix32 dYw = fix_from(A.step + ((long long)kFWc << 32));
     for (int i = 0; i < nch; ++i) {
       const int s = i & 1;
-      const int b0 = blo + i * kFB;
+      const int b0 = blo + i * FB;
       mbar_wait(&full[s], (i >> 1) & 1);
-      const int bs = max(b0, wlo), be = min(b0 + kFB, whi);
+      const int bs = max(b0, wlo), be = min(b0 + FB, whi);
       if (valid && bs < be) {
-        // the stage's value window, with the difference window kBox elements on;
-        // the stage offset rides in the position's integer word
+        // image k of this stage sits k * kBox elements on; the stage offset
+        // rides in the position's integer word
         const float2* win = stage;
         const long long X = X0 + (long long)bs * A.step;
-        Fix32 Y = fix_from(X + ((long long)((bs - b0) * kFWc - cmin_tab[i] + s * 2 * kBox) << 32));
+        Fix32 Y = fix_from(X + ((long long)((bs - b0) * kFWc - cmin_tab[i] + s * NI * kBox) << 32));
         int b = bs;
         for (; b + 4 <= be; b += 4) {
-          float2 v[4], vd[4];
+          float2 v[4], vd[4], vt[4], vdt[4];
           float g[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             v[k] = win[Y.hi];
             vd[k] = win[Y.hi + kBox];
+            if (kQuad) {
+              vt[k] = win[Y.hi + 2 * kBox];
+              vdt[k] = win[Y.hi + 3 * kBox];
+            }
             g[k] = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
             fix_add(Y, dYw);
           }
@@ -461,13 +482,20 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
           for (int k = 0; k < 4; ++k) {
             acc2 = fadd2(acc2, v[k]);
             acc2 = ffma2(g[k], vd[k], acc2);
+            if (kQuad) {
+              accT = fadd2(accT, vt[k]);
+              accT = ffma2(g[k], vdt[k], accT);
+            }
           }
         }
         for (; b < be; ++b) {
-          const float2 v = win[Y.hi], vd = win[Y.hi + kBox];
           const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
-          acc2 = fadd2(acc2, v);
-          acc2 = ffma2(g, vd, acc2);
+          acc2 = fadd2(acc2, win[Y.hi]);
+          acc2 = ffma2(g, win[Y.hi + kBox], acc2);
+          if (kQuad) {
+            accT = fadd2(accT, win[Y.hi + 2 * kBox]);
+            accT = ffma2(g, win[Y.hi + 3 * kBox], accT);
+          }
           fix_add(Y, dYw);
         }
       }
@@ -478,21 +506,22 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
         mbar_wait(&empty[s], (i >> 1) & 1);
         if (lane == 0) {
           mbar_expect_tx(&full[s], kTx);
-          const int col = cmin_tab[i + 2] + 1 + kPadC, row = blo + (i + 2) * kFB;
-          tma_load_2d(stage + (s * 2 + 0) * kBox, mm, col, row, &full[s]);
-          tma_load_2d(stage + (s * 2 + 1) * kBox, mmm, col, row, &full[s]);
+          const int col = cmin_tab[i + 2] + 1 + kPadC, row = blo + (i + 2) * FB;
+#pragma unroll
+          for (int k = 0; k < NI; ++k)
+            tma_load_2d(stage + (s * NI + k) * kBox, mp[k], col, row, &full[s]);
         }
         __syncwarp();
       }
     }
   }
   if (valid && j < n_det) {
+    const float vals[4] = {acc2.x, acc2.y, accT.x, accT.y};
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int row = r == 0 ? a : am;
-      if (row < 0) break;
-      const float val = (r == 0 ? acc2.x : acc2.y) * A.wsc;
-      const size_t q = (size_t)row * n_det + j;
+    for (int r = 0; r < NI; ++r) {
+      if (rows[r] < 0) continue;
+      const float val = vals[r] * A.wsc;
+      const size_t q = (size_t)rows[r] * n_det + j;
       if (kSaga) {
         sino_update(saga, q, sin[r], val);
       } else {
@@ -503,25 +532,30 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
 }
 
 size_t forward_tma_smem() {
+  // both modes stage 2 x 2 x 16 or 2 x 4 x 8 bands of kFWc pairs (48 KB)
   return 2 * 2 * kFB * kFWc * sizeof(float2) + 4 * sizeof(uint64_t) + 8 * sizeof(FwdWarpInfo) +
          (2 * kFMaxChunks + 4) * sizeof(int);
 }
 
 cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float2* PT,
                                const float2* PM, const float2* PTM, int n, const FwdAngle* ang,
-                               const int2* entries, int n_entries, int row_ctas, int n_det,
-                               float* sino, const SinoSaga* saga, cudaStream_t stream) {
+                               const int4* entries, int n_entries, int row_ctas, bool quad,
+                               int n_det, float* sino, const SinoSaga* saga, cudaStream_t stream) {
   dim3 grid((n_det + 31) / 32, (n_entries + 7) / 8);
   const size_t smem = forward_tma_smem();
   SinoSaga none{};
-  if (saga)
-    k_forward_tma<true><<<grid, 256, smem, stream>>>(maps, P, PT, PM, PTM, n, pair_pitch(n), ang,
-                                                      entries, n_entries, row_ctas, n_det, nullptr,
-                                                      *saga);
-  else
-    k_forward_tma<false><<<grid, 256, smem, stream>>>(maps, P, PT, PM, PTM, n, pair_pitch(n), ang,
-                                                       entries, n_entries, row_ctas, n_det, sino,
-                                                       none);
+  const SinoSaga sg = saga ? *saga : none;
+  float* out = saga ? nullptr : sino;
+#define FWD_TMA(S_, Q_)                                                                     \
+  k_forward_tma<S_, Q_><<<grid, 256, smem, stream>>>(maps, P, PT, PM, PTM, n, pair_pitch(n), \
+                                                     ang, entries, n_entries, row_ctas, n_det, \
+                                                     out, sg)
+  if (saga) {
+    if (quad) FWD_TMA(true, true); else FWD_TMA(true, false);
+  } else {
+    if (quad) FWD_TMA(false, true); else FWD_TMA(false, false);
+  }
+#undef FWD_TMA
   return cudaGetLastError();
 }
 
@@ -839,9 +873,13 @@ cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, 
 // Opt-in shared memory beyond 48 KB (called once per device at plan creation,
 // outside any stream capture).
 void init_kernel_attributes() {
-  cudaFuncSetAttribute(k_forward_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_forward_tma<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)forward_tma_smem());
-  cudaFuncSetAttribute(k_forward_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_forward_tma<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)forward_tma_smem());
+  cudaFuncSetAttribute(k_forward_tma<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)forward_tma_smem());
+  cudaFuncSetAttribute(k_forward_tma<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)forward_tma_smem());
 #define ADJ_ATTR(P_, T_, S_, K_)                                                          \
   cudaFuncSetAttribute(k_adjoint<P_, T_, S_, K_>,                                        \
