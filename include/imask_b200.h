@@ -110,8 +110,9 @@ IMASK_API int imask_plan_create_list(int side, int n_angles, int n_det, int n_lo
                                      const double* sin_tab, int r, const double* probs,
                                      double scale, int device, imask_plan** out);
 IMASK_API int imask_plan_destroy(imask_plan* plan);
-/* 1 if the plan's angle rows have the mirror layout above (symmetric kernels
- * in use), else 0. */
+/* 0: no mirror layout; 1: the plan's angle rows have the mirror layout above
+ * (symmetric kernels in use); 2: in addition they are closed under the
+ * transpose a -> n_angles/2 - a (four-ray TMA forward). */
 IMASK_API int imask_plan_symmetric(const imask_plan* plan);
 /* Scratch bytes the plan owns on the device (for memory accounting). */
 IMASK_API int64_t imask_plan_scratch_bytes(const imask_plan* plan);

@@ -645,7 +645,9 @@ int imask_plan_destroy(imask_plan* pl) {
 }
 
 int64_t imask_plan_scratch_bytes(const imask_plan* pl) { return pl ? pl->scratch : 0; }
-int imask_plan_symmetric(const imask_plan* pl) { return pl && pl->sym ? 1 : 0; }
+int imask_plan_symmetric(const imask_plan* pl) {
+  return !pl || !pl->sym ? 0 : (pl->tma_quad ? 2 : 1);
+}
 
 int imask_project(imask_plan* pl, int factor, const float* u, int64_t u_len, float* sino,
                   int64_t sino_len, void* stream) {

@@ -101,6 +101,8 @@ def shard_angles(n_angles: int, rank: int, world: int) -> tuple:
         raise ValueError(f"bad rank {rank} of world {world}")
     if world == 1:
         return tuple(range(n_angles))
+    if n_angles % 4 == 0 and n_angles >= 8:
+        return _shard_quads(n_angles, rank, world)
     bases = list(range(1, n_angles // 2 + 1))
     weight = [1 if 2 * a == n_angles else 2 for a in bases]
     cum = np.concatenate([[1], 1 + np.cumsum(weight)])  # rows up to and including base i (+ angle 0)
@@ -113,6 +115,29 @@ def shard_angles(n_angles: int, rank: int, world: int) -> tuple:
     mine = bases[edges[rank]:edges[rank + 1]]
     mirrors = sorted(n_angles - a for a in mine if 2 * a != n_angles)
     return tuple(([0] if rank == 0 else []) + mine + mirrors)
+
+
+def _shard_quads(n_angles: int, rank: int, world: int) -> tuple:
+    """shard_angles when n_angles % 4 == 0: shards closed under the mirror
+    a -> n - a and the transpose a -> n/2 - a as well, so every rank's forward
+    runs the four-ray (quad) TMA kernel. Units: the quads {a, n/2-a, n/2+a, n-a}
+    (0 < a < n/4) split contiguously; rank 0 adds angles 0 and n/2, the last
+    rank the pair {n/4, 3n/4}. Rows: [0] + the low angles (< n/2, and n/2)
+    ascending + their mirrors ascending."""
+    h, q = n_angles // 2, n_angles // 4
+    quads = list(range(1, q))
+    # rows before unit i: rank 0's two singles, four per quad; the pair adds 2 at the end
+    cum = 2 + 4 * np.arange(1, len(quads) + 1)
+    edges = [0] + [int(np.searchsorted(cum, (k + 1) * n_angles / world - 0.5)) + 1
+                   for k in range(world - 1)] + [len(quads)]
+    edges = [min(max(e, 0), len(quads)) for e in edges]
+    for k in range(1, len(edges)):
+        edges[k] = max(edges[k], edges[k - 1])
+    mine = quads[edges[rank]:edges[rank + 1]]
+    low = sorted(set(mine) | {h - a for a in mine}
+                 | ({h} if rank == 0 else set()) | ({q} if rank == world - 1 else set()))
+    mirrors = sorted(n_angles - a for a in low if a != h)
+    return tuple(([0] if rank == 0 else []) + low + mirrors)
 
 
 def _stream_ptr(device: torch.device) -> ctypes.c_void_p:
@@ -201,7 +226,12 @@ class Plan:
     @property
     def symmetric(self) -> bool:
         """True when the mirror-symmetric kernels serve this plan's angle rows."""
-        return bool(_lib.lib().imask_plan_symmetric(self.handle))
+        return _lib.lib().imask_plan_symmetric(self.handle) >= 1
+
+    @property
+    def quad_forward(self) -> bool:
+        """True when the rows are also transpose-closed (four-ray TMA forward)."""
+        return _lib.lib().imask_plan_symmetric(self.handle) == 2
 
     @property
     def stream(self) -> ctypes.c_void_p:

@@ -8,12 +8,14 @@ where the half-open tie rule decides), odd/even detector counts, the adjoint
 identity, and size-independent properties at the full D / E sizes.
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
 from scipy import sparse
 
-from conftest import rel_l2
+from conftest import REPO, rel_l2
 from oracle import ct_oracle, sketch_oracle
 from paper_2412_10249_b200 import ctmodel, linops
 from paper_2412_10249_b200.synth import CONFIGS, ellipse_phantom
@@ -220,7 +222,29 @@ def test_mirror_closed_shards_match_full(n_angles, world):
             idx = list(ctmodel.shard_angles(n_angles, rank, world))
             plan = ctmodel.Plan(geom, angles=idx)
             assert plan.symmetric
+            assert plan.quad_forward == (n_angles % 4 == 0)
             part = host(plan.project(u, f)).reshape(len(idx), 91)
             assert rel_l2(part, full[idx]) <= 1e-6
             bp_sum += host(plan.backproject(dev(y[idx]), f))
         assert rel_l2(bp_sum, ref) <= 1e-6
+
+
+@pytest.mark.parametrize("geom_args", [(1024, 1440, 1449, 1), (256, 360, 363, 1), (256, 360, 363, 2)])
+def test_forward_paths_bit_identical(geom_args, tmp_path):
+    """The four-ray (quad) TMA forward, the pair TMA forward and the L1 forward
+    trace the same rays with the same arithmetic: bit-identical sinograms. The
+    path switches are read once per process, so each runs in a subprocess."""
+    import subprocess
+    import sys
+
+    script = os.path.join(REPO, "tools", "repro_quad.py")
+    outs = {}
+    for name, env_extra in (("quad", {}), ("pair", {"IMASK_NO_QUAD": "1"}),
+                            ("l1", {"IMASK_NO_TMA": "1"})):
+        out = str(tmp_path / f"{name}.npy")
+        env = dict(os.environ, OUT=out, **env_extra)
+        subprocess.run([sys.executable, script, *map(str, geom_args)], env=env, check=True,
+                       capture_output=True, timeout=300)
+        outs[name] = np.load(out)
+    assert np.array_equal(outs["quad"], outs["pair"])
+    assert np.array_equal(outs["quad"], outs["l1"])

@@ -49,7 +49,8 @@ def test_shards_partition_angles_mirror_closed(n, world):
     flat = [a for sh in shards for a in sh]
     assert sorted(flat) == list(range(n))  # a partition of all angles
     sizes = [len(sh) for sh in shards]
-    assert max(sizes) - min(sizes) <= 3
+    # balanced to the shard unit: 2 rows (mirror pairs), 4 (quads when n % 4 == 0)
+    assert max(sizes) - min(sizes) <= (6 if n % 4 == 0 else 3)
     for rank, sh in enumerate(shards):
         # the row layout imask_plan_create_list turns into mirror-symmetric kernels:
         # [0 on rank 0] + rows i <-> s + n_loc - 1 - i holding a and n - a
@@ -58,6 +59,10 @@ def test_shards_partition_angles_mirror_closed(n, world):
         rows = sh[s0:]
         for i, a in enumerate(rows):
             assert rows[len(rows) - 1 - i] == n - a
+        if n % 4 == 0 and n >= 8:
+            # closed under the transpose a -> n/2 - a too (quad-mode forward)
+            low = {a % (n // 2) for a in sh}
+            assert all((n // 2 - a) % (n // 2) in low for a in low)
 
 
 def test_family_validation_messages():
