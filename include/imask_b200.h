@@ -214,12 +214,14 @@ IMASK_API int imask_graph_destroy(imask_graph* graph);
 IMASK_API int imask_last_launch_count(void);
 
 /* ||x - ref||^2 (ref may be NULL: ||x||^2) accumulated in float64 with a
- * fixed-order reduction, written to out[0] on the device; `out` is device
- * scratch of IMASK_SQDIST_SCRATCH doubles. Backs the rel_dist / psnr columns
- * of run()'s record rows (_metrics, solvers.py:382-390) without a host sync. */
-#define IMASK_SQDIST_SCRATCH 297
+ * fixed-order reduction, written to *result (a device double; NULL: out[0]);
+ * `out` is device scratch of IMASK_SQDIST_SCRATCH doubles, ZERO-INITIALISED
+ * before the first call (it holds a completion counter each call re-arms).
+ * Backs the rel_dist / psnr columns of run()'s record rows (_metrics,
+ * solvers.py:382-390) without a host sync. */
+#define IMASK_SQDIST_SCRATCH 298
 IMASK_API int imask_sq_dist(const float* x, const float* ref, int64_t n, double* out,
-                            void* stream);
+                            double* result, void* stream);
 
 /* Measurement helper (no reference counterpart): thread-level FP32 FFMA
  * throughput of `device` from an FFMA-chain microbenchmark, the FP32-issue

@@ -21,7 +21,7 @@ IMASK_EINVAL = 1
 IMASK_EDIM = 2
 IMASK_ELEVEL = 3
 IMASK_ECUDA = 4
-IMASK_SQDIST_SCRATCH = 297
+IMASK_SQDIST_SCRATCH = 298
 
 _c_float_p = ctypes.POINTER(ctypes.c_float)
 _vp = ctypes.c_void_p
@@ -52,7 +52,7 @@ SIGNATURES = {
     "imask_last_launch_count": (ctypes.c_int, []),
     "imask_probe_ffma_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "imask_probe_smem_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
-    "imask_sq_dist": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp]),
+    "imask_sq_dist": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _vp]),
     "imask_plan_create": (
         ctypes.c_int,
         [

@@ -1,14 +1,15 @@
 // Solver metrics on the device (run()'s record rows, solvers.py:382-390): the
 // squared distance ||x - ref||^2 accumulated in float64 with a fixed-order
-// two-kernel reduction (deterministic), so recording a row costs two small
-// launches and an 8-byte async read-back instead of a host synchronisation.
+// reduction (block partials summed in block order by the last block), so
+// recording a row costs one small launch and an 8-byte async read-back
+// instead of a host synchronisation.
 #include <cuda_runtime.h>
 
 #include "imask_b200.h"
 
 namespace {
 
-constexpr int kBlocks = IMASK_SQDIST_SCRATCH - 1;
+constexpr int kBlocks = IMASK_SQDIST_SCRATCH - 2;
 constexpr int kThreads = 256;
 
 __device__ __forceinline__ double block_sum(double v) {
@@ -26,8 +27,11 @@ __device__ __forceinline__ double block_sum(double v) {
 }
 
 __global__ void __launch_bounds__(kThreads)
-k_sq_dist_partial(const float* __restrict__ x, const float* __restrict__ ref, int64_t n,
-                  double* __restrict__ out) {
+k_sq_dist(const float* __restrict__ x, const float* __restrict__ ref, int64_t n,
+          double* __restrict__ out, double* __restrict__ result) {
+  // out[1 .. kBlocks]: block partials; out[kBlocks + 1] (as an unsigned counter):
+  // blocks done. The last block to finish sums the partials in block order, so
+  // the result does not depend on scheduling.
   double s = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
        i += (int64_t)kBlocks * kThreads) {
@@ -35,23 +39,31 @@ k_sq_dist_partial(const float* __restrict__ x, const float* __restrict__ ref, in
     s = fma(d, d, s);
   }
   s = block_sum(s);
-  if (threadIdx.x == 0) out[1 + blockIdx.x] = s;
-}
-
-__global__ void __launch_bounds__(kThreads) k_sq_dist_final(double* __restrict__ out) {
-  double s = 0.0;
-  for (int i = threadIdx.x; i < kBlocks; i += kThreads) s += out[1 + i];
-  s = block_sum(s);
-  if (threadIdx.x == 0) out[0] = s;
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    out[1 + blockIdx.x] = s;
+    __threadfence();
+    unsigned int* done = reinterpret_cast<unsigned int*>(out + 1 + kBlocks);
+    last = atomicAdd(done, 1u) == kBlocks - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double t = 0.0;
+  for (int i = threadIdx.x; i < kBlocks; i += kThreads) t += ((volatile double*)out)[1 + i];
+  t = block_sum(t);
+  if (threadIdx.x == 0) {
+    *result = t;
+    *reinterpret_cast<unsigned int*>(out + 1 + kBlocks) = 0u;  // re-arm for the next call
+  }
 }
 
 }  // namespace
 
 extern "C" IMASK_API int imask_sq_dist(const float* x, const float* ref, int64_t n, double* out,
-                                       void* stream) {
+                                       double* result, void* stream) {
   if (!x || !out || n < 0) return IMASK_EINVAL;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  k_sq_dist_partial<<<kBlocks, kThreads, 0, s>>>(x, ref, n, out);
-  k_sq_dist_final<<<1, kThreads, 0, s>>>(out);
+  k_sq_dist<<<kBlocks, kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      x, ref, n, out, result ? result : out);
   return cudaGetLastError() == cudaSuccess ? IMASK_OK : IMASK_ECUDA;
 }

@@ -420,8 +420,11 @@ class _Recorder:
         self.device = device
         self.ref_sq = (float(torch.dot(x_ref.double(), x_ref.double()))
                        if x_ref is not None else float("nan"))
-        self.scratch = torch.empty(_lib.IMASK_SQDIST_SCRATCH, dtype=torch.float64, device=device)
+        self.scratch = torch.zeros(_lib.IMASK_SQDIST_SCRATCH, dtype=torch.float64, device=device)
+        self.dev_rows = torch.zeros(max(capacity, 1), dtype=torch.float64, device=device)
         self.host = torch.zeros(max(capacity, 1), dtype=torch.float64).pin_memory()
+        # read-backs ride a side stream so the solver stream never waits for a copy
+        self.copy_stream = torch.cuda.Stream(device=device)
         self.meta: list = []
         self.events: list = []
         self.ev0 = torch.cuda.Event(enable_timing=True)
@@ -436,16 +439,22 @@ class _Recorder:
                 raise ValueError("x_ref must match the iterate's shape")
             _lib.check(_lib.lib().imask_sq_dist(
                 ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(self.ref.data_ptr()), x.numel(),
-                ctypes.c_void_p(self.scratch.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
-            self.host[idx:idx + 1].copy_(self.scratch[:1], non_blocking=True)
+                ctypes.c_void_p(self.scratch.data_ptr()),
+                ctypes.c_void_p(self.dev_rows[idx:idx + 1].data_ptr()),
+                ctypes.c_void_p(stream.cuda_stream)))
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(stream)
+        if self.ref is not None:
+            self.copy_stream.wait_event(ev)
+            with torch.cuda.stream(self.copy_stream):
+                self.host[idx:idx + 1].copy_(self.dev_rows[idx:idx + 1], non_blocking=True)
         self.meta.append((k, cost, level, x.numel()))
         self.events.append(ev)
 
     def rows(self) -> list:
         if self.events:
             self.events[-1].synchronize()
+        self.copy_stream.synchronize()
         out = []
         for idx, ((k, cost, level, d), ev) in enumerate(zip(self.meta, self.events)):
             if self.ref is None:

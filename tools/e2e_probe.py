@@ -1,4 +1,5 @@
-"""Break down bench.py's e2e leg (config D) into its host-visible phases."""
+"""Break down bench.py's e2e leg (config D): host wall time of solvers.run vs the
+device span its metric rows record, with and without per-step rows."""
 import os
 import sys
 import time
@@ -16,31 +17,29 @@ r = cfg.levels
 geom = ctmodel.Geometry(cfg.side, cfg.n_angles, cfg.n_det)
 fam = mrsketch.make_family(r, cfg.side, [1.0 / r] * r, mode="coarse")
 x_true = ellipse_phantom(cfg.side, 0).astype(np.float32).ravel()
-b_host = torch.randn(geom.m).pin_memory()
-xref_host = torch.from_numpy(x_true).pin_memory()
 dev = torch.device("cuda", 0)
-
-
-def phase(name, fn):
+b = torch.randn(geom.m, device=dev)
+xref = torch.from_numpy(x_true).to(dev)
+prob = dist_mod.make_sharded_problem(geom, b, fam, cfg.mu_g)
+prm = solvers._params(1e-6, cfg.mu_g, cfg.mu_g)
+prob.engine.capture_all(solvers.init_state(prob, seed=1), prm)
+solvers.run(prob, "sketch", 1e-6, cfg.mu_g, 5, record_every=1, seed=1, x_ref=xref)
+for rec_every in (1, 1, 200, 200):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    out = fn()
+    rep = solvers.run(prob, "sketch", 1e-6, cfg.mu_g, 200, record_every=rec_every, seed=1, x_ref=xref)
     torch.cuda.synchronize()
-    print(f"{name:32s} {1e3 * (time.perf_counter() - t0):9.2f} ms", flush=True)
-    return out
-
-
-for rep in range(2):
-    print(f"-- rep {rep}")
-    b_dev = phase("h2d", lambda: b_host.to(dev, non_blocking=True))
-    xref = xref_host.to(dev)
-    prob = phase("make_sharded_problem", lambda: dist_mod.make_sharded_problem(geom, b_dev, fam, cfg.mu_g))
-    st = phase("init_state", lambda: solvers.init_state(prob, seed=1))
-    prm = solvers._params(1e-6, cfg.mu_g, cfg.mu_g)
-    phase("graph capture x6", lambda: [prob.engine.graph(st, lv, prm) for lv in range(r)])
-    sched = solvers.draw_levels(1, 0, 100, prob.cum_probs)
-    phase("100 steps (no record)", lambda: [solvers._device_step(prob.engine, st, int(i), prm) for i in sched])
-    phase("100 metrics", lambda: [solvers._metrics(st.x, xref) for _ in range(100)])
-    prob.engine.release_graphs()
-    phase("run(100, record_every=1)", lambda: solvers.run(prob, "sketch", 1e-6, cfg.mu_g, 100,
-                                                         record_every=1, seed=1, x_ref=xref))
+    wall = time.perf_counter() - t0
+    span = rep.rows[-1][5] - rep.rows[0][5]
+    print(f"record_every={rec_every:3d}: wall {1e3 * wall:7.2f} ms  device span k=0..200 "
+          f"{1e3 * span:7.2f} ms  first row at {1e3 * rep.rows[0][5]:6.2f} ms", flush=True)
+# the same 200 steps through the step graphs alone
+st = solvers.init_state(prob, seed=1)
+sched = solvers.draw_levels(1, 0, 200, prob.cum_probs)
+for _ in range(2):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i in sched:
+        solvers._device_step(prob.engine, st, int(i), prm)
+    torch.cuda.synchronize()
+    print(f"200 bare graph steps: {1e3 * (time.perf_counter() - t0):7.2f} ms", flush=True)
