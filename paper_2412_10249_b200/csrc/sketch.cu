@@ -250,13 +250,20 @@ k_saga_image_coarse32(const float* __restrict__ bp, int side, int f, float inv_f
 __global__ void __launch_bounds__(256)
 k_prepare(const float* __restrict__ u, int n, float2* __restrict__ P, float2* __restrict__ PT,
           float2* __restrict__ PM, float2* __restrict__ PTM) {
-  __shared__ float t[33][35];  // t[rr][cc] = u[r0 + rr][c0 - 1 + cc]
+  // t[rr][cc] = u[r0 + rr][c0 - 1 + cc]; for the symmetric layout also the tile
+  // of the mirrored image um[R][C] = u[R][n-1-C] at the same coordinates, so
+  // every output is one coalesced float2 (a value of u, the same of um)
+  __shared__ float t[33][35];
+  __shared__ float tm[33][35];
+  const bool sym = PM != nullptr;
   const int pitch = pair_pitch(n);
   const int r0 = blockIdx.y * 32 - 1 - kPadC, c0 = blockIdx.x * 32 - 1 - kPadC;
   for (int e = threadIdx.x; e < 33 * 34; e += blockDim.x) {
     const int rr = e / 34, cc = e % 34;
     const int R = r0 + rr, C = c0 - 1 + cc;
-    t[rr][cc] = (R >= 0 && R < n && C >= 0 && C < n) ? __ldg(u + (size_t)R * n + C) : 0.f;
+    const bool in = R >= 0 && R < n && C >= 0 && C < n;
+    t[rr][cc] = in ? __ldg(u + (size_t)R * n + C) : 0.f;
+    if (sym) tm[rr][cc] = in ? __ldg(u + (size_t)R * n + (n - 1 - C)) : 0.f;
   }
   __syncthreads();
   for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
@@ -265,21 +272,15 @@ k_prepare(const float* __restrict__ u, int n, float2* __restrict__ P, float2* __
     {
       const int R = r0 + rr, C = c0 + cc, idx = C + 1 + kPadC;
       if (R >= 0 && R < n && idx < pitch) {
-        const float v = t[rr][cc + 1];
-        if (!PM) {
-          P[(size_t)R * pitch + idx] = make_float2(v, t[rr][cc + 2] - v);
+        const float v = t[rr][cc + 1], dv = t[rr][cc + 2] - v;
+        const size_t o = (size_t)R * pitch + idx;
+        if (!sym) {
+          P[o] = make_float2(v, dv);
         } else {
-          // value planes (u, um) in P and difference planes (d, dm) in PM; the
-          // mirrored column c' = n-1-C holds (um, dm) = (u[C], u[C-1] - u[C])
-          float* pu = reinterpret_cast<float*>(P + (size_t)R * pitch);
-          float* pd = reinterpret_cast<float*>(PM + (size_t)R * pitch);
-          pu[2 * idx] = v;
-          pd[2 * idx] = t[rr][cc + 2] - v;
-          const int idm = n - 1 - C + 1 + kPadC;
-          if (idm >= 0 && idm < pitch) {
-            pu[2 * idm + 1] = v;
-            pd[2 * idm + 1] = t[rr][cc] - v;
-          }
+          // value planes (u, um) in P, difference planes (d, dm) in PM
+          const float vm = tm[rr][cc + 1];
+          P[o] = make_float2(v, vm);
+          PM[o] = make_float2(dv, tm[rr][cc + 2] - vm);
         }
       }
     }
@@ -287,16 +288,16 @@ k_prepare(const float* __restrict__ u, int n, float2* __restrict__ P, float2* __
     {
       const int C = c0 + rr, idx = r0 + cc + 1 + kPadC;
       if (C >= 0 && C < n && idx < pitch) {
-        const float v = t[cc][rr + 1];
-        const float dv = t[cc + 1][rr + 1] - v;
-        if (!PTM) {
-          PT[(size_t)C * pitch + idx] = make_float2(v, dv);
+        const float v = t[cc][rr + 1], dv = t[cc + 1][rr + 1] - v;
+        const size_t o = (size_t)C * pitch + idx;
+        if (!sym) {
+          PT[o] = make_float2(v, dv);
         } else {
-          // band C of the transposed image and band n-1-C of its mirror
-          reinterpret_cast<float*>(PT + (size_t)C * pitch)[2 * idx] = v;
-          reinterpret_cast<float*>(PTM + (size_t)C * pitch)[2 * idx] = dv;
-          reinterpret_cast<float*>(PT + (size_t)(n - 1 - C) * pitch)[2 * idx + 1] = v;
-          reinterpret_cast<float*>(PTM + (size_t)(n - 1 - C) * pitch)[2 * idx + 1] = dv;
+          // band C of the transposed image and of the transposed mirror image
+          // (= band n-1-C of the transposed image)
+          const float vm = tm[cc][rr + 1];
+          PT[o] = make_float2(v, vm);
+          PTM[o] = make_float2(dv, tm[cc + 1][rr + 1] - vm);
         }
       }
     }
