@@ -187,6 +187,28 @@ IMASK_API int imask_step_forward(imask_plan* plan, const imask_state* st, int le
                                  const imask_step_params* prm, void* stream);
 IMASK_API int imask_step_image(imask_plan* plan, const imask_state* st, int level0,
                                const imask_step_params* prm, void* stream);
+/* One iteration of the deterministic primal-dual reference solver on the
+ * unsketched operator K (the plan's f = 1 projector, with its scale),
+ * replacing the loop body of pdhg_solve / run(..., "pdhg") (solvers.py:
+ * 331-337, 433-446) for the ridge g and the quadratic-data conjugate f*:
+ *   y    <- (y + sigma K xbar - sigma b) / (1 + sigma)
+ *   x'   <- (x - tau K^T y) / (1 + tau mu_g)
+ *   xbar <- x' + theta (x' - x);  x <- x'
+ * Buffers: x, xbar, bp (scratch): side*side; y, b: n_loc*n_det. Single GPU
+ * (the adjoint is not reduced over ranks). */
+typedef struct imask_pdhg_state {
+  float* x;
+  float* xbar;
+  float* y;
+  const float* b;
+  float* bp;
+} imask_pdhg_state;
+typedef struct imask_pdhg_params {
+  double sigma, tau, theta; /* pdhg_parameters (solvers.py:308-318) */
+  double mu_g;              /* ridge weight of g */
+} imask_pdhg_params;
+IMASK_API int imask_pdhg_step(imask_plan* plan, const imask_pdhg_state* st,
+                              const imask_pdhg_params* prm, void* stream);
 /* Recompute phi_sum / psi_sum from the tables in index order (_resum,
  * solvers.py:184-191). */
 IMASK_API int imask_resum(imask_plan* plan, const imask_state* st, void* stream);

@@ -7,7 +7,9 @@ path: the counter-based RNG `_mix64` / `uniform_at` / `draw_level`
 (solvers.py:194-221) with the ridge prox (proxlib.py:51-63) and the prox of
 the quadratic data term's conjugate (proxlib.py:30-48). The sketched
 operators follow `sketch_forward` in coarse mode (mrsketch.py:181-204):
-K_i = R_f . T_f for i < r and K_r = K . S_r.
+K_i = R_f . T_f for i < r and K_r = K . S_r. Also the deterministic
+primal-dual reference solver `pdhg_solve` with its parameters and the power
+method for ||K|| (solvers.py:308-342, linops.py:181-209).
 """
 
 from __future__ import annotations
@@ -164,3 +166,46 @@ def sketch_step(st: State, ops: SketchedCT, b: np.ndarray, sigma: float, mu: flo
     if st.k % st.resum_every == 0:
         resum(st, ops.probs)
     return st
+
+
+def power_norm(apply, adjoint_apply, dim: int, tol: float = 1e-8, max_iter: int = 2000,
+               seed: int = 0) -> float:
+    """||K|| by power iteration on K^T K (linops.py:181-209), float64."""
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(dim)
+    v /= np.linalg.norm(v)
+    estimate = 0.0
+    for _ in range(max_iter):
+        w = adjoint_apply(apply(v))
+        new = float(np.sqrt(max(float(np.dot(v, w)), 0.0)))
+        wn = float(np.linalg.norm(w))
+        if wn == 0.0:
+            return 0.0
+        v = w / wn
+        if estimate > 0.0 and abs(new - estimate) < tol * estimate:
+            return new
+        estimate = new
+    return estimate
+
+
+def pdhg_parameters(k_norm: float, mu: float, rho: float = 0.99):
+    """(sigma, tau, theta, kappa) of the reference solver (solvers.py:308-318)."""
+    kappa = np.sqrt(1.0 + k_norm ** 2 / (mu * rho ** 2))
+    return 1.0 / (kappa - 1.0), 1.0 / ((kappa - 1.0) * mu), 1.0 - 2.0 / (1.0 + kappa), kappa
+
+
+def pdhg_solve(apply, adjoint_apply, b: np.ndarray, mu_g: float, mu: float, iters: int,
+               k_norm: float, rho: float = 0.99) -> np.ndarray:
+    """pdhg_solve (solvers.py:321-342) for the ridge g and the quadratic-data
+    conjugate f*: y <- (y + s K xbar - s b)/(1+s), x' <- (x - t K^T y)/(1 + t mu_g),
+    xbar <- x' + theta (x' - x)."""
+    sigma, tau, theta, _ = pdhg_parameters(k_norm, mu, rho)
+    x = np.zeros(adjoint_apply(np.zeros_like(b)).size)
+    y = np.zeros_like(b)
+    xbar = x
+    for _ in range(iters):
+        y = ((y + sigma * apply(xbar)) - sigma * b) / (1.0 + sigma)
+        x_new = (x - tau * adjoint_apply(y)) / (1.0 + tau * mu_g)
+        xbar = x_new + theta * (x_new - x)
+        x = x_new
+    return x

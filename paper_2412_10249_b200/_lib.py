@@ -41,6 +41,15 @@ class ImaskState(ctypes.Structure):
     ]
 
 
+class ImaskPdhgState(ctypes.Structure):
+    _fields_ = [("x", _vp), ("xbar", _vp), ("y", _vp), ("b", _vp), ("bp", _vp)]
+
+
+class ImaskPdhgParams(ctypes.Structure):
+    _fields_ = [("sigma", ctypes.c_double), ("tau", ctypes.c_double),
+                ("theta", ctypes.c_double), ("mu_g", ctypes.c_double)]
+
+
 class ImaskStepParams(ctypes.Structure):
     _fields_ = [("sigma", ctypes.c_double), ("mu", ctypes.c_double), ("mu_g", ctypes.c_double)]
 
@@ -117,6 +126,10 @@ SIGNATURES = {
     ),
     "imask_graph_launch": (ctypes.c_int, [_vp, _vp]),
     "imask_graph_destroy": (ctypes.c_int, [_vp]),
+    "imask_pdhg_step": (
+        ctypes.c_int,
+        [_vp, ctypes.POINTER(ImaskPdhgState), ctypes.POINTER(ImaskPdhgParams), _vp],
+    ),
     "imask_step_graph_update": (
         ctypes.c_int,
         [_vp, _vp, ctypes.POINTER(ImaskState), ctypes.c_int, ctypes.POINTER(ImaskStepParams)],

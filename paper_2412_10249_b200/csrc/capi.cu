@@ -41,6 +41,8 @@ cudaError_t launch_saga_image_coarse(const float* bp, int side, int f, const Ima
                                      cudaStream_t s);
 cudaError_t launch_saga_image_full(const float* bp, int side, const CompParams& cp,
                                    const ImageSaga& sg, cudaStream_t s);
+cudaError_t launch_pdhg_image(const float* bp, float* x, float* xbar, size_t d, float tau,
+                              float inv_den, float theta, cudaStream_t s);
 cudaError_t launch_resum(const float* phi_tab, float* phi_sum, int side, const float* psi_tab,
                          float* psi_sum, size_t m, const ResumParams& rp, cudaStream_t s);
 void init_kernel_attributes();
@@ -997,6 +999,42 @@ int imask_graph_destroy(imask_graph* gr) {
   if (gr->exec) cudaGraphExecDestroy(gr->exec);
   if (gr->graph) cudaGraphDestroy(gr->graph);
   delete gr;
+  return IMASK_OK;
+}
+
+int imask_pdhg_step(imask_plan* pl, const imask_pdhg_state* st, const imask_pdhg_params* prm,
+                    void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (!pl || !st || !prm) return fail(IMASK_EINVAL, "null argument");
+  if (!(prm->sigma > 0.0) || !(prm->tau > 0.0) || !(prm->mu_g > 0.0))
+    return fail(IMASK_EINVAL, "sigma, tau and mu_g must be positive");
+  DeviceGuard g(pl->device);
+  const int n = pl->side;
+  LevelTables* t;
+  int rc;
+  if ((rc = get_tables(pl, 1, &t))) return rc;
+  const cudaStream_t s = S(stream);
+  if (pl->n_loc > 0) {
+    // dual step: K xbar fused with the conjugate prox in the forward epilogue
+    LAUNCH(launch_prepare(st->xbar, n, pl->P, pl->PT, pl->PM, pl->PTM, s), "prepare");
+    SinoSaga sg{};
+    sg.psi_tab = nullptr;  // no SAGA tables: zeta = K xbar
+    sg.psi_sum = nullptr;
+    sg.y_in = st->y;
+    sg.y = st->y;
+    sg.b = st->b;
+    sg.sigma = (float)prm->sigma;
+    sg.inv_1ps = (float)(1.0 / (1.0 + prm->sigma));
+    if ((rc = run_forward(pl, 1, t, nullptr, &sg, s))) return rc;
+    // primal step from the new dual
+    if ((rc = run_adjoint(pl, 1, st->y, st->bp, t->adj, s))) return rc;
+  } else {
+    LAUNCH(cudaMemsetAsync(st->bp, 0, sizeof(float) * n * n, s), "memset");
+  }
+  LAUNCH(launch_pdhg_image(st->bp, st->x, st->xbar, (size_t)n * n, (float)prm->tau,
+                           (float)(1.0 / (1.0 + prm->tau * prm->mu_g)), (float)prm->theta, s),
+         "pdhg image");
   return IMASK_OK;
 }
 

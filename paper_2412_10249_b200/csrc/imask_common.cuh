@@ -129,10 +129,14 @@ struct SideStream {
 struct SinoIn {
   float po = 0.f, ps = 0.f, yv = 0.f, bv = 0.f;
 };
+// psi_tab == nullptr is the PDHG dual step (solvers.py:333-334): no tables, so
+// zeta = val and y' = (y + sigma K xbar - sigma b) / (1 + sigma).
 __device__ __forceinline__ SinoIn sino_load(const SinoSaga& sg, size_t q) {
   SinoIn in;
-  in.po = sg.psi_tab[q];
-  in.ps = sg.psi_sum[q];
+  if (sg.psi_tab) {
+    in.po = sg.psi_tab[q];
+    in.ps = sg.psi_sum[q];
+  }
   in.yv = sg.y_in[q];
   in.bv = __ldg(sg.b + q);
   return in;
@@ -141,8 +145,10 @@ __device__ __forceinline__ void sino_update(const SinoSaga& sg, size_t q, const 
                                             float val) {
   const float d = val - in.po;
   const float zeta = d + in.ps;
-  sg.psi_sum[q] = fmaf(sg.p_i, d, in.ps);
-  sg.psi_tab[q] = val;
+  if (sg.psi_tab) {
+    sg.psi_sum[q] = fmaf(sg.p_i, d, in.ps);
+    sg.psi_tab[q] = val;
+  }
   const float yv = fmaf(sg.sigma, zeta, in.yv);
   sg.y[q] = (yv - sg.sigma * in.bv) * sg.inv_1ps;
 }

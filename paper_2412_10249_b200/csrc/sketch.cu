@@ -359,6 +359,25 @@ k_saga_image_full(const float* __restrict__ bp, int side, CompParams cp, ImageSa
   }
 }
 
+// ---- PDHG primal step (solvers.py:335-337) -----------------------------------
+// x' = (x - tau K^T y) / (1 + tau mu_g) (ridge prox), xbar = x' + theta (x' - x).
+__global__ void __launch_bounds__(256)
+k_pdhg_image(const float* __restrict__ bp, float* __restrict__ x, float* __restrict__ xbar,
+             size_t d, float tau, float inv_den, float theta) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d) return;
+  const float xo = x[i];
+  const float xn = fmaf(-tau, __ldg(bp + i), xo) * inv_den;
+  x[i] = xn;
+  xbar[i] = fmaf(theta, xn - xo, xn);
+}
+
+cudaError_t launch_pdhg_image(const float* bp, float* x, float* xbar, size_t d, float tau,
+                              float inv_den, float theta, cudaStream_t s) {
+  k_pdhg_image<<<(unsigned)((d + 255) / 256), 256, 0, s>>>(bp, x, xbar, d, tau, inv_den, theta);
+  return cudaGetLastError();
+}
+
 // ---- resum (solvers.py:184-191) --------------------------------------------
 
 __global__ void k_resum_image(const float* __restrict__ phi_tab, float* __restrict__ phi_sum,

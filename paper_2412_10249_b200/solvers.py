@@ -17,8 +17,10 @@ all-reduced between the first and the last call while the forward runs.
 Storage difference: coarse phi rows are kept compact ((side/f)^2 values)
 since the reference's full-resolution rows are their replication
 (mrsketch.py:54-55); `SaddleState.phi_full(i)` returns the reference layout.
-The other algorithms of `run` (pdhg, sketch-seq, saga-saddle) are the
-SURVEY §8(f) "next" rows.
+`pdhg_solve` / `run(..., "pdhg")` (solvers.py:308-342, 433-446; SURVEY
+§8(f) rank 1) run on the device too, one native call per iteration when K
+is the B200 projector. sketch-seq and saga-saddle are the remaining §8(f)
+rows.
 """
 
 from __future__ import annotations
@@ -32,7 +34,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .ctmodel import Geometry, get_plan, shard_angles
+from .ctmodel import Geometry, ProjectorMeta, get_plan, shard_angles
 from .linops import LinOp, to_device
 from .mrsketch import SketchFamily, SketchedMeta, cost_fraction, forward_family
 from .proxlib import ProxFn
@@ -498,6 +500,82 @@ class SolveReport:
         return np.array([row[3] for row in self.rows])
 
 
+def pdhg_parameters(k_norm: float, mu: float, rho: float = 0.99):
+    """Strong-convexity step sizes (sigma, tau, theta, kappa) of the reference
+    solver (solvers.py:308-318)."""
+    if k_norm <= 0:
+        raise ValueError("operator norm must be positive for the reference parameters")
+    if mu <= 0:
+        raise ValueError("mu must be positive")
+    kappa = float(np.sqrt(1.0 + k_norm ** 2 / (mu * rho ** 2)))
+    sigma = 1.0 / (kappa - 1.0)
+    tau = 1.0 / ((kappa - 1.0) * mu)
+    theta = 1.0 - 2.0 / (1.0 + kappa)
+    return sigma, tau, theta, kappa
+
+
+class _Pdhg:
+    """PDHG iterate on the device (solvers.py:321-342, 433-446).
+
+    With the B200 projector as K (one GPU), the ridge g and the quadratic-data
+    conjugate f*, an iteration is one native call (imask_pdhg_step: the dual
+    prox fused into the forward epilogue, the adjoint, one elementwise primal
+    kernel); any other problem runs the same recursion with its LinOp and prox
+    callables on device tensors.
+    """
+
+    def __init__(self, prob: "Problem", sigma: float, tau: float, theta: float):
+        self.prob, self.sigma, self.tau, self.theta = prob, sigma, tau, theta
+        meta = getattr(prob.K, "meta", None)
+        self.plan = None
+        if (isinstance(meta, ProjectorMeta) and meta.factor == 1 and prob.shard.world == 1
+                and prob.g.kind == "ridge" and prob.f_conj.kind == "quadratic_conjugate"):
+            eng = prob.engine
+            if eng is not None and eng.plan.scale == meta.scale:
+                self.plan = eng.plan
+            else:
+                self.plan = get_plan(meta.geom, scale=meta.scale, angles=meta.angles)
+        dev = self.plan.device if self.plan is not None else None
+        self.x = torch.zeros(prob.K.domain_dim, device=dev or "cuda")
+        self.y = torch.zeros(prob.K.range_dim, device=self.x.device)
+        self.xbar = self.x.clone()
+        if self.plan is not None:
+            self.b = prob.f_conj.param.to(self.x.device, torch.float32).contiguous()
+            self.bp = torch.empty_like(self.x)
+            self._st = _lib.ImaskPdhgState(self.x.data_ptr(), self.xbar.data_ptr(),
+                                           self.y.data_ptr(), self.b.data_ptr(),
+                                           self.bp.data_ptr())
+            self._prm = _lib.ImaskPdhgParams(sigma, tau, theta, float(prob.g.param))
+
+    def step(self) -> None:
+        if self.plan is not None:
+            _lib.check(_lib.lib().imask_pdhg_step(self.plan.handle, ctypes.byref(self._st),
+                                                  ctypes.byref(self._prm), self.plan.stream))
+            return
+        prob = self.prob
+        self.y.copy_(prob.f_conj.prox(self.y + self.sigma * prob.K.apply(self.xbar), self.sigma))
+        x_new = prob.g.prox(self.x - self.tau * prob.K.adjoint_apply(self.y), self.tau)
+        self.xbar.copy_(x_new + self.theta * (x_new - self.x))
+        self.x.copy_(x_new)
+
+
+def pdhg_solve(prob: "Problem", mu: float, iters: int = 5000, k_norm: Optional[float] = None,
+               rho: float = 0.99) -> torch.Tensor:
+    """Deterministic primal-dual reference solution of the unsketched problem
+    (solvers.py:321-342), on the device."""
+    if prob.shard.world > 1:
+        raise NotImplementedError("pdhg_solve runs on one GPU (the unsharded problem)")
+    if k_norm is None:
+        from .linops import power_method
+
+        k_norm = power_method(prob.K, tol=1e-8, max_iter=2000, seed=0).norm
+    sigma, tau, theta, _ = pdhg_parameters(k_norm, mu, rho)
+    it = _Pdhg(prob, sigma, tau, theta)
+    for _ in range(iters):
+        it.step()
+    return it.x
+
+
 def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
         record_every: int = 1, seed: int = 0, x_ref=None, theta_extrap: float = 1.0,
         resum_every: int = 1000, snapshot_costs: Sequence[float] = ()) -> SolveReport:
@@ -508,9 +586,11 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
     """
     if algorithm not in ALGORITHMS:
         raise ValueError(f"unknown algorithm {algorithm!r}; expected one of {ALGORITHMS}")
+    if algorithm == "pdhg":
+        return _run_pdhg(prob, mu, iters, record_every, seed, x_ref, snapshot_costs)
     if algorithm != "sketch":
         raise NotImplementedError(
-            f"{algorithm!r} is a SURVEY 8(f) 'next' row; the B200 path runs 'sketch'"
+            f"{algorithm!r} is a SURVEY 8(f) 'next' row; the B200 path runs 'sketch' and 'pdhg'"
         )
     eng = _require_engine(prob)
     x_ref_t = None if x_ref is None else to_device(x_ref, eng.device)
@@ -540,4 +620,34 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
             record(k, state.cost, state.last_level, state.x)
     rows = rec.rows()
     return SolveReport(rows=rows, x=state.x, y=state.y, algorithm=algorithm, seed=seed,
+                       snapshots=snapshots)
+
+
+def _run_pdhg(prob: Problem, mu: float, iters: int, record_every: int, seed: int, x_ref,
+              snapshot_costs: Sequence[float]) -> SolveReport:
+    """run(..., "pdhg"): sigma is ignored; the strong-convexity parameters come
+    from mu and the operator norm (solvers.py:433-452). Cost ledger: 2 per
+    iteration (one full forward and one full adjoint), level column 0."""
+    if prob.shard.world > 1:
+        raise NotImplementedError("run(..., 'pdhg') runs on one GPU (the unsharded problem)")
+    from .linops import power_method
+
+    t0 = time.perf_counter()
+    k_norm = power_method(prob.K, tol=1e-8, max_iter=2000, seed=0).norm
+    sig, tau, theta, _ = pdhg_parameters(k_norm, mu)
+    it = _Pdhg(prob, sig, tau, theta)
+    x_ref_t = None if x_ref is None else to_device(x_ref, it.x.device)
+    rec = _Recorder(x_ref_t, it.x.device, 2 + iters // max(record_every, 1), t0)
+    budgets = sorted(float(cb) for cb in snapshot_costs)
+    snapshots: dict = {}
+    rec.record(0, 0.0, 0, it.x)
+    cost = 0.0
+    for k in range(1, iters + 1):
+        it.step()
+        cost += 2.0
+        while budgets and cost >= budgets[0]:
+            snapshots[budgets.pop(0)] = it.x.clone()
+        if k % record_every == 0 or k == iters:
+            rec.record(k, cost, 0, it.x)
+    return SolveReport(rows=rec.rows(), x=it.x, y=it.y, algorithm="pdhg", seed=seed,
                        snapshots=snapshots)

@@ -318,4 +318,56 @@ def test_rejects_unsupported_problems():
     with pytest.raises(ValueError, match="sigma and mu_g must be positive"):
         solvers.sketch_step(st, prob, 0.0, 1.0)
     with pytest.raises(NotImplementedError):
-        solvers.run(prob, "pdhg", 1e-3, 1.0, 3)
+        solvers.run(prob, "sketch-seq", 1e-3, 1.0, 3)
+
+
+def test_pdhg_matches_oracle():
+    """pdhg_solve on the device (one imask_pdhg_step per iteration) against the
+    float64 restatement of solvers.py:321-342, same operator norm."""
+    side, na, nd, mu_g, mu = 32, 36, 47, 0.5, 0.5
+    orc = ct_oracle.ProjectorOracle(side, na, nd)
+    b = orc.apply(np.random.default_rng(12).random(side * side))
+    k_norm = so.power_norm(orc.apply, orc.adjoint_apply, side * side)
+    geom = ctmodel.Geometry(side, na, nd)
+    K = ctmodel.projector_op(geom)
+    fam = mrsketch.make_family(1, side, [1.0], mode="coarse")
+    prob = solvers.make_problem(K, b, fam, proxlib.ridge_fn(mu_g), proxlib.quadratic_conjugate_fn(b),
+                                coarse_projector=lambda f: ctmodel.coarse_projector(geom, f))
+    x_ref = so.pdhg_solve(orc.apply, orc.adjoint_apply, b, mu_g, mu, 300, k_norm)
+    x = solvers.pdhg_solve(prob, mu, iters=300, k_norm=k_norm)
+    assert rel_l2(host(x), x_ref) <= 1e-4
+    # the generic device path (a LinOp the engine does not recognise) agrees
+    K_plain = linops.LinOp(K.domain_dim, K.range_dim, K.apply, K.adjoint_apply)
+    prob2 = solvers.Problem(K=K_plain, b=prob.b, g=prob.g, f_conj=prob.f_conj, probs=prob.probs,
+                            ops=prob.ops, fractions=prob.fractions, family=prob.family)
+    x2 = solvers.pdhg_solve(prob2, mu, iters=300, k_norm=k_norm)
+    assert rel_l2(host(x2), host(x)) <= 1e-5
+
+
+def test_pdhg_reaches_dense_ridge_solution():
+    """test_solvers.py:277-281 on the device: 5000 PDHG iterations reach the
+    closed-form ridge solution (to float32 precision)."""
+    side, na, nd = 16, 20, 23
+    orc = ct_oracle.ProjectorOracle(side, na, nd)
+    Kd = orc.to_csr().toarray()
+    b = Kd @ np.random.default_rng(13).random(side * side)
+    x_hat = np.linalg.solve(Kd.T @ Kd + np.eye(side * side), Kd.T @ b)
+    prob = build(side, na, nd, [1.0], b, mu_g=1.0)
+    x = solvers.pdhg_solve(prob, mu=1.0, iters=5000)
+    assert rel_l2(host(x), x_hat) <= 2e-5
+
+
+def test_run_pdhg_rows_and_ledger():
+    side, na, nd = 32, 36, 47
+    orc = ct_oracle.ProjectorOracle(side, na, nd)
+    x_true = np.random.default_rng(14).random(side * side)
+    b = orc.apply(x_true)
+    prob = build(side, na, nd, [0.5, 0.5], b, mu_g=1e-2)
+    rep = solvers.run(prob, "pdhg", 123.0, 1e-2, 20, record_every=5, x_ref=x_true)
+    assert [r[0] for r in rep.rows] == [0, 5, 10, 15, 20]
+    assert [r[1] for r in rep.rows] == [0.0, 10.0, 20.0, 30.0, 40.0]
+    assert all(r[2] == 0 for r in rep.rows)
+    x = solvers.pdhg_solve(prob, 1e-2, iters=20)
+    assert np.array_equal(host(rep.x), host(x))
+    rel = float(np.dot(host(x) - x_true, host(x) - x_true) / np.dot(x_true, x_true))
+    assert abs(rep.rows[-1][3] - rel) <= 1e-6 * rel

@@ -94,3 +94,18 @@ def test_epoch_iteration_counts():
     # E[dcost/iter] = 2 sum_i p_i / f_i: A 1.1667, D 0.65625
     assert CONFIGS["A"].iters_for_epochs() == math.ceil(20 / (2 * (1 / 3) * (1 / 4 + 1 / 2 + 1)))
     assert CONFIGS["D"].iters_for_epochs() == math.ceil(50 / 0.65625)
+
+
+def test_pdhg_parameter_formulas():
+    """test_solvers.py:258-271: ||K||^2 = 3 mu rho^2 gives kappa 2, sigma 1,
+    tau 1/mu, theta 1/3; a zero norm is rejected."""
+    from paper_2412_10249_b200.solvers import pdhg_parameters
+
+    mu, rho = 2.0, 0.99
+    sigma, tau, theta, kappa = pdhg_parameters(np.sqrt(3.0 * mu * rho ** 2), mu, rho)
+    assert kappa == pytest.approx(2.0, rel=1e-12)
+    assert sigma == pytest.approx(1.0, rel=1e-12)
+    assert tau == pytest.approx(1.0 / mu, rel=1e-12)
+    assert theta == pytest.approx(1.0 / 3.0, rel=1e-12)
+    with pytest.raises(ValueError):
+        pdhg_parameters(0.0, 1.0)
