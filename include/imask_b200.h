@@ -64,6 +64,9 @@ typedef struct imask_state {
    * the forward concurrently with the adjoint (which reads y^k); the caller
    * swaps y and y_next after each step. NULL: in-place update. */
   float* y_next;
+  /* Extrapolated primal point of the sequential variant (imask_seq_step):
+   * side*side, or NULL. */
+  float* xbar;
 } imask_state;
 
 /* Per-iteration scalars of sketch_step (solvers.py:194-221) with the ridge
@@ -209,6 +212,13 @@ typedef struct imask_pdhg_params {
 } imask_pdhg_params;
 IMASK_API int imask_pdhg_step(imask_plan* plan, const imask_pdhg_state* st,
                               const imask_pdhg_params* prm, void* stream);
+/* One sequential-update iteration with primal extrapolation, ImaSk-Seq
+ * (sketch_seq_step, solvers.py:265-305): psi_new = K_i xbar with the
+ * sinogram-side update and the dual prox (y in place), then phi_new =
+ * K_i^T y_new with the image-side update and the primal prox, then
+ * xbar = x' + theta (x' - x). theta in [0, 1]; st->xbar required. */
+IMASK_API int imask_seq_step(imask_plan* plan, const imask_state* st, int level0,
+                             const imask_step_params* prm, double theta, void* stream);
 /* Recompute phi_sum / psi_sum from the tables in index order (_resum,
  * solvers.py:184-191). */
 IMASK_API int imask_resum(imask_plan* plan, const imask_state* st, void* stream);

@@ -8,8 +8,9 @@ path: the counter-based RNG `_mix64` / `uniform_at` / `draw_level`
 the quadratic data term's conjugate (proxlib.py:30-48). The sketched
 operators follow `sketch_forward` in coarse mode (mrsketch.py:181-204):
 K_i = R_f . T_f for i < r and K_r = K . S_r. Also the deterministic
-primal-dual reference solver `pdhg_solve` with its parameters and the power
-method for ||K|| (solvers.py:308-342, linops.py:181-209).
+primal-dual reference solver `pdhg_solve` with its parameters, the power
+method for ||K|| (solvers.py:308-342, linops.py:181-209) and the sequential
+variant `sketch_seq_step` (solvers.py:265-305).
 """
 
 from __future__ import annotations
@@ -107,6 +108,7 @@ class State:
     last_level: int = 0
     resum_every: int = 1000
     levels: list = field(default_factory=list)
+    xbar: Optional[np.ndarray] = None
 
 
 def init_state(ops: SketchedCT, seed=0, x0=None, y0=None, exact_memory=False, resum_every=1000):
@@ -127,7 +129,8 @@ def init_state(ops: SketchedCT, seed=0, x0=None, y0=None, exact_memory=False, re
         psi = [np.zeros(m) for _ in range(r)]
         phi_sum = np.zeros(d)
         psi_sum = np.zeros(m)
-    return State(x, y, phi, psi, phi_sum, psi_sum, seed=seed, resum_every=resum_every)
+    return State(x, y, phi, psi, phi_sum, psi_sum, seed=seed, resum_every=resum_every,
+                 xbar=x.copy())
 
 
 def resum(st: State, probs) -> None:
@@ -159,6 +162,36 @@ def sketch_step(st: State, ops: SketchedCT, b: np.ndarray, sigma: float, mu: flo
     s = sigma / mu
     st.x = (st.x - s * xi) / (1.0 + s * mu_g)  # proxlib.py:51-55
     st.y = ((st.y + sigma * zeta) - sigma * b) / (1.0 + sigma)  # proxlib.py:30-34
+    st.k += 1
+    st.cost += 2.0 * ops.fraction(i)
+    st.last_level = i + 1
+    st.levels.append(i)
+    if st.k % st.resum_every == 0:
+        resum(st, ops.probs)
+    return st
+
+
+def sketch_seq_step(st: State, ops: SketchedCT, b: np.ndarray, sigma: float, mu: float,
+                    mu_g: float, theta_extrap: float) -> State:
+    """One sequential ImaSk-Seq iteration with primal extrapolation
+    (solvers.py:265-305), ridge g, quadratic f*."""
+    cum = np.cumsum(ops.probs)
+    i = draw_level(st.seed, st.k, cum)
+    p_i = ops.probs[i]
+    psi_new = ops.apply(i, st.xbar)
+    zeta = (psi_new - st.psi[i]) + st.psi_sum
+    st.psi_sum = st.psi_sum + p_i * (psi_new - st.psi[i])
+    st.psi[i] = psi_new
+    y_new = ((st.y + sigma * zeta) - sigma * b) / (1.0 + sigma)
+    phi_new = ops.adjoint_apply(i, y_new)
+    xi = (phi_new - st.phi[i]) + st.phi_sum
+    st.phi_sum = st.phi_sum + p_i * (phi_new - st.phi[i])
+    st.phi[i] = phi_new
+    s = sigma / mu
+    x_new = (st.x - s * xi) / (1.0 + s * mu_g)
+    st.xbar = x_new if theta_extrap == 0.0 else x_new + theta_extrap * (x_new - st.x)
+    st.x = x_new
+    st.y = y_new
     st.k += 1
     st.cost += 2.0 * ops.fraction(i)
     st.last_level = i + 1

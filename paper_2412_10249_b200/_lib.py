@@ -38,6 +38,7 @@ class ImaskState(ctypes.Structure):
         ("psi_tab", _vp),
         ("bp", _vp),
         ("y_next", _vp),
+        ("xbar", _vp),
     ]
 
 
@@ -126,6 +127,11 @@ SIGNATURES = {
     ),
     "imask_graph_launch": (ctypes.c_int, [_vp, _vp]),
     "imask_graph_destroy": (ctypes.c_int, [_vp]),
+    "imask_seq_step": (
+        ctypes.c_int,
+        [_vp, ctypes.POINTER(ImaskState), ctypes.c_int, ctypes.POINTER(ImaskStepParams),
+         ctypes.c_double, _vp],
+    ),
     "imask_pdhg_step": (
         ctypes.c_int,
         [_vp, ctypes.POINTER(ImaskPdhgState), ctypes.POINTER(ImaskPdhgParams), _vp],

@@ -356,6 +356,9 @@ constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
 
 namespace {
 
+int step_image(imask_plan* pl, const imask_state* st, int level0, const imask_step_params* prm,
+               float* xbar, double theta, void* stream);
+
 // Restriction (or compensation at the full level) of x into pl->u, then the
 // pair images of the forward projector.
 int stage_forward_input(imask_plan* pl, const float* x, int level0, cudaStream_t s) {
@@ -372,7 +375,7 @@ int stage_forward_input(imask_plan* pl, const float* x, int level0, cudaStream_t
 
 // psi_new = K_i u on this slab fused with the sinogram-side SAGA update.
 int forward_saga(imask_plan* pl, const imask_state* st, int level0, const imask_step_params* prm,
-                 const LevelTables* t, cudaStream_t stream) {
+                 const LevelTables* t, cudaStream_t stream, bool in_place = false) {
   if (pl->n_loc == 0) return IMASK_OK;
   const int f = pl->factors[level0];
   int rc;
@@ -381,7 +384,7 @@ int forward_saga(imask_plan* pl, const imask_state* st, int level0, const imask_
   sg.psi_tab = st->psi_tab + (size_t)level0 * m;
   sg.psi_sum = st->psi_sum;
   sg.y_in = st->y;
-  sg.y = st->y_next ? st->y_next : st->y;
+  sg.y = st->y_next && !in_place ? st->y_next : st->y;
   sg.b = st->b;
   sg.p_i = (float)pl->probs[level0];
   sg.sigma = (float)prm->sigma;
@@ -831,6 +834,46 @@ int imask_step_forward(imask_plan* pl, const imask_state* st, int level0,
 
 int imask_step_image(imask_plan* pl, const imask_state* st, int level0,
                      const imask_step_params* prm, void* stream) {
+  return step_image(pl, st, level0, prm, nullptr, 0.0, stream);
+}
+
+int imask_seq_step(imask_plan* pl, const imask_state* st, int level0,
+                   const imask_step_params* prm, double theta, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  int rc = check_level0(pl, level0);
+  if (rc) return rc;
+  if (!(prm->sigma > 0.0) || !(prm->mu_g > 0.0))
+    return fail(IMASK_EINVAL, "sigma and mu_g must be positive");
+  if (!(prm->mu > 0.0)) return fail(IMASK_EINVAL, "mu must be positive");
+  if (!(theta >= 0.0 && theta <= 1.0)) return fail(IMASK_EINVAL, "theta_extrap must lie in [0, 1]");
+  if (!st->xbar) return fail(IMASK_EINVAL, "sketch_seq_step needs st->xbar");
+  DeviceGuard g(pl->device);
+  const int f = pl->factors[level0];
+  const int n = pl->side / f;
+  LevelTables* t;
+  if ((rc = get_tables(pl, f, &t))) return rc;
+  const cudaStream_t s = S(stream);
+  // forward memory from the extrapolated point, dual first (in place) ...
+  if ((rc = stage_forward_input(pl, st->xbar, level0, s))) return rc;
+  if ((rc = forward_saga(pl, st, level0, prm, t, s, true))) return rc;
+  // ... then the adjoint memory from the new dual, the primal step and xbar
+  if (pl->n_loc == 0)
+    LAUNCH(cudaMemsetAsync(st->bp, 0, sizeof(float) * n * n, s), "memset");
+  else if ((rc = run_adjoint(pl, f, st->y, st->bp, t->adj, s)))
+    return rc;
+  const int launches = g_launches;
+  if ((rc = step_image(pl, st, level0, prm, st->xbar, theta, stream))) return rc;
+  g_launches += launches;
+  return IMASK_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int step_image(imask_plan* pl, const imask_state* st, int level0, const imask_step_params* prm,
+               float* xbar, double theta, void* stream) {
   g_err.clear();
   g_launches = 0;
   int rc = check_level0(pl, level0);
@@ -841,6 +884,8 @@ int imask_step_image(imask_plan* pl, const imask_state* st, int level0,
   DeviceGuard g(pl->device);
   const int f = pl->factors[level0];
   ImageSaga sg;
+  sg.xbar = xbar;
+  sg.theta = (float)theta;
   sg.phi_tab = st->phi_tab + pl->phi_off[level0];
   sg.phi_sum = st->phi_sum;
   sg.x = st->x;
@@ -854,6 +899,10 @@ int imask_step_image(imask_plan* pl, const imask_state* st, int level0,
     LAUNCH(launch_saga_image_full(st->bp, pl->side, pl->cp, sg, S(stream)), "saga_image_full");
   return IMASK_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 int imask_sketch_step(imask_plan* pl, const imask_state* st, int level0,
                       const imask_step_params* prm, void* stream) {

@@ -160,6 +160,20 @@ struct ImageSaga {
   float p_i;
   float s;        // sigma / mu
   float inv_den;  // 1 / (1 + s*mu_g)
+  float* xbar = nullptr;  // sketch_seq_step: xbar = x' + theta (x' - x) (nullptr: none)
+  float theta = 0.f;
 };
+
+// Primal extrapolation of sketch_seq_step (solvers.py:296-300) for one pixel /
+// four pixels, given the old and the new primal value.
+__device__ __forceinline__ void extrapolate(const ImageSaga& sg, size_t p, float xo, float xn) {
+  if (sg.xbar) sg.xbar[p] = fmaf(sg.theta, xn - xo, xn);
+}
+__device__ __forceinline__ void extrapolate4(const ImageSaga& sg, size_t p, float4 xo, float4 xn) {
+  if (sg.xbar)
+    *reinterpret_cast<float4*>(sg.xbar + p) =
+        make_float4(fmaf(sg.theta, xn.x - xo.x, xn.x), fmaf(sg.theta, xn.y - xo.y, xn.y),
+                    fmaf(sg.theta, xn.z - xo.z, xn.z), fmaf(sg.theta, xn.w - xo.w, xn.w));
+}
 
 }  // namespace imask

@@ -186,6 +186,7 @@ k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, Image
   float4 tab = *reinterpret_cast<const float4*>(sg.phi_tab + g);
   float4 sum = *reinterpret_cast<const float4*>(sg.phi_sum + g);
   float4 xv = *reinterpret_cast<const float4*>(sg.x + g);
+  const float4 xo = xv;
   __syncthreads();
   comp32_build(sm, cp.r);
   const float4 pn = comp32_quad(sm, cp, py, px);
@@ -196,6 +197,7 @@ k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, Image
   *reinterpret_cast<float4*>(sg.phi_tab + g) = tab;
   *reinterpret_cast<float4*>(sg.phi_sum + g) = sum;
   *reinterpret_cast<float4*>(sg.x + g) = xv;
+  extrapolate4(sg, g, xo, xv);
 }
 
 // Coarse level, fast path (side % 32 == 0, f <= 32): 32 x 32 full-resolution
@@ -210,6 +212,7 @@ k_saga_image_coarse32(const float* __restrict__ bp, int side, int f, float inv_f
   const int qrow = (row / f) * n;
   float4 sum = *reinterpret_cast<const float4*>(sg.phi_sum + g);
   float4 xv = *reinterpret_cast<const float4*>(sg.x + g);
+  const float4 xo = xv;
   float pn[4], po[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -224,6 +227,7 @@ k_saga_image_coarse32(const float* __restrict__ bp, int side, int f, float inv_f
   d = pn[3] - po[3]; { const float xi = d + sum.w; sum.w = fmaf(sg.p_i, d, sum.w); xv.w = fmaf(-sg.s, xi, xv.w) * sg.inv_den; }
   *reinterpret_cast<float4*>(sg.phi_sum + g) = sum;
   *reinterpret_cast<float4*>(sg.x + g) = xv;
+  extrapolate4(sg, g, xo, xv);
   __syncthreads();  // every old table value of this tile's blocks has been read
   const int tc = 32 / f;
   if ((int)threadIdx.x < tc * tc) {
@@ -324,7 +328,9 @@ k_saga_image_coarse(const float* __restrict__ bp, int side, int f, int ts, float
     const float ps = sg.phi_sum[p];
     const float xi = d + ps;
     sg.phi_sum[p] = fmaf(sg.p_i, d, ps);
-    sg.x[p] = fmaf(-sg.s, xi, sg.x[p]) * sg.inv_den;
+    const float xo = sg.x[p], xn = fmaf(-sg.s, xi, xo) * sg.inv_den;
+    sg.x[p] = xn;
+    extrapolate(sg, p, xo, xn);
   }
   __syncthreads();
   const int tc = ts / f;
@@ -355,7 +361,9 @@ k_saga_image_full(const float* __restrict__ bp, int side, CompParams cp, ImageSa
     const float xi = d + ps;
     sg.phi_sum[p] = fmaf(sg.p_i, d, ps);
     sg.phi_tab[p] = pn;
-    sg.x[p] = fmaf(-sg.s, xi, sg.x[p]) * sg.inv_den;
+    const float xo = sg.x[p], xn = fmaf(-sg.s, xi, xo) * sg.inv_den;
+    sg.x[p] = xn;
+    extrapolate(sg, p, xo, xn);
   }
 }
 

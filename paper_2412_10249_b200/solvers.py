@@ -19,8 +19,10 @@ since the reference's full-resolution rows are their replication
 (mrsketch.py:54-55); `SaddleState.phi_full(i)` returns the reference layout.
 `pdhg_solve` / `run(..., "pdhg")` (solvers.py:308-342, 433-446; SURVEY
 §8(f) rank 1) run on the device too, one native call per iteration when K
-is the B200 projector. sketch-seq and saga-saddle are the remaining §8(f)
-rows.
+is the B200 projector, and so do `sketch_seq_step` / `run(..., "sketch-seq")`
+(ImaSk-Seq, solvers.py:265-305) and `run(..., "saga-saddle")` with the
+blocks A_i = p_i K_i, which reproduces the parallel step (solvers.py:233-237;
+SURVEY §8(f) rank 2).
 """
 
 from __future__ import annotations
@@ -246,13 +248,15 @@ class SaddleState:
 
     def c_state(self, b: torch.Tensor) -> _lib.ImaskState:
         """The C view of this state for the current dual buffer."""
-        key = (self.y.data_ptr(), b.data_ptr())
+        key = (self.y.data_ptr(), b.data_ptr(),
+               None if self.xbar is None else self.xbar.data_ptr())
         cs = self._cstates.get(key)
         if cs is None:
             cs = _lib.ImaskState(
                 self.x.data_ptr(), self.y.data_ptr(), b.data_ptr(), self.phi_sum.data_ptr(),
                 self.psi_sum.data_ptr(), self.phi_tab.data_ptr(), self.psi_tab.data_ptr(),
                 self.bp.data_ptr(), None if self.y_alt is None else self.y_alt.data_ptr(),
+                None if self.xbar is None else self.xbar.data_ptr(),
             )
             self._cstates[key] = cs
         return cs
@@ -377,6 +381,29 @@ def sketch_step(state: SaddleState, prob: Problem, sigma: float, mu: float) -> S
     eng = _require_engine(prob)
     i = draw_level(state.seed, state.k, prob.cum_probs)
     _device_step(eng, state, i, _params(sigma, mu, eng.mu_g))
+    state.k += 1
+    state.cost += 2.0 * prob.fractions[i]
+    state.last_level = i + 1
+    if state.k % state.resum_every == 0:
+        _resum(state, prob)
+    return state
+
+
+def sketch_seq_step(state: SaddleState, prob: Problem, sigma: float, mu: float,
+                    theta_extrap: float) -> SaddleState:
+    """One sequential-update iteration with primal extrapolation, ImaSk-Seq
+    (solvers.py:265-305), on the device: the forward memory is refreshed from
+    xbar and the dual moves first, then the adjoint memory from the new dual,
+    the primal step and the extrapolation (one native call, imask_seq_step)."""
+    if not 0.0 <= theta_extrap <= 1.0:
+        raise ValueError("theta_extrap must lie in [0, 1]")
+    eng = _require_engine(prob)
+    if eng.shard.world > 1:
+        raise NotImplementedError("sketch_seq_step runs on one GPU")
+    i = draw_level(state.seed, state.k, prob.cum_probs)
+    _lib.check(_lib.lib().imask_seq_step(
+        eng.plan.handle, ctypes.byref(state.c_state(eng.b)), i,
+        ctypes.byref(_params(sigma, mu, eng.mu_g)), float(theta_extrap), eng.plan.stream))
     state.k += 1
     state.cost += 2.0 * prob.fractions[i]
     state.last_level = i + 1
@@ -588,10 +615,15 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
         raise ValueError(f"unknown algorithm {algorithm!r}; expected one of {ALGORITHMS}")
     if algorithm == "pdhg":
         return _run_pdhg(prob, mu, iters, record_every, seed, x_ref, snapshot_costs)
-    if algorithm != "sketch":
-        raise NotImplementedError(
-            f"{algorithm!r} is a SURVEY 8(f) 'next' row; the B200 path runs 'sketch' and 'pdhg'"
-        )
+    if algorithm == "sketch-seq" and not 0.0 <= theta_extrap <= 1.0:
+        raise ValueError("theta_extrap must lie in [0, 1]")
+    if algorithm == "saga-saddle":
+        # A_i = p_i K_i with sigma_x = sigma/mu, sigma_y = sigma reproduces the
+        # sketched parallel step (solvers.py:233-237); the blocks must sum to K
+        # (solvers.py:463-467, checked here in float32)
+        gap = verify_decomposition(prob)
+        if gap > 1e-5:
+            raise ValueError(f"operator blocks do not sum to the full map (gap {gap:.2e})")
     eng = _require_engine(prob)
     x_ref_t = None if x_ref is None else to_device(x_ref, eng.device)
     t0 = time.perf_counter()
@@ -606,9 +638,15 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
     record = rec.record
 
     record(0, 0.0, 0, state.x)
+    seq = algorithm == "sketch-seq"
     for k in range(1, iters + 1):
         i = int(schedule[k - 1])
-        _device_step(eng, state, i, prm)
+        if seq:
+            _lib.check(_lib.lib().imask_seq_step(
+                eng.plan.handle, ctypes.byref(state.c_state(eng.b)), i, ctypes.byref(prm),
+                float(theta_extrap), eng.plan.stream))
+        else:
+            _device_step(eng, state, i, prm)
         state.k += 1
         state.cost += 2.0 * prob.fractions[i]
         state.last_level = i + 1
@@ -621,6 +659,21 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
     rows = rec.rows()
     return SolveReport(rows=rows, x=state.x, y=state.y, algorithm=algorithm, seed=seed,
                        snapshots=snapshots)
+
+
+def verify_decomposition(prob: Problem, trials: int = 1, seed: int = 0) -> float:
+    """max relative gap of sum_i p_i K_i x against K x over random x
+    (the check run() makes for saga-saddle, solvers.py:463-467)."""
+    gen = np.random.default_rng(seed)
+    worst = 0.0
+    for _ in range(trials):
+        x = to_device(gen.standard_normal(prob.K.domain_dim))
+        full = prob.K.apply(x).double()
+        acc = torch.zeros_like(full)
+        for p_i, op in zip(prob.probs, prob.ops):
+            acc += float(p_i) * op.apply(x).double()
+        worst = max(worst, float(torch.linalg.norm(acc - full) / torch.linalg.norm(full)))
+    return worst
 
 
 def _run_pdhg(prob: Problem, mu: float, iters: int, record_every: int, seed: int, x_ref,

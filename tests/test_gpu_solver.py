@@ -317,8 +317,10 @@ def test_rejects_unsupported_problems():
     st = solvers.init_state(prob)
     with pytest.raises(ValueError, match="sigma and mu_g must be positive"):
         solvers.sketch_step(st, prob, 0.0, 1.0)
-    with pytest.raises(NotImplementedError):
-        solvers.run(prob, "sketch-seq", 1e-3, 1.0, 3)
+    with pytest.raises(ValueError, match="unknown algorithm"):
+        solvers.run(prob, "sketch-par", 1e-3, 1.0, 3)
+    with pytest.raises(ValueError, match="theta_extrap"):
+        solvers.run(prob, "sketch-seq", 1e-3, 1.0, 3, theta_extrap=-0.1)
 
 
 def test_pdhg_matches_oracle():
@@ -371,3 +373,47 @@ def test_run_pdhg_rows_and_ledger():
     assert np.array_equal(host(rep.x), host(x))
     rel = float(np.dot(host(x) - x_true, host(x) - x_true) / np.dot(x_true, x_true))
     assert abs(rep.rows[-1][3] - rel) <= 1e-6 * rel
+
+
+@pytest.mark.parametrize("theta", [0.0, 0.7])
+def test_sketch_seq_step_matches_oracle(theta):
+    """ImaSk-Seq (solvers.py:265-305) on the device against its float64
+    restatement: same level sequence, iterates and tables."""
+    side, na, nd, probs = 64, 90, 91, [0.3, 0.3, 0.2, 0.2]
+    orc = so.SketchedCT(side, na, nd, probs)
+    b = orc.proj[1].apply(np.random.default_rng(15).random(side * side))
+    prob = build(side, na, nd, probs, b)
+    st = solvers.init_state(prob, seed=6)
+    ost = so.init_state(orc, seed=6)
+    for _ in range(10):
+        solvers.sketch_seq_step(st, prob, 2e-4, 1e-2, theta)
+        so.sketch_seq_step(ost, orc, b, 2e-4, 1e-2, 1e-2, theta)
+        assert st.last_level == ost.last_level
+    assert rel_l2(host(st.x), ost.x) <= 1e-4
+    assert rel_l2(host(st.y), ost.y) <= 1e-4
+    assert rel_l2(host(st.xbar), ost.xbar) <= 1e-4
+    assert rel_l2(host(st.psi_sum), ost.psi_sum) <= 1e-4
+    assert st.cost == ost.cost
+    with pytest.raises(ValueError, match="theta_extrap"):
+        solvers.sketch_seq_step(st, prob, 2e-4, 1e-2, 1.5)
+
+
+def test_run_sketch_seq_and_saga_saddle():
+    """run() for the sequential variant follows sketch_seq_step; saga-saddle with
+    A_i = p_i K_i is the parallel sketched step (solvers.py:233-237)."""
+    side, na, nd, probs = 32, 36, 47, [0.25] * 4
+    orc = so.SketchedCT(side, na, nd, probs)
+    b = orc.proj[1].apply(np.random.default_rng(16).random(side * side))
+    prob = build(side, na, nd, probs, b)
+    rep = solvers.run(prob, "sketch-seq", 1e-3, 1e-2, 12, record_every=4, seed=3,
+                      theta_extrap=0.5)
+    st = solvers.init_state(prob, seed=3)
+    for _ in range(12):
+        solvers.sketch_seq_step(st, prob, 1e-3, 1e-2, 0.5)
+    assert np.array_equal(host(rep.x), host(st.x))
+    assert [r[0] for r in rep.rows] == [0, 4, 8, 12]
+    assert rep.rows[-1][1] == st.cost and rep.rows[-1][2] == st.last_level
+    assert solvers.verify_decomposition(prob) <= 1e-5
+    rep_s = solvers.run(prob, "saga-saddle", 1e-3, 1e-2, 12, record_every=4, seed=3)
+    rep_p = solvers.run(prob, "sketch", 1e-3, 1e-2, 12, record_every=4, seed=3)
+    assert np.array_equal(host(rep_s.x), host(rep_p.x))
