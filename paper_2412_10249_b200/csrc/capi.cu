@@ -46,6 +46,8 @@ cudaError_t launch_pdhg_image(const float* bp, float* x, float* xbar, size_t d, 
 cudaError_t launch_resum(const float* phi_tab, float* phi_sum, int side, const float* psi_tab,
                          float* psi_sum, size_t m, const ResumParams& rp, cudaStream_t s);
 void init_kernel_attributes();
+int forward_tma_entries_per_cta();
+int forward_tma_window();
 struct TmaMaps {
   CUtensorMap row, row_m, col, col_m;
 };
@@ -107,7 +109,7 @@ bool encode_pair_map(CUtensorMap* map, void* base, int n, unsigned box_h) {
   if (!fn || !base) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)pair_pitch(n), (cuuint64_t)n};
   const cuuint64_t strides[1] = {(cuuint64_t)pair_pitch(n) * sizeof(float2)};
-  const cuuint32_t box[2] = {96, box_h};
+  const cuuint32_t box[2] = {(cuuint32_t)forward_tma_window(), box_h};
   const cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, base, dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -523,8 +525,9 @@ int imask_plan_create_list(int side, int n_angles, int n_det, int n_loc, const i
     std::vector<int2> tent;
     for (auto* lst : {&rowf, &colf}) {
       for (const int2& e2 : *lst) tent.push_back(e2);
-      while (tent.size() % 8) tent.push_back(make_int2(-1, -1));
-      if (lst == &rowf) pl->tma_row_ctas = (int)tent.size() / 8;
+      const size_t fe = (size_t)forward_tma_entries_per_cta();
+      while (tent.size() % fe) tent.push_back(make_int2(-1, -1));
+      if (lst == &rowf) pl->tma_row_ctas = (int)(tent.size() / fe);
     }
     // quad mode when every row's transpose partner n/2 - a (pi/2 - theta) is local
     // too: the singles 0 and n/2 (a transposed-family entry), entries
@@ -567,8 +570,9 @@ int imask_plan_create_list(int side, int n_angles, int n_det, int n_loc, const i
     if (!qent.empty()) {
       pl->tma_quad = true;
       tent4 = qent;
-      while (tent4.size() % 8) tent4.push_back(make_int4(-1, -1, -1, -1));
-      pl->tma_row_ctas = (int)tent4.size() / 8;
+      const size_t fe = (size_t)forward_tma_entries_per_cta();
+      while (tent4.size() % fe) tent4.push_back(make_int4(-1, -1, -1, -1));
+      pl->tma_row_ctas = (int)(tent4.size() / fe);
     } else {
       for (const int2& e2 : tent) tent4.push_back(make_int4(e2.x, e2.y, -1, -1));
     }

@@ -228,7 +228,16 @@ k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
 // rounded down to an even pair index: a tensor copy must start 16-byte aligned.
 constexpr int kFB = 16;           // bands per chunk (pair mode)
 constexpr int kFBQuad = 8;        // bands per chunk (quad mode: twice the images)
-constexpr int kFWc = 96;          // window width in pair columns (x 8 B = 768 B per row)
+#ifndef IMASK_FWD_ENTRIES
+#define IMASK_FWD_ENTRIES 8
+#endif
+#ifndef IMASK_FWD_WINDOW
+#define IMASK_FWD_WINDOW 96
+#endif
+constexpr int kFE = IMASK_FWD_ENTRIES;  // entries per CTA (4 per warp row, kFE / 4 warp rows)
+constexpr int kFThreads = kFE * 32;     // 8 detectors x 4 entries per warp, 32 detectors per CTA
+constexpr int kFWc = IMASK_FWD_WINDOW;  // window width in pair columns: the TMA box; the
+                                        // window write costs kFWc / (32 kFE) of the reads
 constexpr int kFMaxChunks = 1024;  // side up to 8192
 
 struct TmaMaps {
@@ -280,7 +289,7 @@ struct FwdWarpInfo {
 // address is computed once for four rays. Pair mode (kQuad = false): entries
 // (a, n-a), one ray family per CTA.
 template <bool kSaga, bool kQuad>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kFThreads)
 k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P,
               const float2* __restrict__ PT, const float2* __restrict__ PM,
               const float2* __restrict__ PTM, int n, int pitch, const FwdAngle* __restrict__ ang,
@@ -294,7 +303,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * NI * kBox * sizeof(float2));
   uint64_t* empty = full + 2;
   FwdWarpInfo* info = reinterpret_cast<FwdWarpInfo*>(empty + 2);
-  int* cmin_tab = reinterpret_cast<int*>(info + 8);
+  int* cmin_tab = reinterpret_cast<int*>(info + kFE);
   int* ctl = cmin_tab + kFMaxChunks;  // [0] overflow, [1] first band, [2] chunks, then cmax_tab
 
   // A warp holds 4 entries x 8 consecutive detectors (lane = 8 q + d): each
@@ -303,7 +312,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   // where 32 detectors of one angle (up to 45 columns) cost up to 4.
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q4 = lane >> 3;
-  const int e = blockIdx.y * 8 + (warp >> 2) * 4 + q4;
+  const int e = blockIdx.y * kFE + (warp >> 2) * 4 + q4;
   const int4 ent = e < n_entries ? entries[e] : make_int4(-1, -1, -1, -1);
   const int rows[4] = {ent.x, ent.y, ent.z, ent.w};
   const int tab = ent.x >= 0 ? ent.x : ent.z;  // the entry's parameter row
@@ -338,7 +347,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   // union of the lockstep band ranges of the four warps holding it (every lane
   // walks its warp's whole range)
   int* cmax_tab = ctl + 4;  // [kFMaxChunks]
-  if (threadIdx.x < 8) {
+  if (threadIdx.x < kFE) {
     info[threadIdx.x] = FwdWarpInfo{0, 0, 0, n, 0};
     ctl[0] = 0;
   }
@@ -358,7 +367,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   __syncthreads();
   if (threadIdx.x == 0) {
     int blo = n, bhi = 0;
-    for (int w = 0; w < 8; ++w) {
+    for (int w = 0; w < kFE; ++w) {
       blo = min(blo, info[w].lo);
       bhi = max(bhi, info[w].hi);
     }
@@ -376,9 +385,9 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
       cmax_tab[t] = INT_MIN;
     }
     __syncthreads();
-    for (int it = threadIdx.x; it < nch * 8; it += blockDim.x) {
-      const int t = it >> 3;
-      const FwdWarpInfo& I = info[it & 7];
+    for (int it = threadIdx.x; it < nch * kFE; it += blockDim.x) {
+      const int t = it / kFE;
+      const FwdWarpInfo& I = info[it % kFE];
       const int b0 = blo + t * FB;
       const int bs = max(b0, I.lo), be = min(b0 + FB, I.hi) - 1;
       if (bs > be) continue;
@@ -433,8 +442,8 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
     if (threadIdx.x == 0) {
       mbar_init(&full[0], 1);
       mbar_init(&full[1], 1);
-      mbar_init(&empty[0], 8);
-      mbar_init(&empty[1], 8);
+      mbar_init(&empty[0], kFThreads / 32);
+      mbar_init(&empty[1], kFThreads / 32);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -532,8 +541,8 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
 }
 
 size_t forward_tma_smem() {
-  // both modes stage 2 x 2 x 16 or 2 x 4 x 8 bands of kFWc pairs (48 KB)
-  return 2 * 2 * kFB * kFWc * sizeof(float2) + 4 * sizeof(uint64_t) + 8 * sizeof(FwdWarpInfo) +
+  // both modes stage 2 x 2 x 16 or 2 x 4 x 8 bands of kFWc pairs
+  return 2 * 2 * kFB * kFWc * sizeof(float2) + 4 * sizeof(uint64_t) + kFE * sizeof(FwdWarpInfo) +
          (2 * kFMaxChunks + 4) * sizeof(int);
 }
 
@@ -541,13 +550,13 @@ cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float
                                const float2* PM, const float2* PTM, int n, const FwdAngle* ang,
                                const int4* entries, int n_entries, int row_ctas, bool quad,
                                int n_det, float* sino, const SinoSaga* saga, cudaStream_t stream) {
-  dim3 grid((n_det + 31) / 32, (n_entries + 7) / 8);
+  dim3 grid((n_det + 31) / 32, (n_entries + kFE - 1) / kFE);
   const size_t smem = forward_tma_smem();
   SinoSaga none{};
   const SinoSaga sg = saga ? *saga : none;
   float* out = saga ? nullptr : sino;
 #define FWD_TMA(S_, Q_)                                                                     \
-  k_forward_tma<S_, Q_><<<grid, 256, smem, stream>>>(maps, P, PT, PM, PTM, n, pair_pitch(n), \
+  k_forward_tma<S_, Q_><<<grid, kFThreads, smem, stream>>>(maps, P, PT, PM, PTM, n, pair_pitch(n), \
                                                      ang, entries, n_entries, row_ctas, n_det, \
                                                      out, sg)
   if (saga) {
@@ -1057,4 +1066,9 @@ cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n,
   return cudaGetLastError();
 }
 
+}  // namespace imask
+
+namespace imask {
+int forward_tma_entries_per_cta() { return kFE; }
+int forward_tma_window() { return kFWc; }
 }  // namespace imask
