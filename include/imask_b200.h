@@ -255,6 +255,18 @@ IMASK_API int imask_last_launch_count(void);
 IMASK_API int imask_sq_dist(const float* x, const float* ref, int64_t n, double* out,
                             double* result, void* stream);
 
+/* TV + nonnegativity prox (prox_tv_nonneg, proxlib.py:102-148):
+ * out = argmin_u 0.5||u - xp||^2 + sigma mu_g ||grad u||_{1,2} + [u >= 0]
+ * by the fast gradient projection on the dual gradient field (step 1/8,
+ * at most inner_iters iterations, stopping when the relative dual progress
+ * drops below inner_tol), for a side x side image; out may alias xp.
+ * `scratch` is device memory of imask_prox_tv_scratch_bytes(side) bytes. One
+ * launch per inner iteration, no host synchronisation. */
+IMASK_API int64_t imask_prox_tv_scratch_bytes(int side);
+IMASK_API int imask_prox_tv_nonneg(int side, const float* xp, float* out, double sigma,
+                                   double mu_g, int inner_iters, double inner_tol, void* scratch,
+                                   void* stream);
+
 /* Measurement helper (no reference counterpart): thread-level FP32 FFMA
  * throughput of `device` from an FFMA-chain microbenchmark, the FP32-issue
  * denominator of bench.py's roofline. */

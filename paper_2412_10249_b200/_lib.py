@@ -60,6 +60,12 @@ SIGNATURES = {
     "imask_version": (ctypes.c_char_p, []),
     "imask_last_error": (ctypes.c_char_p, []),
     "imask_last_launch_count": (ctypes.c_int, []),
+    "imask_prox_tv_scratch_bytes": (ctypes.c_int64, [ctypes.c_int]),
+    "imask_prox_tv_nonneg": (
+        ctypes.c_int,
+        [ctypes.c_int, _vp, _vp, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+         ctypes.c_double, _vp, _vp],
+    ),
     "imask_probe_ffma_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "imask_probe_smem_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "imask_sq_dist": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _vp]),

@@ -66,6 +66,11 @@ def g_solver_A():
     return golden("solver_A.npz")
 
 
+@pytest.fixture(scope="session")
+def g_tv():
+    return golden("tv.npz")
+
+
 def rel_l2(a, b):
     a = np.asarray(a, dtype=float).ravel()
     b = np.asarray(b, dtype=float).ravel()

@@ -20,6 +20,8 @@ Fixtures:
                {0, 1, 359, 360, 719, 720, 721, 1439} at f = 1 and 32 via
                ray_matrix (Kx rows, and K^T y at 4096 sampled pixels)
   sketch.npz   decimate / upsample / SketchFamily.apply_sketch (mrsketch.py)
+  tv.npz       prox_tv_nonneg (proxlib.py:102-148) on seeded images: 50
+               inner iterations (the default) and a 4x4 step image at 4000
   solver_A.npz sketch_step trajectory on config A (coarse mode, ridge
                mu_g = 1e-2, sigma = 3e-5, mu = mu_g): x, y, sums after
                18 iterations (= 20 epochs) and after 200 iterations
@@ -165,7 +167,29 @@ def gen_solver_A():
     save("solver_A.npz", **out)
 
 
+def gen_tv():
+    out = {}
+    rng = np.random.default_rng(21)
+    for side, sigma, mu_g in ((16, 0.8, 0.5), (40, 0.3, 1.0), (64, 1.0, 0.25)):
+        xp = rng.standard_normal(side * side) * 0.5 + 0.3
+        out[f"xp_{side}"] = xp
+        out[f"out_{side}"] = proxlib.prox_tv_nonneg(xp, sigma, mu_g)
+        out[f"par_{side}"] = np.array([sigma, mu_g])
+    img = np.zeros((4, 4))
+    img[:, 2:] = 1.0
+    img[1, 1] = -0.3
+    out["xp_step"] = img.ravel()
+    out["out_step"] = proxlib.prox_tv_nonneg(img.ravel(), 0.8, 0.5, inner_iters=4000,
+                                             inner_tol=1e-13)
+    save("tv.npz", **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # e.g. `make_golden.py tv`: one fixture
+        for name in sys.argv[1:]:
+            globals()[f"gen_{name}"]()
+        sys.exit(0)
+    gen_tv()
     gen_rng()
     gen_proj_small()
     gen_sketch()

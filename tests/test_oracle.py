@@ -126,3 +126,16 @@ def test_against_live_reference_odd_and_even_detectors():
         ref = ctmodel.ray_matrix(side // f, float(f), g.angles, g.offsets)
         mine = ct_oracle.ProjectorOracle(side, na, g.n_detectors, f).to_csr()
         assert abs(mine - ref).max() <= 1e-12
+
+
+def test_tv_oracle_pinned_to_reference(g_tv):
+    """oracle/prox_oracle.py reproduces the reference's prox_tv_nonneg
+    (proxlib.py:102-148) on the golden inputs."""
+    from oracle import prox_oracle as po
+
+    for side in (16, 40, 64):
+        sigma, mu_g = g_tv[f"par_{side}"]
+        out = po.prox_tv_nonneg(g_tv[f"xp_{side}"], sigma, mu_g)
+        assert np.max(np.abs(out - g_tv[f"out_{side}"])) <= 1e-12
+    out = po.prox_tv_nonneg(g_tv["xp_step"], 0.8, 0.5, inner_iters=4000, inner_tol=1e-13)
+    assert np.max(np.abs(out - g_tv["out_step"])) <= 1e-12
