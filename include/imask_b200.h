@@ -76,6 +76,16 @@ typedef struct imask_step_params {
   double sigma; /* dual step sigma; primal step is sigma/mu */
   double mu;    /* solver strong-convexity parameter mu      */
   double mu_g;  /* ridge weight of g(x) = mu_g/2 ||x||^2      */
+  /* g_kind 1: g = TV + nonnegativity (tv_nonneg_fn, proxlib.py:151-166) with
+   * weight tv_mu instead of the ridge: the primal step is then
+   * x' = prox_tv_nonneg(x - s xi, s) (imask_prox_tv_nonneg, tv_iters inner
+   * iterations, tolerance tv_tol, device scratch tv_scratch of
+   * imask_prox_tv_scratch_bytes(side) bytes); mu_g is ignored. 0: ridge. */
+  int g_kind;
+  int tv_iters;
+  double tv_tol;
+  double tv_mu;
+  void* tv_scratch;
 } imask_step_params;
 
 /* Library version string. */

@@ -144,9 +144,11 @@ def resum(st: State, probs) -> None:
     st.psi_sum = psi_sum
 
 
-def sketch_step(st: State, ops: SketchedCT, b: np.ndarray, sigma: float, mu: float, mu_g: float) -> State:
-    """One parallel ImaSk iteration (solvers.py:194-221), ridge g, quadratic f*."""
-    if sigma <= 0 or mu_g <= 0:
+def sketch_step(st: State, ops: SketchedCT, b: np.ndarray, sigma: float, mu: float, mu_g: float,
+                gprox=None) -> State:
+    """One parallel ImaSk iteration (solvers.py:194-221), ridge g (or the prox
+    callable gprox(p, s) of another g), quadratic f*."""
+    if sigma <= 0 or (gprox is None and mu_g <= 0):
         raise ValueError("sigma and mu_g must be positive")
     cum = np.cumsum(ops.probs)
     i = draw_level(st.seed, st.k, cum)
@@ -160,7 +162,10 @@ def sketch_step(st: State, ops: SketchedCT, b: np.ndarray, sigma: float, mu: flo
     st.phi[i] = phi_new
     st.psi[i] = psi_new
     s = sigma / mu
-    st.x = (st.x - s * xi) / (1.0 + s * mu_g)  # proxlib.py:51-55
+    if gprox is not None:
+        st.x = gprox(st.x - s * xi, s)
+    else:
+        st.x = (st.x - s * xi) / (1.0 + s * mu_g)  # proxlib.py:51-55
     st.y = ((st.y + sigma * zeta) - sigma * b) / (1.0 + sigma)  # proxlib.py:30-34
     st.k += 1
     st.cost += 2.0 * ops.fraction(i)

@@ -52,7 +52,9 @@ class ImaskPdhgParams(ctypes.Structure):
 
 
 class ImaskStepParams(ctypes.Structure):
-    _fields_ = [("sigma", ctypes.c_double), ("mu", ctypes.c_double), ("mu_g", ctypes.c_double)]
+    _fields_ = [("sigma", ctypes.c_double), ("mu", ctypes.c_double), ("mu_g", ctypes.c_double),
+                ("g_kind", ctypes.c_int), ("tv_iters", ctypes.c_int), ("tv_tol", ctypes.c_double),
+                ("tv_mu", ctypes.c_double), ("tv_scratch", ctypes.c_void_p)]
 
 
 # name -> (restype, argtypes)

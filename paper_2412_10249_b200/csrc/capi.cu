@@ -337,6 +337,17 @@ int check_factor(const imask_plan* pl, int f) {
   return IMASK_OK;
 }
 
+int check_params(const imask_step_params* prm) {
+  if (!prm) return fail(IMASK_EINVAL, "null step parameters");
+  if (!(prm->sigma > 0.0) || !(prm->g_kind == 1 || prm->mu_g > 0.0))
+    return fail(IMASK_EINVAL, "sigma and mu_g must be positive");
+  if (!(prm->mu > 0.0)) return fail(IMASK_EINVAL, "mu must be positive");
+  if (prm->g_kind == 1 && (!(prm->tv_mu > 0.0) || prm->tv_iters < 0 || !prm->tv_scratch))
+    return fail(IMASK_EINVAL, "TV step needs tv_mu > 0, tv_iters >= 0 and tv_scratch");
+  if (prm->g_kind != 0 && prm->g_kind != 1) return fail(IMASK_EINVAL, "unknown g_kind");
+  return IMASK_OK;
+}
+
 int check_level0(const imask_plan* pl, int level0) {
   if (level0 < 0 || level0 >= pl->r)
     return fail(IMASK_ELEVEL, "level " + std::to_string(level0 + 1) + " out of range 1.." +
@@ -847,9 +858,7 @@ int imask_seq_step(imask_plan* pl, const imask_state* st, int level0,
   g_launches = 0;
   int rc = check_level0(pl, level0);
   if (rc) return rc;
-  if (!(prm->sigma > 0.0) || !(prm->mu_g > 0.0))
-    return fail(IMASK_EINVAL, "sigma and mu_g must be positive");
-  if (!(prm->mu > 0.0)) return fail(IMASK_EINVAL, "mu must be positive");
+  if ((rc = check_params(prm))) return rc;
   if (!(theta >= 0.0 && theta <= 1.0)) return fail(IMASK_EINVAL, "theta_extrap must lie in [0, 1]");
   if (!st->xbar) return fail(IMASK_EINVAL, "sketch_seq_step needs st->xbar");
   DeviceGuard g(pl->device);
@@ -882,9 +891,7 @@ int step_image(imask_plan* pl, const imask_state* st, int level0, const imask_st
   g_launches = 0;
   int rc = check_level0(pl, level0);
   if (rc) return rc;
-  if (!(prm->sigma > 0.0) || !(prm->mu_g > 0.0))
-    return fail(IMASK_EINVAL, "sigma and mu_g must be positive");
-  if (!(prm->mu > 0.0)) return fail(IMASK_EINVAL, "mu must be positive");
+  if ((rc = check_params(prm))) return rc;
   DeviceGuard g(pl->device);
   const int f = pl->factors[level0];
   ImageSaga sg;
@@ -895,12 +902,21 @@ int step_image(imask_plan* pl, const imask_state* st, int level0, const imask_st
   sg.x = st->x;
   sg.p_i = (float)pl->probs[level0];
   const double s = prm->sigma / prm->mu;
+  const bool tv = prm->g_kind == 1;
   sg.s = (float)s;
-  sg.inv_den = (float)(1.0 / (1.0 + s * prm->mu_g));
+  sg.inv_den = tv ? 1.0f : (float)(1.0 / (1.0 + s * prm->mu_g));  // TV: x - s xi, prox below
+  if (tv && xbar) return fail(IMASK_EINVAL, "the sequential variant takes the ridge g only");
   if (level0 < pl->r - 1)
     LAUNCH(launch_saga_image_coarse(st->bp, pl->side, f, sg, S(stream)), "saga_image");
   else
     LAUNCH(launch_saga_image_full(st->bp, pl->side, pl->cp, sg, S(stream)), "saga_image_full");
+  if (tv) {
+    // x' = prox_{s g}(x - s xi) in place: memset + tv_iters iterations + recovery
+    const int trc = imask_prox_tv_nonneg(pl->side, st->x, st->x, s, prm->tv_mu, prm->tv_iters,
+                                         prm->tv_tol, prm->tv_scratch, stream);
+    if (trc) return fail(trc, std::string("prox_tv_nonneg: ") + cudaGetErrorString(cudaGetLastError()));
+    g_launches += prm->tv_iters + 1;  // iteration kernels + the recovery (plus one memset)
+  }
   return IMASK_OK;
 }
 
@@ -914,9 +930,7 @@ int imask_sketch_step(imask_plan* pl, const imask_state* st, int level0,
   g_launches = 0;
   int rc = check_level0(pl, level0);
   if (rc) return rc;
-  if (!(prm->sigma > 0.0) || !(prm->mu_g > 0.0))
-    return fail(IMASK_EINVAL, "sigma and mu_g must be positive");
-  if (!(prm->mu > 0.0)) return fail(IMASK_EINVAL, "mu must be positive");
+  if ((rc = check_params(prm))) return rc;
   DeviceGuard g(pl->device);
   const int f = pl->factors[level0];
   const int n = pl->side / f;

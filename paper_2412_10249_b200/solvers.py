@@ -107,7 +107,7 @@ class Engine:
         A graph is only launched after its pointers were checked against the
         state's, so it never holds the state alive.
         """
-        key = (level0, prm.sigma, prm.mu, prm.mu_g, state.parity)
+        key = (level0, prm.sigma, prm.mu, prm.mu_g, prm.g_kind, state.parity)
         cst = state.c_state(self.b)
         ptrs = tuple(getattr(cst, name) for name, _ in cst._fields_)
         hit = self._graphs.get(key)
@@ -129,6 +129,26 @@ class Engine:
         """Destroy the cached step graphs (``state`` is accepted for compatibility)."""
         for key in list(self._graphs):
             _lib.lib().imask_graph_destroy(self._graphs.pop(key)[0])
+
+    def set_tv(self, mu: float, inner_iters: int, inner_tol: float) -> None:
+        """g = TV + nonnegativity (tv_nonneg_fn): the primal step's prox runs inside
+        the native step (and its graph) with plan-lifetime scratch."""
+        self.tv = (float(mu), int(inner_iters), float(inner_tol))
+        self.tv_scratch = torch.empty(
+            int(_lib.lib().imask_prox_tv_scratch_bytes(self.geom.side)), dtype=torch.uint8,
+            device=self.device)
+
+    def params(self, sigma: float, mu: float) -> _lib.ImaskStepParams:
+        """Step scalars for this engine's g (ridge or TV + nonnegativity)."""
+        tv = getattr(self, "tv", None)
+        if tv is None:
+            return _params(sigma, mu, self.mu_g)
+        if sigma <= 0:
+            raise ValueError("sigma and mu_g must be positive")
+        if mu <= 0:
+            raise ValueError("mu must be positive")
+        return _lib.ImaskStepParams(float(sigma), float(mu), 0.0, 1, tv[1], tv[2], tv[0],
+                                    self.tv_scratch.data_ptr())
 
     def side_stream(self) -> torch.cuda.Stream:
         """Stream of the forward chain in angle-sharded steps (created on first use)."""
@@ -191,14 +211,18 @@ class Problem:
         proj = metas[0].projector
         if proj is None or any(m.projector != proj or m.family != self.family for m in metas):
             return None
-        if self.g.kind != "ridge" or self.f_conj.kind != "quadratic_conjugate":
+        if self.g.kind not in ("ridge", "tv_nonneg") or self.f_conj.kind != "quadratic_conjugate":
             return None
         angles = proj.angle_list
         if self.shard.world > 1 and angles != shard_angles(
                 proj.geom.n_angles, self.shard.rank, self.shard.world):
             raise ValueError("projector angle set does not match this rank's shard")
-        return Engine(proj.geom, self.family, proj.scale, self.g.param, self.f_conj.param,
-                      self.shard, angles)
+        eng = Engine(proj.geom, self.family, proj.scale,
+                     self.g.param if self.g.kind == "ridge" else 0.0, self.f_conj.param,
+                     self.shard, angles)
+        if self.g.kind == "tv_nonneg":
+            eng.set_tv(*self.g.param)
+        return eng
 
 
 def make_problem(K: LinOp, b, family: SketchFamily, g: ProxFn, f_conj: ProxFn,
@@ -380,7 +404,7 @@ def sketch_step(state: SaddleState, prob: Problem, sigma: float, mu: float) -> S
     """One parallel-update sketched iteration (solvers.py:194-221), on the device."""
     eng = _require_engine(prob)
     i = draw_level(state.seed, state.k, prob.cum_probs)
-    _device_step(eng, state, i, _params(sigma, mu, eng.mu_g))
+    _device_step(eng, state, i, eng.params(sigma, mu))
     state.k += 1
     state.cost += 2.0 * prob.fractions[i]
     state.last_level = i + 1
@@ -403,7 +427,7 @@ def sketch_seq_step(state: SaddleState, prob: Problem, sigma: float, mu: float,
     i = draw_level(state.seed, state.k, prob.cum_probs)
     _lib.check(_lib.lib().imask_seq_step(
         eng.plan.handle, ctypes.byref(state.c_state(eng.b)), i,
-        ctypes.byref(_params(sigma, mu, eng.mu_g)), float(theta_extrap), eng.plan.stream))
+        ctypes.byref(eng.params(sigma, mu)), float(theta_extrap), eng.plan.stream))
     state.k += 1
     state.cost += 2.0 * prob.fractions[i]
     state.last_level = i + 1
@@ -630,7 +654,7 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
     snapshots: dict = {}
     budgets = sorted(float(cb) for cb in snapshot_costs)
     state = init_state(prob, seed=seed, resum_every=resum_every)
-    prm = _params(sigma, mu, eng.mu_g)
+    prm = eng.params(sigma, mu)
     schedule = draw_levels(seed, 0, iters, prob.cum_probs)
 
     n_rows = 2 + iters // max(record_every, 1)
