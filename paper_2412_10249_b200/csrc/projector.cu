@@ -630,17 +630,19 @@ template <> struct AdjWin<true, true> { using T = float4; };
 // a warp cover a compact 8 x 4 pixel block at every k, so one window read
 // touches few distinct bins (ideally ~8|cos| + 4|sin| + 1 slots, many lanes
 // broadcast) instead of a 32-pixel row's ~32:
-//   T = 32 (lanes 128): fixed column 8*warp + p%8, rows p%32/8 + 4k
-//   T = 16 (lanes 32) : columns p%8 + 8*(k&1), rows p/8 + 4*(k>>1)
+//   T = 32 (lanes 128): fixed column 8*warp + 4*half + p%4, rows (p/4)%4 + 4k
+//   T = 16 (lanes 32) : columns 4*half + p%4 + 8*(k&1), rows (p/4)%4 + 4*(k>>1)
 //   T = 8  (lanes 32) : column p%8, rows p/8 + 4k
 template <int T>
 __device__ __forceinline__ void adj_pixel(int p, int k, int& dx, int& dy) {
+  // (each half-warp is a 4 x 4 sub-block, whose window reads stay within one
+  // bank period at factors 2 and 4)
   if constexpr (T == 32) {
-    dx = ((p >> 5) << 3) + (p & 7);
-    dy = ((p & 31) >> 3) + 4 * k;
+    dx = ((p >> 5) << 3) + (((p >> 4) & 1) << 2) + (p & 3);
+    dy = ((p >> 2) & 3) + 4 * k;
   } else if constexpr (T == 16) {
-    dx = (p & 7) + 8 * (k & 1);
-    dy = (p >> 3) + 4 * (k >> 1);
+    dx = (((p >> 4) & 1) << 2) + (p & 3) + 8 * (k & 1);
+    dy = ((p >> 2) & 3) + 4 * (k >> 1);
   } else {
     dx = p & 7;
     dy = (p >> 3) + 4 * k;
@@ -775,7 +777,7 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
           u[k] = s.c0 - onep32(e.lo);
           fix_add(e, (T == 16 && (k & 1)) ? estep2 : estep);
         }
-        for (int b = 0; b < s.nb; ++b) {
+        auto bin = [&](int b) {
 #pragma unroll
           for (int k = 0; k < kPPT; ++k) {
             const float w = __saturatef(fmaf(fabsf(u[k]), s.kneg, s.Rk));
@@ -788,6 +790,14 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
             }
             u[k] += 1.0f;
           }
+        };
+        if (s.nb == 3) {
+          // factor 2 (every oblique angle has 3 candidate bins): fully unrolled,
+          // the bin offsets become immediate offsets of the window reads
+#pragma unroll
+          for (int b = 0; b < 3; ++b) bin(b);
+        } else {
+          for (int b = 0; b < s.nb; ++b) bin(b);
         }
       }
     }
