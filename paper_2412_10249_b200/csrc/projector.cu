@@ -632,7 +632,7 @@ template <> struct AdjWin<true, true> { using T = float4; };
 // broadcast) instead of a 32-pixel row's ~32:
 //   T = 32 (lanes 128): fixed column 8*warp + 4*half + p%4, rows (p/4)%4 + 4k
 //   T = 16 (lanes 32) : columns 4*half + p%4 + 8*(k&1), rows (p/4)%4 + 4*(k>>1)
-//   T = 8  (lanes 32) : column p%8, rows p/8 + 4k
+//   T = 8  (lanes 32) : column 4*half + p%4, rows (p/4)%4 + 4k
 template <int T>
 __device__ __forceinline__ void adj_pixel(int p, int k, int& dx, int& dy) {
   // (each half-warp is a 4 x 4 sub-block, whose window reads stay within one
@@ -644,8 +644,8 @@ __device__ __forceinline__ void adj_pixel(int p, int k, int& dx, int& dy) {
     dx = (((p >> 4) & 1) << 2) + (p & 3) + 8 * (k & 1);
     dy = ((p >> 2) & 3) + 4 * (k >> 1);
   } else {
-    dx = p & 7;
-    dy = (p >> 3) + 4 * k;
+    dx = (((p >> 4) & 1) << 2) + (p & 3);
+    dy = ((p >> 2) & 3) + 4 * k;
   }
 }
 
