@@ -18,6 +18,28 @@
 
 namespace imask {
 
+// Programmatic dependent launch: a kernel launched with launch_pdl may start
+// (and run its independent prologue) while its stream predecessor drains; it
+// must call griddep_wait() before reading anything the predecessor writes.
+// In a kernel launched normally griddep_wait() returns at once.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 constexpr double kFix = 4294967296.0;  // 2^32
 
 // Zero columns on each side of every pair-image row (see k_forward): a lane

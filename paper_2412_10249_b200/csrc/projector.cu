@@ -168,6 +168,7 @@ k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
   Fix32 Y = fix_from(X0 + (long long)wlo * dYl + ((long long)(1 + kPadC) << 32));
   const Fix32 dY = fix_from(dYl);
   const float S = A.S, B = A.B;
+  griddep_wait();  // the pair images come from the stream predecessor (k_prepare)
   // img holds value pairs (u, um), imgm difference pairs (d, dm) (k_prepare):
   // (acc, accm) += (u, um) + g * (d, dm) with packed FP32 ops
   float2 acc2 = make_float2(0.f, 0.f);
@@ -407,6 +408,9 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
     }
   }
   __syncthreads();
+  // everything above reads only tables and the solver state; the pair images
+  // come from the stream predecessor (k_prepare)
+  griddep_wait();
   // pair mode: one ray family per CTA, the row-family CTAs first, so the family
   // (and the tensor-map pointers below) is uniform, derived from blockIdx
   const bool trans = !kQuad && (int)blockIdx.y >= row_ctas;
@@ -555,10 +559,9 @@ cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float
   SinoSaga none{};
   const SinoSaga sg = saga ? *saga : none;
   float* out = saga ? nullptr : sino;
-#define FWD_TMA(S_, Q_)                                                                     \
-  k_forward_tma<S_, Q_><<<grid, kFThreads, smem, stream>>>(maps, P, PT, PM, PTM, n, pair_pitch(n), \
-                                                     ang, entries, n_entries, row_ctas, n_det, \
-                                                     out, sg)
+#define FWD_TMA(S_, Q_)                                                                   \
+  launch_pdl(k_forward_tma<S_, Q_>, grid, dim3(kFThreads), smem, stream, maps, P, PT, PM, PTM, n, \
+             pair_pitch(n), ang, entries, n_entries, row_ctas, n_det, out, sg)
   if (saga) {
     if (quad) FWD_TMA(true, true); else FWD_TMA(true, false);
   } else {
@@ -841,6 +844,7 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
 // planes l, l+32, ... and a fixed xor tree combines the lanes (deterministic).
 __global__ void k_adjoint_reduce_warp(const float* __restrict__ part, float* __restrict__ out,
                                       int npix, int S) {
+  griddep_wait();
   const int p = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (p >= npix) return;
@@ -854,6 +858,7 @@ __global__ void k_adjoint_reduce_warp(const float* __restrict__ part, float* __r
 // Sum of the per-split partial images in split order (deterministic).
 __global__ void k_adjoint_reduce(const float* __restrict__ part, float* __restrict__ out,
                                  int npix, int S) {
+  griddep_wait();
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= npix) return;
   float v = 0.f;
@@ -871,11 +876,11 @@ cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, 
   if (sym_entries) {
     dim3 grid((n_det + 31) / 32, (n_entries + 7) / 8);
     if (saga)
-      k_forward_sym<true><<<grid, 256, 0, stream>>>(P, PT, PM, PTM, n, pair_pitch(n), ang,
-                                                    sym_entries, n_entries, n_det, nullptr, *saga);
+      launch_pdl(k_forward_sym<true>, grid, dim3(256), 0, stream, P, PT, PM, PTM, n,
+                 pair_pitch(n), ang, sym_entries, n_entries, n_det, (float*)nullptr, *saga);
     else
-      k_forward_sym<false><<<grid, 256, 0, stream>>>(P, PT, PM, PTM, n, pair_pitch(n), ang,
-                                                     sym_entries, n_entries, n_det, sino, none);
+      launch_pdl(k_forward_sym<false>, grid, dim3(256), 0, stream, P, PT, PM, PTM, n,
+                 pair_pitch(n), ang, sym_entries, n_entries, n_det, sino, none);
     return cudaGetLastError();
   }
   dim3 grid((n_det + 31) / 32, (n_loc + 7) / 8);
@@ -1015,9 +1020,11 @@ static size_t adj_smem(bool pair, bool sym, int T, int W, int* CA_io) {
 
 static void adj_reduce(const float* partial, float* out, int npix, int S, cudaStream_t stream) {
   if (S >= 32 && npix <= 65536)
-    k_adjoint_reduce_warp<<<(npix * 32 + 255) / 256, 256, 0, stream>>>(partial, out, npix, S);
+    launch_pdl(k_adjoint_reduce_warp, dim3((npix * 32 + 255) / 256), dim3(256), 0, stream,
+               partial, out, npix, S);
   else
-    k_adjoint_reduce<<<(npix + 255) / 256, 256, 0, stream>>>(partial, out, npix, S);
+    launch_pdl(k_adjoint_reduce, dim3((npix + 255) / 256), dim3(256), 0, stream, partial, out,
+               npix, S);
 }
 
 cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n, int factor,

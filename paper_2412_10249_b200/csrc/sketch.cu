@@ -179,6 +179,7 @@ __device__ __forceinline__ float saga_px(float pn, float& tab, float& sum, float
 __global__ void __launch_bounds__(256)
 k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, ImageSaga sg) {
   __shared__ __align__(16) CompTile32 sm;
+  griddep_wait();  // bp comes from the stream predecessor (the adjoint reduction)
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
   const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
   const size_t g = (size_t)(y0 + py) * side + x0 + px;
@@ -204,6 +205,7 @@ k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, Image
 // tile, four contiguous pixels per thread, 128-bit accesses to x / phi_sum.
 __global__ void __launch_bounds__(256)
 k_saga_image_coarse32(const float* __restrict__ bp, int side, int f, float inv_f2, ImageSaga sg) {
+  griddep_wait();  // bp comes from the stream predecessor (the adjoint reduction)
   const int n = side / f;
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
   const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
@@ -259,6 +261,7 @@ k_prepare(const float* __restrict__ u, int n, float2* __restrict__ P, float2* __
   // every output is one coalesced float2 (a value of u, the same of um)
   __shared__ float t[33][35];
   __shared__ float tm[33][35];
+  griddep_wait();  // u comes from the stream predecessor (restriction / compensation)
   const bool sym = PM != nullptr;
   const int pitch = pair_pitch(n);
   const int r0 = blockIdx.y * 32 - 1 - kPadC, c0 = blockIdx.x * 32 - 1 - kPadC;
@@ -464,15 +467,15 @@ cudaError_t launch_prepare(const float* u, int n, float2* P, float2* PT, float2*
                            float2* PTM, cudaStream_t s) {
   const int tiles = (pair_pitch(n) + 31) / 32;
   dim3 grid(tiles, tiles);
-  k_prepare<<<grid, 256, 0, s>>>(u, n, P, PT, PM, PTM);
+  launch_pdl(k_prepare, grid, dim3(256), 0, s, u, n, P, PT, PM, PTM);
   return cudaGetLastError();
 }
 
 cudaError_t launch_saga_image_coarse(const float* bp, int side, int f, const ImageSaga& sg,
                                      cudaStream_t s) {
   if (side % 32 == 0 && f <= 32 && 32 % f == 0) {
-    k_saga_image_coarse32<<<dim3(side / 32, side / 32), 256, 0, s>>>(bp, side, f,
-                                                                     1.0f / (float)(f * f), sg);
+    launch_pdl(k_saga_image_coarse32, dim3(side / 32, side / 32), dim3(256), 0, s, bp, side, f,
+               1.0f / (float)(f * f), sg);
     return cudaGetLastError();
   }
   int ts = f > 32 ? f : 32;
@@ -485,7 +488,7 @@ cudaError_t launch_saga_image_coarse(const float* bp, int side, int f, const Ima
 cudaError_t launch_saga_image_full(const float* bp, int side, const CompParams& cp,
                                    const ImageSaga& sg, cudaStream_t s) {
   if (side % 32 == 0 && cp.r <= 6) {
-    k_saga_image_full32<<<dim3(side / 32, side / 32), 256, 0, s>>>(bp, side, cp, sg);
+    launch_pdl(k_saga_image_full32, dim3(side / 32, side / 32), dim3(256), 0, s, bp, side, cp, sg);
     return cudaGetLastError();
   }
   const int TT = comp_tile(cp.r);
