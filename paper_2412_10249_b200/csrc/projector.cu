@@ -940,6 +940,9 @@ void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_o
   if (T > np2) T = np2;
   int tiles = ((n + T - 1) / T) * ((n + T - 1) / T);
   if (sym) tiles /= 2;
+  // angle splits: ~16-20 CTAs per SM. (At f >= 16 a lighter grid, ~4 per SM,
+  // makes an L2-warm step faster by leaving room for the concurrent forward
+  // chain, but a cold-L2 step slower: the windows' HBM latency needs the CTAs.)
   int per_sm = factor == 1 ? 20 : 16;
   if (const char* e = getenv("IMASK_ADJ_CTAS")) {  // tuning: "f:ctas_per_sm,..."
     for (const char* q = e; *q;) {
