@@ -200,7 +200,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    n_gpus = world if world > 1 else args.gpus
+    n_gpus = world  # the GPUs actually used (one process per GPU under torchrun)
+    if args.gpus != world:
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}: launch N > 1 under "
+              "torch.distributed.run; measuring {world} GPU(s)".replace("{world}", str(world)),
+              file=sys.stderr)
 
     base = {
         "metric": "imask_iters_per_sec",
