@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--config", default=CONFIG_KEY)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-microbench", action="store_true",
+                    help="skip the projector microbenchmark (config E)")
     ap.add_argument("--steps-only", action="store_true",
                     help="skip the post-run kernel measurements (launch-list profiling runs)")
     return ap.parse_args()
@@ -83,6 +85,52 @@ def ray_band_count(side: int, n_angles: int, n_det: int, angles=None) -> float:
     hi = np.clip(np.ceil(np.maximum(e1, e2)), 0, n)
     cnt = np.where(st == 0, np.where((x0 >= -1) & (x0 < n), n, 0), np.maximum(hi - lo, 0))
     return float(cnt.sum())
+
+
+def projector_microbench(device, reps: int = 20) -> dict:
+    """Config E: forward K and adjoint K^T alone on the seeded
+    2048^2 ellipse image (2048 angles x 2897 bins) at every level f = 1..64,
+    median of `reps` CUDA-event timed launches each (L2 warm: a projector's
+    operands are on-chip between launches anyway)."""
+    import torch
+
+    from paper_2412_10249_b200 import ctmodel, mrsketch
+    from paper_2412_10249_b200.synth import CONFIGS, ellipse_phantom
+
+    e = CONFIGS["E"]
+    geom = ctmodel.Geometry(e.side, e.n_angles, e.n_det)
+    plan = ctmodel.get_plan(geom)
+    x = torch.from_numpy(ellipse_phantom(e.side, 0).astype(np.float32)).to(device)
+    y = torch.from_numpy(np.random.default_rng(7).standard_normal(geom.m).astype(np.float32)).to(device)
+    sino = torch.empty(geom.m, device=device)
+    stream = torch.cuda.current_stream(device)
+    out = {}
+
+    def med(fn):
+        for _ in range(3):
+            fn()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(reps)]
+        for a, b in ev:
+            a.record(stream)
+            fn()
+            b.record(stream)
+        torch.cuda.synchronize()
+        return float(np.median([a.elapsed_time(b) for a, b in ev]))
+
+    f = 1
+    while f <= 64:
+        u = (x if f == 1 else mrsketch.decimate(x, f)).reshape(-1).contiguous()
+        bp = torch.empty(u.numel(), device=device)
+        fwd = med(lambda: plan.project(u, f, sino))
+        adj = med(lambda: plan.backproject(y, f, bp))
+        nnz = 4.0 / np.pi * e.n_angles * e.side * e.side / f
+        out[f"f{f}"] = {"forward_ms": round(fwd, 4), "adjoint_ms": round(adj, 4),
+                        "fwd_adj_pairs_per_s": round(1e3 / (fwd + adj), 1),
+                        "footprint_evals_per_s": round(2 * nnz / ((fwd + adj) * 1e-3), 1)}
+        f *= 2
+    return {"config": f"E: {e.side}^2, {e.n_angles} angles x {e.n_det} bins, levels f = 1..64",
+            "reps": reps, "statistic": "median", "levels": out}
 
 
 def cpu_reference(cfg, steps: int, warmup: int, sample: int = CPU_SAMPLE_ANGLES):
@@ -488,6 +536,10 @@ def main():
                "api": "solvers.run(prob, 'sketch', ..., record_every=1, x_ref=...)",
                "steps": e2e_steps}
 
+    micro = None
+    if not args.no_microbench and world == 1:
+        micro = projector_microbench(device)
+
     cpu = None
     if not args.no_cpu_baseline and rank == 0:
         cps, det = cpu_reference(cfg, args.steps, args.warmup)
@@ -500,6 +552,7 @@ def main():
                     config=dict(workload, l2="flushed between steps (256 MiB write outside the "
                                              "per-step CUDA events)"),
                     e2e=e2e, roofline=roofline, cpu_baseline=cpu, clocks=clocks,
+                    projector_microbench=micro,
                     gpu_launches=launches, per_level_ms=per_level_ms, level_counts=level_counts)
         print(json.dumps(line))
         try:
