@@ -41,6 +41,7 @@ cudaError_t launch_saga_image_coarse(const float* bp, int side, int f, const Ima
                                      cudaStream_t s);
 cudaError_t launch_saga_image_full(const float* bp, int side, const CompParams& cp,
                                    const ImageSaga& sg, cudaStream_t s);
+cudaError_t launch_saga_sino(const float* psi_new, size_t m, const SinoSaga& sg, cudaStream_t s);
 cudaError_t launch_pdhg_image(const float* bp, float* x, float* xbar, size_t d, float tau,
                               float inv_den, float theta, cudaStream_t s);
 cudaError_t launch_resum(const float* phi_tab, float* phi_sum, int side, const float* psi_tab,
@@ -402,6 +403,16 @@ int forward_saga(imask_plan* pl, const imask_state* st, int level0, const imask_
   sg.p_i = (float)pl->probs[level0];
   sg.sigma = (float)prm->sigma;
   sg.inv_1ps = (float)(1.0 / (1.0 + prm->sigma));
+  static const int split_min_n = [] {
+    const char* e = std::getenv("IMASK_SAGA_SPLIT_MIN_N");  // tuning / A-B runs
+    return e ? std::atoi(e) : 1024;  // measured: a win at n = 1024, a loss at 256-512
+  }();
+  if (pl->side / f >= split_min_n) {
+    // large levels: projection into scratch, then the update as its own pass
+    if ((rc = run_forward(pl, f, t, pl->sino_tmp, nullptr, S(stream)))) return rc;
+    LAUNCH(launch_saga_sino(pl->sino_tmp, m, sg, S(stream)), "saga_sino");
+    return IMASK_OK;
+  }
   if ((rc = run_forward(pl, f, t, nullptr, &sg, S(stream)))) return rc;
   return IMASK_OK;
 }

@@ -370,6 +370,30 @@ k_saga_image_full(const float* __restrict__ bp, int side, CompParams cp, ImageSa
   }
 }
 
+// ---- sinogram-side SAGA update as its own pass --------------------------------
+// psi_new = K_i x from the projector, then solvers.py:205-215 per bin (psi row,
+// psi_sum, dual prox) with 128-bit accesses; used where the forward kernel is
+// better off without the epilogue's prefetched state (large levels).
+__global__ void __launch_bounds__(256)
+k_saga_sino(const float* __restrict__ psi_new, size_t m, SinoSaga sg) {
+  griddep_wait();  // psi_new comes from the stream predecessor (the forward)
+  const size_t q4 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (q4 + 4 <= m) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(psi_new + q4));
+    const float vals[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sino_update(sg, q4 + k, sino_load(sg, q4 + k), vals[k]);
+  } else {
+    for (size_t q = q4; q < m; ++q) sino_update(sg, q, sino_load(sg, q), psi_new[q]);
+  }
+}
+
+cudaError_t launch_saga_sino(const float* psi_new, size_t m, const SinoSaga& sg, cudaStream_t s) {
+  const size_t threads = (m + 3) / 4;
+  return launch_pdl(k_saga_sino, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s,
+                    psi_new, m, sg);
+}
+
 // ---- PDHG primal step (solvers.py:335-337) -----------------------------------
 // x' = (x - tau K^T y) / (1 + tau mu_g) (ridge prox), xbar = x' + theta (x' - x).
 __global__ void __launch_bounds__(256)
