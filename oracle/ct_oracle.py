@@ -166,6 +166,26 @@ class ProjectorOracle:
             self._csr_t = self._csr.T.tocsr()
         return self._csr, self._csr_t
 
+    def set_threads(self, pool, n_threads: int) -> None:
+        """Multi-core CPU baseline: both CSR matvecs split into `n_threads` row
+        blocks run on `pool` (scipy's csr_matvec releases the GIL). Each block
+        writes its own output rows, so results equal the one-core product."""
+        a, at = self.csr_pair()
+        # small operators stay on one core: a thread hand-off costs more than the product
+        n_threads = int(min(n_threads, max(1, a.nnz // 100_000)))
+
+        def blocks(m):
+            cuts = np.linspace(0, m.shape[0], n_threads + 1).astype(np.int64)
+            return [m[lo:hi] for lo, hi in zip(cuts[:-1], cuts[1:]) if hi > lo]
+
+        self._pool = pool
+        self._blocks = (blocks(a), blocks(at))
+
+    def _matvec(self, which: int, v: np.ndarray) -> np.ndarray:
+        if getattr(self, "_pool", None) is None:
+            return (self._csr, self._csr_t)[which] @ v
+        return np.concatenate(list(self._pool.map(lambda blk: blk @ v, self._blocks[which])))
+
     @property
     def domain_dim(self) -> int:
         return self.low * self.low
@@ -179,7 +199,7 @@ class ProjectorOracle:
         if x.size != self.domain_dim:
             raise ValueError(f"image has {x.size} pixels, expected {self.domain_dim}")
         if self._csr is not None:
-            return self._csr @ x
+            return self._matvec(0, x)
         out = np.empty((len(self.angle_idx), self.n_det))
         for k, (ray, pix, w) in enumerate(self._chords):
             out[k] = np.bincount(ray, weights=w * x[pix], minlength=self.n_det)
@@ -187,7 +207,7 @@ class ProjectorOracle:
 
     def adjoint_apply(self, y: np.ndarray) -> np.ndarray:
         if self._csr is not None:
-            return self._csr_t @ np.asarray(y, dtype=float).ravel()
+            return self._matvec(1, np.asarray(y, dtype=float).ravel())
         y = np.asarray(y, dtype=float).reshape(len(self.angle_idx), self.n_det)
         img = np.zeros(self.domain_dim)
         for k, (ray, pix, w) in enumerate(self._chords):
