@@ -23,8 +23,9 @@
 namespace imask {
 cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, const float2* PTM,
                            int n, const FwdAngle* ang, int n_loc, int n_det,
-                           const int2* sym_entries, int n_entries, float* sino,
-                           const SinoSaga* saga, cudaStream_t stream);
+                           const int2* sym_entries, int n_entries, const int4* quad_entries,
+                           int n_quad_entries, float* sino, const SinoSaga* saga,
+                           cudaStream_t stream);
 cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n, int factor,
                            int n_loc, int n_det, const AdjAngle* ang, int sym_s,
                            cudaStream_t stream, const SideStream& side, int* launches);
@@ -325,9 +326,13 @@ int run_forward(imask_plan* pl, int f, const LevelTables* t, float* sino, const 
     e = launch_forward_tma(t->maps, pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->tma_entries,
                            pl->n_tma_entries, pl->tma_row_ctas, pl->tma_quad, pl->n_det, sino,
                            saga, s);
-  else
+  else {
+    static const bool no_quad_l1 = std::getenv("IMASK_NO_QUAD_L1") != nullptr;  // A-B runs
+    const bool quad = pl->tma_quad && !no_quad_l1;
     e = launch_forward(pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->n_loc, pl->n_det,
-                       pl->fwd_entries, pl->n_entries, sino, saga, s);
+                       pl->fwd_entries, pl->n_entries, quad ? pl->tma_entries : nullptr,
+                       pl->n_tma_entries, sino, saga, s);
+  }
   return cuda_check(e, "forward");
 }
 

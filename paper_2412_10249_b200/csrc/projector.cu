@@ -214,6 +214,96 @@ k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
   }
 }
 
+// Quad form of k_forward_sym (the plan's rows closed under a -> n/2 - a too):
+// entry (a, n-a, n/2-a, n/2+a) of the TMA forward's list, one position walk for
+// four rays -- the transpose partners read PT / PTM at the same index as P /
+// PM (the ray through u at pi/2 - theta is the ray through u^T at theta).
+// Singles and the pair (n/4, 3n/4) come as entries with -1 slots; padding
+// entries (all -1) idle. L1-cached loads: the coarse levels, where the images
+// fit on chip and the walks are short.
+template <bool kSaga>
+__global__ void __launch_bounds__(256, 4)
+k_forward_quad(const float2* __restrict__ P, const float2* __restrict__ PT,
+               const float2* __restrict__ PM, const float2* __restrict__ PTM, int n, int pitch,
+               const FwdAngle* __restrict__ ang, const int4* __restrict__ entries, int n_entries,
+               int n_det, float* __restrict__ sino, SinoSaga saga) {
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.y * 8 + warp;
+  if (e >= n_entries) return;
+  const int4 ent = entries[e];
+  const int rows[4] = {ent.x, ent.y, ent.z, ent.w};
+  const int tab = ent.x >= 0 ? ent.x : ent.z;  // the entry's parameter row
+  if (tab < 0) return;
+  const int j = blockIdx.x * 32 + lane;
+  const FwdAngle A = ang[tab];
+  const int jr = min(j, n_det - 1);
+  SinoIn sin[4];
+  if (kSaga && j < n_det) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if (rows[r] >= 0) sin[r] = sino_load(saga, (size_t)rows[r] * n_det + j);
+  }
+  const long long X0 = __double2ll_rn(fma((double)jr, A.xi_dj, A.xi_base) * kFix);
+  int lo, hi;
+  band_range(X0, A.step, A.inv_step, n, &lo, &hi);
+  int wlo = lo < hi ? lo : n, whi = lo < hi ? hi : 0;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    wlo = min(wlo, __shfl_xor_sync(0xffffffffu, wlo, o));
+    whi = max(whi, __shfl_xor_sync(0xffffffffu, whi, o));
+  }
+  const long long dYl = A.step + ((long long)pitch << 32);
+  Fix32 Y = fix_from(X0 + (long long)wlo * dYl + ((long long)(1 + kPadC) << 32));
+  const Fix32 dY = fix_from(dYl);
+  const float S = A.S, B = A.B;
+  griddep_wait();  // the pair images come from the stream predecessor (k_prepare)
+  float2 acc2 = make_float2(0.f, 0.f), accT = make_float2(0.f, 0.f);
+  int b = wlo;
+#pragma unroll 1
+  for (; b + 2 <= whi; b += 2) {
+    float2 v[2], vd[2], vt[2], vdt[2];
+    float g[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      v[k] = __ldg(P + Y.hi);
+      vd[k] = __ldg(PM + Y.hi);
+      vt[k] = __ldg(PT + Y.hi);
+      vdt[k] = __ldg(PTM + Y.hi);
+      g[k] = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
+      fix_add(Y, dY);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      acc2 = fadd2(acc2, v[k]);
+      acc2 = ffma2(g[k], vd[k], acc2);
+      accT = fadd2(accT, vt[k]);
+      accT = ffma2(g[k], vdt[k], accT);
+    }
+  }
+  if (b < whi) {
+    const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
+    acc2 = fadd2(acc2, __ldg(P + Y.hi));
+    acc2 = ffma2(g, __ldg(PM + Y.hi), acc2);
+    accT = fadd2(accT, __ldg(PT + Y.hi));
+    accT = ffma2(g, __ldg(PTM + Y.hi), accT);
+  }
+  if (j < n_det) {
+    const float vals[4] = {acc2.x, acc2.y, accT.x, accT.y};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (rows[r] < 0) continue;
+      const float val = vals[r] * A.wsc;
+      const size_t q = (size_t)rows[r] * n_det + j;
+      if (kSaga) {
+        sino_update(saga, q, sin[r], val);
+      } else {
+        sino[q] = val;
+      }
+    }
+  }
+}
+
 // ---- TMA-staged mirror-symmetric forward ---------------------------------------
 //
 // Same rays and arithmetic as k_forward_sym, but the image data come from
@@ -870,9 +960,20 @@ __global__ void k_adjoint_reduce(const float* __restrict__ part, float* __restri
 
 cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, const float2* PTM,
                            int n, const FwdAngle* ang, int n_loc, int n_det,
-                           const int2* sym_entries, int n_entries, float* sino,
-                           const SinoSaga* saga, cudaStream_t stream) {
+                           const int2* sym_entries, int n_entries, const int4* quad_entries,
+                           int n_quad_entries, float* sino, const SinoSaga* saga,
+                           cudaStream_t stream) {
   SinoSaga none{};
+  if (quad_entries) {
+    dim3 grid((n_det + 31) / 32, (n_quad_entries + 7) / 8);
+    if (saga)
+      launch_pdl(k_forward_quad<true>, grid, dim3(256), 0, stream, P, PT, PM, PTM, n,
+                 pair_pitch(n), ang, quad_entries, n_quad_entries, n_det, (float*)nullptr, *saga);
+    else
+      launch_pdl(k_forward_quad<false>, grid, dim3(256), 0, stream, P, PT, PM, PTM, n,
+                 pair_pitch(n), ang, quad_entries, n_quad_entries, n_det, sino, none);
+    return cudaGetLastError();
+  }
   if (sym_entries) {
     dim3 grid((n_det + 31) / 32, (n_entries + 7) / 8);
     if (saga)
