@@ -77,6 +77,12 @@ class Shard:
     world: int = 1
     group: Any = None
 
+    @property
+    def collective(self) -> bool:
+        """The step reduces its partial backprojection over a process group (a
+        group of one included: that is how the path is exercised on one GPU)."""
+        return self.world > 1 or self.group is not None
+
 
 class Engine:
     """Native state of the fused sketch_step for one problem on one device."""
@@ -96,6 +102,8 @@ class Engine:
         # same geometry and family shares them: (level, sigma, mu, mu_g, parity)
         # -> [handle, launches, pointers it was captured for]
         self._graphs: dict = self.plan.graph_cache
+        self._sharded: dict = {}  # angle-sharded step graphs (torch CUDA graphs with NCCL)
+        self._comm_ready = False
         self.use_graphs = True
 
     def graph(self, state: "SaddleState", level0: int, prm) -> tuple:
@@ -124,6 +132,35 @@ class Engine:
                 hit[0], self.plan.handle, ctypes.byref(cst), level0, ctypes.byref(prm)))
             hit[2] = ptrs
         return hit[0], hit[1]
+
+    def sharded_graph(self, state: "SaddleState", level0: int, prm) -> tuple:
+        """(CUDA graph, kernels per replay) of one angle-sharded step: the forward
+        chain on the side stream, the adjoint, the NCCL all-reduce of the coarse
+        partial backprojection, the image update -- captured once per (level,
+        step scalars, dual-buffer parity, buffers), so a multi-GPU step is one
+        host launch like the single-GPU one (NCCL collectives are capturable)."""
+        cst = state.c_state(self.b)
+        key = ("sharded", level0, prm.sigma, prm.mu, prm.mu_g, prm.g_kind, state.parity,
+               tuple(getattr(cst, name) for name, _ in cst._fields_))
+        hit = self._sharded.get(key)
+        if hit is None:
+            if not self._comm_ready:
+                # the communicator must exist before its first collective is captured
+                _allreduce(self, torch.zeros(1, device=self.device))
+                torch.cuda.synchronize(self.device)
+                self._comm_ready = True
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self._capture_stream()):
+                n = _sharded_step_eager(self, state, level0, prm,
+                                        torch.cuda.current_stream(self.device))
+            hit = (g, n)
+            self._sharded[key] = hit
+        return hit
+
+    def _capture_stream(self) -> torch.cuda.Stream:
+        if getattr(self, "_cap", None) is None:
+            self._cap = torch.cuda.Stream(device=self.device)
+        return self._cap
 
     def release_graphs(self, state: Optional["SaddleState"] = None) -> None:
         """Destroy the cached step graphs (``state`` is accepted for compatibility)."""
@@ -160,7 +197,10 @@ class Engine:
         """Capture the graphs of every level for both dual buffers (outside timing)."""
         for _ in range(2 if state.y_alt is not None else 1):
             for lv in range(self.family.r):
-                self.graph(state, lv, prm)
+                if self.shard.collective:
+                    self.sharded_graph(state, lv, prm)
+                else:
+                    self.graph(state, lv, prm)
             state.swap_dual()
 
 
@@ -338,7 +378,7 @@ def init_state(prob: Problem, seed: int = 0, x0=None, y0=None, exact_memory: boo
 
 
 def _allreduce(eng: Engine, t: torch.Tensor, async_op: bool = False):
-    if eng.shard.world == 1:
+    if not eng.shard.collective:
         return None
     import torch.distributed as dist
 
@@ -364,21 +404,37 @@ def _device_step(eng: Engine, state: SaddleState, level0: int, prm: _lib.ImaskSt
     """Enqueue one iteration; returns the number of kernels launched."""
     L = _lib.lib()
     h, s = eng.plan.handle, eng.plan.stream
-    if eng.shard.world == 1 and eng.use_graphs:
-        g, launches = eng.graph(state, level0, prm)
-        _lib.check(L.imask_graph_launch(g, s))
-        state.swap_dual()
-        return launches
-    cst = ctypes.byref(state.c_state(eng.b))
-    if eng.shard.world == 1:
-        _lib.check(L.imask_sketch_step(h, cst, level0, ctypes.byref(prm), s))
+    if not eng.shard.collective:
+        if eng.use_graphs:
+            g, launches = eng.graph(state, level0, prm)
+            _lib.check(L.imask_graph_launch(g, s))
+            state.swap_dual()
+            return launches
+        _lib.check(L.imask_sketch_step(h, ctypes.byref(state.c_state(eng.b)), level0,
+                                       ctypes.byref(prm), s))
         state.swap_dual()
         return _lib.last_launch_count()
-    # angle-sharded: adjoint -> all-reduce of the coarse partial (NCCL stream); the
-    # forward chain overlaps both (side stream when the dual is double-buffered,
-    # else after the adjoint on this stream); then the replicated image update
+    if eng.use_graphs and state.y_alt is not None:
+        g, launches = eng.sharded_graph(state, level0, prm)
+        g.replay()
+    else:
+        launches = _sharded_step_eager(eng, state, level0, prm,
+                                       torch.cuda.current_stream(eng.device))
+    state.swap_dual()
+    return launches
+
+
+def _sharded_step_eager(eng: Engine, state: SaddleState, level0: int, prm,
+                        main: torch.cuda.Stream) -> int:
+    """Angle-sharded step on ``main``: adjoint -> all-reduce of the coarse partial
+    (NCCL stream); the forward chain overlaps both (side stream when the dual is
+    double-buffered, else after the adjoint on ``main``); then the replicated image
+    update. Returns the kernels launched (the collective not counted)."""
+    L = _lib.lib()
+    h = eng.plan.handle
+    s = ctypes.c_void_p(main.cuda_stream)
+    cst = ctypes.byref(state.c_state(eng.b))
     n = (eng.geom.side // eng.plan.factors[level0]) ** 2
-    main = torch.cuda.current_stream(eng.device)
     side = eng.side_stream() if state.y_alt is not None else None
     launches = 0
     if side is not None:
@@ -388,15 +444,16 @@ def _device_step(eng: Engine, state: SaddleState, level0: int, prm: _lib.ImaskSt
         launches += _lib.last_launch_count()
     _lib.check(L.imask_step_adjoint(h, cst, level0, s))
     launches += _lib.last_launch_count()
-    work = _allreduce(eng, state.bp[:n], async_op=True)
+    with torch.cuda.stream(main):
+        work = _allreduce(eng, state.bp[:n], async_op=True)
     if side is None:
         _lib.check(L.imask_step_forward(h, cst, level0, ctypes.byref(prm), s))
         launches += _lib.last_launch_count()
-    work.wait()
+    with torch.cuda.stream(main):
+        work.wait()
     if side is not None:
         main.wait_stream(side)
     _lib.check(L.imask_step_image(h, cst, level0, ctypes.byref(prm), s))
-    state.swap_dual()
     return launches + _lib.last_launch_count()
 
 

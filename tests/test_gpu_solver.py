@@ -417,3 +417,22 @@ def test_run_sketch_seq_and_saga_saddle():
     rep_s = solvers.run(prob, "saga-saddle", 1e-3, 1e-2, 12, record_every=4, seed=3)
     rep_p = solvers.run(prob, "sketch", 1e-3, 1e-2, 12, record_every=4, seed=3)
     assert np.array_equal(host(rep_s.x), host(rep_p.x))
+
+
+def test_sharded_step_graph_with_nccl():
+    """The multi-GPU step captured as one CUDA graph with its NCCL all-reduce
+    (a real one-rank NCCL group on this GPU): replays are bit-identical to the
+    eager sharded step and match the single-GPU step."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, os.path.join(repo, "tools", "sharded_graph_check.py")],
+                         capture_output=True, text=True, timeout=600, cwd=repo)
+    assert res.returncode == 0, res.stderr[-3000:]
+    out = json.loads(res.stdout.strip().splitlines()[-1])
+    assert out["graph_eq_eager"], out
+    assert out["rel_x_vs_single"] <= 1e-6 and out["rel_y_vs_single"] <= 1e-6, out
+    assert out["graphs_captured"] >= 2, out
