@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-microbench", action="store_true",
                     help="skip the projector microbenchmark (config E)")
+    ap.add_argument("--collective", action="store_true",
+                    help="run the angle-sharded (NCCL) step path even at one rank (path check)")
     ap.add_argument("--steps-only", action="store_true",
                     help="skip the post-run kernel measurements (launch-list profiling runs)")
     return ap.parse_args()
@@ -285,7 +287,8 @@ def main():
                 "side": cfg.side, "n_angles": cfg.n_angles, "n_det": cfg.n_det,
                 "levels": cfg.levels, "seed": SEED, "sigma": SIGMA, "mu_g": cfg.mu_g,
                 "parallelism": (f"mirror-closed angle shards x{n_gpus}, NCCL all-reduce of the "
-                                "coarse backprojection" if n_gpus > 1 else "single GPU")}
+                                "coarse backprojection (one CUDA graph per step)"
+                                if n_gpus > 1 or args.collective else "single GPU")}
 
     if args.impl == "reference":
         if world > 1 and rank != 0:
@@ -308,9 +311,18 @@ def main():
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     group = None
-    if world > 1:
+    dist_on = world > 1 or args.collective
+    if dist_on:
         import torch.distributed as dist
 
+        if "MASTER_ADDR" not in os.environ:  # --collective without torchrun: a group of one
+            import socket
+
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0",
+                              WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=device)
         group = dist.group.WORLD
 
@@ -386,7 +398,7 @@ def main():
             print(json.dumps(dict(base, value=ips, ms_per_step=total_ms / args.steps,
                                   gpu_launches=launches, per_level_ms=per_level_ms,
                                   note="--steps-only: no roofline / e2e / cpu_baseline")))
-        if world > 1:
+        if dist_on:
             torch.distributed.destroy_process_group()
         return
 
@@ -581,7 +593,7 @@ def main():
             os.remove(clk_path)
         except OSError:
             pass
-    if world > 1:
+    if dist_on:
         torch.distributed.destroy_process_group()
 
 
