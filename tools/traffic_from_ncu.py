@@ -31,8 +31,6 @@ fwd = [b for n, g, b in launches if "k_forward_tma" in n]
 # prof_step: imask_project for b (no SAGA), then steps at f=1, f=2, f=32
 if fwd:
     res["forward_f1"] = int(fwd[0])
-    if len(fwd) > 1:
-        res["forward_f1_saga"] = int(fwd[1])
 adj = [b for n, g, b in launches if "k_adjoint<1, 32, 1" in n]
 if adj:
     res["adjoint_f1"] = int(adj[0])
