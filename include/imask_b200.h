@@ -198,6 +198,12 @@ IMASK_API int imask_step_adjoint(imask_plan* plan, const imask_state* st, int le
                                  void* stream);
 IMASK_API int imask_step_forward(imask_plan* plan, const imask_state* st, int level0,
                                  const imask_step_params* prm, void* stream);
+/* Step order (no reference counterpart: scheduling only): at large levels
+ * (coarse side >= 256) makes `stream` wait until the input staging of the last
+ * imask_step_forward on this plan is done, so an adjoint enqueued next on
+ * `stream` starts after the forward kernel has its SM slots (see DESIGN.md,
+ * step DAG); a no-op at coarse levels. */
+IMASK_API int imask_step_wait_staging(imask_plan* plan, int level0, void* stream);
 IMASK_API int imask_step_image(imask_plan* plan, const imask_state* st, int level0,
                                const imask_step_params* prm, void* stream);
 /* One iteration of the deterministic primal-dual reference solver on the

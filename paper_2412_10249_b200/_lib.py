@@ -119,6 +119,7 @@ SIGNATURES = {
         [_vp, ctypes.POINTER(ImaskState), ctypes.c_int, ctypes.POINTER(ImaskStepParams), _vp],
     ),
     "imask_step_adjoint": (ctypes.c_int, [_vp, ctypes.POINTER(ImaskState), ctypes.c_int, _vp]),
+    "imask_step_wait_staging": (ctypes.c_int, [_vp, ctypes.c_int, _vp]),
     "imask_step_forward": (
         ctypes.c_int,
         [_vp, ctypes.POINTER(ImaskState), ctypes.c_int, ctypes.POINTER(ImaskStepParams), _vp],

@@ -442,6 +442,8 @@ def _sharded_step_eager(eng: Engine, state: SaddleState, level0: int, prm,
         _lib.check(L.imask_step_forward(h, cst, level0, ctypes.byref(prm),
                                         ctypes.c_void_p(side.cuda_stream)))
         launches += _lib.last_launch_count()
+        # large levels: the adjoint after the forward's staging (forward CTAs first)
+        _lib.check(L.imask_step_wait_staging(h, level0, s))
     _lib.check(L.imask_step_adjoint(h, cst, level0, s))
     launches += _lib.last_launch_count()
     with torch.cuda.stream(main):

@@ -149,10 +149,13 @@ def test_sharded_phases_match_single_gpu(world):
         assert rel_l2(host(st.y).reshape(len(idx), nd), y1[idx]) <= 1e-5
 
 
-def test_sharded_device_step_stream_ordering(monkeypatch):
+@pytest.mark.parametrize("side,na,nd", [(64, 90, 91), (256, 180, 363)])
+def test_sharded_device_step_stream_ordering(monkeypatch, side, na, nd):
     """solvers._device_step's multi-GPU branch (forward chain on a side stream,
-    adjoint + all-reduce on the main stream) on rank 0 of a 2-rank shard, with
-    the collective stubbed out, equals the three phases run back to back."""
+    adjoint + all-reduce on the main stream; at 256^2 the large levels order the
+    adjoint behind the forward's staging, imask_step_wait_staging) on rank 0 of
+    a 2-rank shard, with the collective stubbed out, equals the three phases run
+    back to back."""
     import ctypes
 
     from paper_2412_10249_b200 import _lib
@@ -163,7 +166,7 @@ def test_sharded_device_step_stream_ordering(monkeypatch):
             pass
 
     monkeypatch.setattr(solvers, "_allreduce", lambda eng, t, async_op=False: _Done())
-    side, na, nd, probs, mu_g = 64, 90, 91, [0.3, 0.3, 0.2, 0.2], 1e-2
+    probs, mu_g = [0.3, 0.3, 0.2, 0.2], 1e-2
     geom = ctmodel.Geometry(side, na, nd)
     b = np.random.default_rng(7).standard_normal(geom.m)
     fam = mrsketch.make_family(4, side, probs, mode="coarse")

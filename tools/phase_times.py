@@ -1,7 +1,9 @@
 """Per-level CUDA-event times of the three step phases (adjoint / forward+SAGA /
 image) of config D, for locating per-level overheads.
 
-    python tools/phase_times.py [--config D] [--reps 20]
+    python tools/phase_times.py [--config D] [--reps 20] [--world W --rank p]
+
+With --world W the shard plan of rank p runs alone on this GPU (no collective).
 """
 import argparse
 import ctypes
@@ -19,13 +21,16 @@ from paper_2412_10249_b200.synth import CONFIGS  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="D")
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--world", type=int, default=1, help="time rank --rank's shard of a world this size")
+ap.add_argument("--rank", type=int, default=0)
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 r = cfg.levels
 geom = ctmodel.Geometry(cfg.side, cfg.n_angles, cfg.n_det)
 b = torch.randn(geom.m, device="cuda").double().cpu().numpy()
 fam = mrsketch.make_family(r, cfg.side, [1.0 / r] * r, mode="coarse")
-prob = dist_mod.make_sharded_problem(geom, b, fam, cfg.mu_g)
+b = dist_mod.local_rows(geom, b, args.rank, args.world)
+prob = dist_mod.make_sharded_problem(geom, b, fam, cfg.mu_g, rank=args.rank, world=args.world)
 eng = prob.engine
 st = solvers.init_state(prob, seed=1)
 prm = solvers._params(1e-6, cfg.mu_g, cfg.mu_g)

@@ -17,12 +17,15 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="D")
 ap.add_argument("--factors", default="1,2,4,8,16,32")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--world", type=int, default=1, help="rank --rank's angle shard of this world size")
+ap.add_argument("--rank", type=int, default=0)
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 geom = ctmodel.Geometry(cfg.side, cfg.n_angles, cfg.n_det)
-plan = ctmodel.get_plan(geom)
+angles = ctmodel.shard_angles(geom.n_angles, args.rank, args.world) if args.world > 1 else None
+plan = ctmodel.get_plan(geom, angles=angles) if angles is not None else ctmodel.get_plan(geom)
 x = torch.from_numpy(ellipse_phantom(cfg.side, 0).astype(np.float32).ravel()).cuda()
-y = torch.randn(geom.m, device="cuda")
+y = torch.randn(plan.m_loc, device="cuda")
 from paper_2412_10249_b200 import mrsketch  # noqa: E402
 
 for f in [int(v) for v in args.factors.split(",")]:
