@@ -80,87 +80,128 @@ k_compensate(const float* __restrict__ x, float* __restrict__ out, int side, Com
   }
 }
 
-// Fast path (side % 32 == 0, r <= 6): 32 x 32 tile, four contiguous pixels per
-// thread with 128-bit loads/stores; the pyramid terms of levels >= 2 are shared
-// by the four pixels, so acc = (sum over levels r-1..2, coarsest first) + the
-// level-1 term, which keeps the reference's accumulation order.
-struct CompTile32 {
-  float tile[32 * 32];
-  float pyr[16 * 16 + 8 * 8 + 4 * 4 + 2 * 2 + 1];
+// Fast path (side % 32 == 0, r <= 6): a 32 x 32 tile held as one float4 per
+// thread (256 threads; thread t holds row py = t >> 3, pixels px = 4 (t & 7) ..
+// px + 3). The block-mean pyramid is built in registers: level 1 (2 x 2 means)
+// and level 2 (4 x 4) by warp shuffles (a warp holds four pixel rows), levels
+// 3..5 by warp 0 from the 8 x 8 level-2 values, with the additions of
+// build_pyramid in the same order, ((s00 + s01) + (s10 + s11)) * 0.25. The
+// compensation's accumulation keeps the reference's order too (coarsest level
+// first, mrsketch.py:141-153): warp 0 folds levels r-1..3 per level-3 node,
+// then every thread adds the level-2 and level-1 terms of its pixels.
+struct Pyr32Smem {
+  float l2[64];  // level-2 values (8 x 8)
+  float a3[16];  // per level-3 node: the accumulated terms of levels r-1..3
 };
 
-__device__ __forceinline__ void comp32_build(CompTile32& sm, int r) {
-  // level j has side 32 >> j at offset off(j) = sum_{l<j} (32 >> l)^2 (level 1 at 0)
-  const float* src = sm.tile;
-  float* dst = sm.pyr;
-  int sn = 32;
-  for (int lev = 1; lev < r; ++lev) {
-    const int dn = sn >> 1;
-    if ((int)threadIdx.x < dn * dn) {
-      const int rr = threadIdx.x / dn, cc = threadIdx.x % dn;
-      const float* s0 = src + (2 * rr) * sn + 2 * cc;
-      dst[threadIdx.x] = ((s0[0] + s0[1]) + (s0[sn] + s0[sn + 1])) * 0.25f;
-    }
-    __syncthreads();
-    src = dst;
-    dst += dn * dn;
-    sn = dn;
-  }
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ void pyr32_low(const float4 v, float& l1a, float& l1b, float& l2) {
+  const float h0 = v.x + v.y, h1 = v.z + v.w;  // horizontal pair sums of this row
+  const float o0 = __shfl_xor_sync(kFull, h0, 8), o1 = __shfl_xor_sync(kFull, h1, 8);  // row py ^ 1
+  const bool odd = (threadIdx.x >> 3) & 1;
+  l1a = (odd ? (o0 + h0) : (h0 + o0)) * 0.25f;  // level-1 node (py >> 1, 2 (t & 7))
+  l1b = (odd ? (o1 + h1) : (h1 + o1)) * 0.25f;  // level-1 node (py >> 1, 2 (t & 7) + 1)
+  const float t = l1a + l1b;
+  const float ot = __shfl_xor_sync(kFull, t, 16);  // level-1 row (py >> 1) ^ 1
+  const bool bot = (threadIdx.x >> 4) & 1;
+  l2 = (bot ? (ot + t) : (t + ot)) * 0.25f;  // level-2 node (py >> 2, t & 7)
 }
 
-// S_r of the four pixels (py, px..px+3) of the staged tile.
-__device__ __forceinline__ float4 comp32_quad(const CompTile32& sm, const CompParams& cp, int py,
-                                             int px) {
-  const float4 v = *reinterpret_cast<const float4*>(&sm.tile[py * 32 + px]);
-  if (cp.r == 1) return v;  // S_1 = I (mrsketch.py:137-138)
-  float shared_acc = 0.f;
-  bool first = true;
-  for (int i = 1; i < cp.r - 1; ++i) {  // levels j = r-1 .. 2
-    const int j = cp.r - i;
-    const int sj = 32 >> j;
-    const int off = (1024 - (1 << (12 - 2 * j))) / 3;  // sum of (32 >> l)^2, l < j
-    const float term = cp.p[i - 1] * sm.pyr[off + (py >> j) * sj + (px >> j)];
-    shared_acc = first ? term : shared_acc + term;
-    first = false;
+// Warp 0 (after the level-2 values are in sm.l2): levels 3, 4 and 5. Lane l < 16
+// holds the level-3 node (l >> 2, l & 3); L4a / L5 are that node's ancestors;
+// lanes 0..3 also hold the level-4 node (l >> 1, l & 1) in L4.
+__device__ __forceinline__ void pyr32_high(const Pyr32Smem& sm, float& L3, float& L4, float& L4a,
+                                           float& L5) {
+  const int l = threadIdx.x & 31;
+  const int R = (l >> 2) & 3, C = l & 3;
+  const float* q = sm.l2 + (2 * R) * 8 + 2 * C;
+  L3 = ((q[0] + q[1]) + (q[8] + q[9])) * 0.25f;
+  const int b4 = ((l >> 1) & 1) * 8 + (l & 1) * 2;
+  const float a = __shfl_sync(kFull, L3, b4), b = __shfl_sync(kFull, L3, b4 + 1),
+              c = __shfl_sync(kFull, L3, b4 + 4), d = __shfl_sync(kFull, L3, b4 + 5);
+  L4 = ((a + b) + (c + d)) * 0.25f;
+  const float e0 = __shfl_sync(kFull, L4, 0), e1 = __shfl_sync(kFull, L4, 1),
+              e2 = __shfl_sync(kFull, L4, 2), e3 = __shfl_sync(kFull, L4, 3);
+  L5 = ((e0 + e1) + (e2 + e3)) * 0.25f;
+  L4a = __shfl_sync(kFull, L4, (R >> 1) * 2 + (C >> 1));
+}
+
+// S_r of the thread's four pixels (block-wide: every thread of the CTA calls it).
+__device__ __forceinline__ float4 comp32(const float4 v, const CompParams& cp, Pyr32Smem& sm) {
+  const int r = cp.r;
+  if (r == 1) return v;  // S_1 = I (mrsketch.py:137-138)
+  float l1a, l1b, l2;
+  pyr32_low(v, l1a, l1b, l2);
+  float acc = 0.f;
+  if (r >= 4) {
+    const int py = threadIdx.x >> 3;
+    if ((py & 3) == 0) sm.l2[(py >> 2) * 8 + (threadIdx.x & 7)] = l2;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float L3, L4, L4a, L5;
+      pyr32_high(sm, L3, L4, L4a, L5);
+      float A = 0.f;
+      if (r >= 6) A = A + cp.p[r - 6] * L5;
+      if (r >= 5) A = A + cp.p[r - 5] * L4a;
+      A = A + cp.p[r - 4] * L3;
+      if (threadIdx.x < 16) sm.a3[threadIdx.x] = A;
+    }
+    __syncthreads();
+    acc = sm.a3[(py >> 3) * 4 + ((threadIdx.x & 7) >> 1)];
   }
-  const float pl = cp.p[cp.r - 2];  // level-1 term (factor 2), last in the telescoping order
-  const float t0 = pl * sm.pyr[(py >> 1) * 16 + (px >> 1)];
-  const float t1 = pl * sm.pyr[(py >> 1) * 16 + (px >> 1) + 1];
-  const float a0 = first ? t0 : shared_acc + t0;
-  const float a1 = first ? t1 : shared_acc + t1;
+  if (r >= 3) acc = acc + cp.p[r - 3] * l2;
+  const float pl = cp.p[r - 2];  // level-1 term (factor 2), last in the telescoping order
+  const float a0 = acc + pl * l1a, a1 = acc + pl * l1b;
   return make_float4((v.x - a0) / cp.pr, (v.y - a0) / cp.pr, (v.z - a1) / cp.pr,
                      (v.w - a1) / cp.pr);
 }
 
 __global__ void __launch_bounds__(256)
 k_compensate32(const float* __restrict__ x, float* __restrict__ out, int side, CompParams cp) {
-  __shared__ __align__(16) CompTile32 sm;
+  __shared__ __align__(16) Pyr32Smem sm;
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
   const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
   const size_t g = (size_t)(y0 + py) * side + x0 + px;
-  *reinterpret_cast<float4*>(&sm.tile[py * 32 + px]) = __ldg(reinterpret_cast<const float4*>(x + g));
-  __syncthreads();
-  comp32_build(sm, cp.r);
-  *reinterpret_cast<float4*>(out + g) = comp32_quad(sm, cp, py, px);
+  const float4 v = __ldg(reinterpret_cast<const float4*>(x + g));
+  *reinterpret_cast<float4*>(out + g) = comp32(v, cp, sm);
 }
 
 // Restriction by a power-of-two factor f = 2^lg <= 32 (side % 32 == 0): each
-// CTA stages a 32 x 32 tile of x with 128-bit loads, builds the block-mean
-// pyramid in shared memory and writes the tile's (32/f)^2 coarse pixels.
+// CTA loads a 32 x 32 tile of x with 128-bit loads, builds the block-mean
+// pyramid up to level lg and writes the tile's (32/f)^2 coarse pixels.
 __global__ void __launch_bounds__(256)
 k_restrict32(const float* __restrict__ x, float* __restrict__ u, int side, int lg) {
-  __shared__ __align__(16) CompTile32 sm;
+  __shared__ __align__(16) Pyr32Smem sm;
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
-  const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
-  *reinterpret_cast<float4*>(&sm.tile[py * 32 + px]) =
-      __ldg(reinterpret_cast<const float4*>(x + (size_t)(y0 + py) * side + x0 + px));
+  const int py = threadIdx.x >> 3, c8 = threadIdx.x & 7;
+  const float4 v =
+      __ldg(reinterpret_cast<const float4*>(x + (size_t)(y0 + py) * side + x0 + c8 * 4));
+  float l1a, l1b, l2;
+  pyr32_low(v, l1a, l1b, l2);
+  const int n = side >> lg;
+  if (lg == 1) {
+    if ((py & 1) == 0)
+      *reinterpret_cast<float2*>(u + (size_t)((y0 >> 1) + (py >> 1)) * n + (x0 >> 1) + 2 * c8) =
+          make_float2(l1a, l1b);
+    return;
+  }
+  if (lg == 2) {
+    if ((py & 3) == 0) u[(size_t)((y0 >> 2) + (py >> 2)) * n + (x0 >> 2) + c8] = l2;
+    return;
+  }
+  if ((py & 3) == 0) sm.l2[(py >> 2) * 8 + c8] = l2;
   __syncthreads();
-  comp32_build(sm, lg + 1);
-  const int sj = 32 >> lg, n = side >> lg;
-  const int off = (1024 - (1 << (12 - 2 * lg))) / 3;  // pyramid offset of level lg
-  if ((int)threadIdx.x < sj * sj) {
-    const int rr = threadIdx.x / sj, cc = threadIdx.x % sj;
-    u[(size_t)((y0 >> lg) + rr) * n + (x0 >> lg) + cc] = sm.pyr[off + rr * sj + cc];
+  if (threadIdx.x < 32) {
+    float L3, L4, L4a, L5;
+    pyr32_high(sm, L3, L4, L4a, L5);
+    const int l = threadIdx.x;
+    if (lg == 3 && l < 16)
+      u[(size_t)((y0 >> 3) + (l >> 2)) * n + (x0 >> 3) + (l & 3)] = L3;
+    else if (lg == 4 && l < 4)
+      u[(size_t)((y0 >> 4) + (l >> 1)) * n + (x0 >> 4) + (l & 1)] = L4;
+    else if (lg == 5 && l == 0)
+      u[(size_t)(y0 >> 5) * n + (x0 >> 5)] = L5;
   }
 }
 
@@ -178,19 +219,17 @@ __device__ __forceinline__ float saga_px(float pn, float& tab, float& sum, float
 // SAGA image update, all with 128-bit accesses.
 __global__ void __launch_bounds__(256)
 k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, ImageSaga sg) {
-  __shared__ __align__(16) CompTile32 sm;
+  __shared__ __align__(16) Pyr32Smem sm;
   griddep_wait();  // bp comes from the stream predecessor (the adjoint reduction)
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
   const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
   const size_t g = (size_t)(y0 + py) * side + x0 + px;
-  *reinterpret_cast<float4*>(&sm.tile[py * 32 + px]) = __ldg(reinterpret_cast<const float4*>(bp + g));
+  const float4 v = __ldg(reinterpret_cast<const float4*>(bp + g));
   float4 tab = *reinterpret_cast<const float4*>(sg.phi_tab + g);
   float4 sum = *reinterpret_cast<const float4*>(sg.phi_sum + g);
   float4 xv = *reinterpret_cast<const float4*>(sg.x + g);
   const float4 xo = xv;
-  __syncthreads();
-  comp32_build(sm, cp.r);
-  const float4 pn = comp32_quad(sm, cp, py, px);
+  const float4 pn = comp32(v, cp, sm);
   saga_px(pn.x, tab.x, sum.x, xv.x, sg);
   saga_px(pn.y, tab.y, sum.y, xv.y, sg);
   saga_px(pn.z, tab.z, sum.z, xv.z, sg);
@@ -204,21 +243,21 @@ k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, Image
 // Coarse level, fast path (side % 32 == 0, f <= 32): 32 x 32 full-resolution
 // tile, four contiguous pixels per thread, 128-bit accesses to x / phi_sum.
 __global__ void __launch_bounds__(256)
-k_saga_image_coarse32(const float* __restrict__ bp, int side, int f, float inv_f2, ImageSaga sg) {
+k_saga_image_coarse32(const float* __restrict__ bp, int side, int lg, float inv_f2, ImageSaga sg) {
   griddep_wait();  // bp comes from the stream predecessor (the adjoint reduction)
-  const int n = side / f;
+  const int n = side >> lg;
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
   const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
   const int row = y0 + py, col = x0 + px;
   const size_t g = (size_t)row * side + col;
-  const int qrow = (row / f) * n;
+  const int qrow = (row >> lg) * n;
   float4 sum = *reinterpret_cast<const float4*>(sg.phi_sum + g);
   float4 xv = *reinterpret_cast<const float4*>(sg.x + g);
   const float4 xo = xv;
   float pn[4], po[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const int q = qrow + (col + k) / f;
+    const int q = qrow + ((col + k) >> lg);
     pn[k] = __ldg(bp + q) * inv_f2;
     po[k] = sg.phi_tab[q];
   }
@@ -231,9 +270,9 @@ k_saga_image_coarse32(const float* __restrict__ bp, int side, int f, float inv_f
   *reinterpret_cast<float4*>(sg.x + g) = xv;
   extrapolate4(sg, g, xo, xv);
   __syncthreads();  // every old table value of this tile's blocks has been read
-  const int tc = 32 / f;
+  const int lt = 5 - lg, tc = 1 << lt;  // coarse pixels per tile side
   if ((int)threadIdx.x < tc * tc) {
-    const int q = (y0 / f + threadIdx.x / tc) * n + x0 / f + threadIdx.x % tc;
+    const int q = ((y0 >> lg) + (threadIdx.x >> lt)) * n + (x0 >> lg) + (threadIdx.x & (tc - 1));
     sg.phi_tab[q] = __ldg(bp + q) * inv_f2;
   }
 }
@@ -374,23 +413,53 @@ k_saga_image_full(const float* __restrict__ bp, int side, CompParams cp, ImageSa
 // psi_new = K_i x from the projector, then solvers.py:205-215 per bin (psi row,
 // psi_sum, dual prox) with 128-bit accesses; used where the forward kernel is
 // better off without the epilogue's prefetched state (large levels).
+template <bool kVec>
 __global__ void __launch_bounds__(256)
 k_saga_sino(const float* __restrict__ psi_new, size_t m, SinoSaga sg) {
   griddep_wait();  // psi_new comes from the stream predecessor (the forward)
   const size_t q4 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (q4 + 4 <= m) {
+  if (kVec && q4 + 4 <= m) {
+    // every operand 16-byte aligned: one 128-bit access per array and thread
     const float4 v = __ldg(reinterpret_cast<const float4*>(psi_new + q4));
-    const float vals[4] = {v.x, v.y, v.z, v.w};
+    const float4 yv = *reinterpret_cast<const float4*>(sg.y_in + q4);
+    const float4 bv = __ldg(reinterpret_cast<const float4*>(sg.b + q4));
+    float4 po = make_float4(0.f, 0.f, 0.f, 0.f), ps = po;
+    if (sg.psi_tab) {
+      po = *reinterpret_cast<const float4*>(sg.psi_tab + q4);
+      ps = *reinterpret_cast<const float4*>(sg.psi_sum + q4);
+    }
+    const float vals[4] = {v.x, v.y, v.z, v.w}, pos[4] = {po.x, po.y, po.z, po.w},
+                pss[4] = {ps.x, ps.y, ps.z, ps.w}, ys[4] = {yv.x, yv.y, yv.z, yv.w},
+                bs[4] = {bv.x, bv.y, bv.z, bv.w};
+    float nsum[4], ny[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) sino_update(sg, q4 + k, sino_load(sg, q4 + k), vals[k]);
+    for (int k = 0; k < 4; ++k) {
+      // sino_update's arithmetic (solvers.py:205-215)
+      const float d = vals[k] - pos[k];
+      const float zeta = d + pss[k];
+      nsum[k] = fmaf(sg.p_i, d, pss[k]);
+      const float yn = fmaf(sg.sigma, zeta, ys[k]);
+      ny[k] = (yn - sg.sigma * bs[k]) * sg.inv_1ps;
+    }
+    if (sg.psi_tab) {
+      *reinterpret_cast<float4*>(sg.psi_sum + q4) = make_float4(nsum[0], nsum[1], nsum[2], nsum[3]);
+      *reinterpret_cast<float4*>(sg.psi_tab + q4) = v;
+    }
+    *reinterpret_cast<float4*>(sg.y + q4) = make_float4(ny[0], ny[1], ny[2], ny[3]);
   } else {
-    for (size_t q = q4; q < m; ++q) sino_update(sg, q, sino_load(sg, q), psi_new[q]);
+    for (size_t q = q4; q < m && q < q4 + 4; ++q) sino_update(sg, q, sino_load(sg, q), psi_new[q]);
   }
 }
 
 cudaError_t launch_saga_sino(const float* psi_new, size_t m, const SinoSaga& sg, cudaStream_t s) {
   const size_t threads = (m + 3) / 4;
-  return launch_pdl(k_saga_sino, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s,
+  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  const bool vec = al(psi_new) && al(sg.y_in) && al(sg.y) && al(sg.b) &&
+                   (!sg.psi_tab || (al(sg.psi_tab) && al(sg.psi_sum)));
+  if (vec)
+    return launch_pdl(k_saga_sino<true>, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s,
+                      psi_new, m, sg);
+  return launch_pdl(k_saga_sino<false>, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s,
                     psi_new, m, sg);
 }
 
@@ -498,7 +567,9 @@ cudaError_t launch_prepare(const float* u, int n, float2* P, float2* PT, float2*
 cudaError_t launch_saga_image_coarse(const float* bp, int side, int f, const ImageSaga& sg,
                                      cudaStream_t s) {
   if (side % 32 == 0 && f <= 32 && 32 % f == 0) {
-    launch_pdl(k_saga_image_coarse32, dim3(side / 32, side / 32), dim3(256), 0, s, bp, side, f,
+    int lg = 0;
+    while ((1 << lg) < f) ++lg;
+    launch_pdl(k_saga_image_coarse32, dim3(side / 32, side / 32), dim3(256), 0, s, bp, side, lg,
                1.0f / (float)(f * f), sg);
     return cudaGetLastError();
   }
