@@ -114,6 +114,14 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
         "l"(*reinterpret_cast<const unsigned long long*>(&b)));
   return r;
 }
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  float2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;"
+      : "=l"(*reinterpret_cast<unsigned long long*>(&r))
+      : "l"(*reinterpret_cast<const unsigned long long*>(&a)),
+        "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+  return r;
+}
 // c + g * b with the scalar g broadcast
 __device__ __forceinline__ float2 ffma2(float g, float2 b, float2 c) {
   float2 r;

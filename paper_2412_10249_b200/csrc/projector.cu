@@ -379,7 +379,7 @@ struct FwdWarpInfo {
 // value and difference planes of P and of PT) and every position, weight and
 // address is computed once for four rays. Pair mode (kQuad = false): entries
 // (a, n-a), one ray family per CTA.
-template <bool kSaga, bool kQuad>
+template <bool kSaga, bool kQuad, bool kVal>
 __global__ void __launch_bounds__(kFThreads)
 k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P,
               const float2* __restrict__ PT, const float2* __restrict__ PM,
@@ -387,7 +387,13 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
               const int4* __restrict__ entries, int n_entries, int row_ctas, int n_det,
               float* __restrict__ sino, SinoSaga saga) {
   constexpr int FB = kQuad ? kFBQuad : kFB;  // bands per chunk
-  constexpr int NI = kQuad ? 4 : 2;          // staged images per chunk
+  // staged images per chunk: kVal stages only the value planes (P, and PT in
+  // quad mode) and forms the difference pair of column c as P[c+1] - P[c], the
+  // subtraction k_prepare does for the difference planes (bit-identical sums,
+  // half the window bytes and shared memory, two more packed adds per band);
+  // otherwise the value and difference planes are staged
+  constexpr int NI = (kQuad ? 2 : 1) * (kVal ? 1 : 2);
+  constexpr int NR = kQuad ? 4 : 2;          // rays (sinogram rows) per entry
   constexpr int kBox = FB * kFWc;            // float2 per image per stage
   extern __shared__ __align__(128) unsigned char smem[];
   float2* stage = reinterpret_cast<float2*>(smem);  // [2 stages][NI images][FB][kFWc]
@@ -412,10 +418,10 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   const int jr = min(j, n_det - 1);
   FwdAngle A{};
   if (valid) A = ang[tab];
-  SinoIn sin[NI];
+  SinoIn sin[NR];
   if (kSaga && valid && j < n_det) {
 #pragma unroll
-    for (int r = 0; r < NI; ++r)
+    for (int r = 0; r < NR; ++r)
       if (rows[r] >= 0) sin[r] = sino_load(saga, (size_t)rows[r] * n_det + j);
   }
   long long X0 = 0;
@@ -493,7 +499,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
       if (cmn > cmx) cmn = cmx = 0;  // no warp walks this chunk
       // TMA needs a 16-byte aligned start in the inner dimension: even pair index
       const int corig = ((cmn + 1 + kPadC) & ~1) - 1 - kPadC;
-      if (cmx - corig + 1 > kFWc) atomicExch(&ctl[0], 1);
+      if (cmx + (kVal ? 1 : 0) - corig + 1 > kFWc) atomicExch(&ctl[0], 1);  // kVal: c .. c + 1
       cmin_tab[t] = corig;
     }
   }
@@ -530,8 +536,9 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
       }
     }
   } else if (nch > 0) {
-    const CUtensorMap* mp[4] = {trans ? &maps.col : &maps.row, trans ? &maps.col_m : &maps.row_m,
-                                &maps.col, &maps.col_m};
+    const CUtensorMap* mp[4] = {trans ? &maps.col : &maps.row,
+                                kVal ? &maps.col : (trans ? &maps.col_m : &maps.row_m), &maps.col,
+                                &maps.col_m};
     constexpr uint32_t kTx = NI * kBox * sizeof(float2);
     if (threadIdx.x == 0) {
       mbar_init(&full[0], 1);
@@ -573,16 +580,28 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             v[k] = win[Y.hi];
-            vd[k] = win[Y.hi + kBox];
-            if (kQuad) {
-              vt[k] = win[Y.hi + 2 * kBox];
-              vdt[k] = win[Y.hi + 3 * kBox];
+            if (kVal) {
+              vd[k] = win[Y.hi + 1];  // value pair of column c + 1 (difference below)
+              if (kQuad) {
+                vt[k] = win[Y.hi + kBox];
+                vdt[k] = win[Y.hi + kBox + 1];
+              }
+            } else {
+              vd[k] = win[Y.hi + kBox];
+              if (kQuad) {
+                vt[k] = win[Y.hi + 2 * kBox];
+                vdt[k] = win[Y.hi + 3 * kBox];
+              }
             }
             g[k] = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
             fix_add(Y, dYw);
           }
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
+            if (kVal) {
+              vd[k] = fsub2(vd[k], v[k]);
+              if (kQuad) vdt[k] = fsub2(vdt[k], vt[k]);
+            }
             acc2 = fadd2(acc2, v[k]);
             acc2 = ffma2(g[k], vd[k], acc2);
             if (kQuad) {
@@ -593,11 +612,15 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
         }
         for (; b < be; ++b) {
           const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
-          acc2 = fadd2(acc2, win[Y.hi]);
-          acc2 = ffma2(g, win[Y.hi + kBox], acc2);
+          const float2 v = win[Y.hi];
+          const float2 vd = kVal ? fsub2(win[Y.hi + 1], v) : win[Y.hi + kBox];
+          acc2 = fadd2(acc2, v);
+          acc2 = ffma2(g, vd, acc2);
           if (kQuad) {
-            accT = fadd2(accT, win[Y.hi + 2 * kBox]);
-            accT = ffma2(g, win[Y.hi + 3 * kBox], accT);
+            const float2 vt = win[Y.hi + (kVal ? 1 : 2) * kBox];
+            const float2 vdt = kVal ? fsub2(win[Y.hi + kBox + 1], vt) : win[Y.hi + 3 * kBox];
+            accT = fadd2(accT, vt);
+            accT = ffma2(g, vdt, accT);
           }
           fix_add(Y, dYw);
         }
@@ -621,7 +644,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   if (valid && j < n_det) {
     const float vals[4] = {acc2.x, acc2.y, accT.x, accT.y};
 #pragma unroll
-    for (int r = 0; r < NI; ++r) {
+    for (int r = 0; r < NR; ++r) {
       if (rows[r] < 0) continue;
       const float val = vals[r] * A.wsc;
       const size_t q = (size_t)rows[r] * n_det + j;
@@ -634,10 +657,37 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   }
 }
 
-size_t forward_tma_smem() {
-  // both modes stage 2 x 2 x 16 or 2 x 4 x 8 bands of kFWc pairs
-  return 2 * 2 * kFB * kFWc * sizeof(float2) + 4 * sizeof(uint64_t) + kFE * sizeof(FwdWarpInfo) +
-         (2 * kFMaxChunks + 4) * sizeof(int);
+size_t forward_tma_smem(bool val) {
+  // both modes stage 2 x (1 or 2) x 16 or 2 x (2 or 4) x 8 bands of kFWc pairs
+  return (val ? 1 : 2) * 2 * kFB * kFWc * sizeof(float2) + 4 * sizeof(uint64_t) +
+         kFE * sizeof(FwdWarpInfo) + (2 * kFMaxChunks + 4) * sizeof(int);
+}
+
+namespace {
+int sm_count() {
+  static const int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+}  // namespace
+
+// Value-plane staging (kVal) where the grid is large (the whole angle set):
+// its CTAs take half the shared memory, so they co-reside with the concurrent
+// adjoint's (f=1 step 932 -> 907 us on one GPU) while the projection alone runs
+// as fast. A small grid (an angle shard: a fraction of a wave) runs latency-
+// bound along each CTA's band walk, where the extra packed subtractions cost
+// (1/8 and 1/4 shards' f=1 forward +7% / +15%), so it stages both planes.
+bool forward_tma_val(int ctas) {
+  static const int forced = [] {
+    const char* e = std::getenv("IMASK_FWD_VAL");  // tuning / A-B runs: 0 or 1
+    return e ? std::atoi(e) : -1;
+  }();
+  if (forced == 0 || forced == 1) return forced == 1;
+  return ctas >= 6 * sm_count();
 }
 
 cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float2* PT,
@@ -645,18 +695,22 @@ cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float
                                const int4* entries, int n_entries, int row_ctas, bool quad,
                                int n_det, float* sino, const SinoSaga* saga, cudaStream_t stream) {
   dim3 grid((n_det + 31) / 32, (n_entries + kFE - 1) / kFE);
-  const size_t smem = forward_tma_smem();
+  const bool val = forward_tma_val((int)(grid.x * grid.y));
+  const size_t smem = forward_tma_smem(val);
   SinoSaga none{};
   const SinoSaga sg = saga ? *saga : none;
   float* out = saga ? nullptr : sino;
-#define FWD_TMA(S_, Q_)                                                                   \
-  launch_pdl(k_forward_tma<S_, Q_>, grid, dim3(kFThreads), smem, stream, maps, P, PT, PM, PTM, n, \
-             pair_pitch(n), ang, entries, n_entries, row_ctas, n_det, out, sg)
+#define FWD_TMA(S_, Q_, V_)                                                                    \
+  launch_pdl(k_forward_tma<S_, Q_, V_>, grid, dim3(kFThreads), smem, stream, maps, P, PT, PM, PTM, \
+             n, pair_pitch(n), ang, entries, n_entries, row_ctas, n_det, out, sg)
+#define FWD_TMA_V(S_, Q_) \
+  if (val) FWD_TMA(S_, Q_, true); else FWD_TMA(S_, Q_, false)
   if (saga) {
-    if (quad) FWD_TMA(true, true); else FWD_TMA(true, false);
+    if (quad) { FWD_TMA_V(true, true); } else { FWD_TMA_V(true, false); }
   } else {
-    if (quad) FWD_TMA(false, true); else FWD_TMA(false, false);
+    if (quad) { FWD_TMA_V(false, true); } else { FWD_TMA_V(false, false); }
   }
+#undef FWD_TMA_V
 #undef FWD_TMA
   return cudaGetLastError();
 }
@@ -998,14 +1052,18 @@ cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, 
 // Opt-in shared memory beyond 48 KB (called once per device at plan creation,
 // outside any stream capture).
 void init_kernel_attributes() {
-  cudaFuncSetAttribute(k_forward_tma<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)forward_tma_smem());
-  cudaFuncSetAttribute(k_forward_tma<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)forward_tma_smem());
-  cudaFuncSetAttribute(k_forward_tma<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)forward_tma_smem());
-  cudaFuncSetAttribute(k_forward_tma<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)forward_tma_smem());
+#define FWD_ATTR(S_, Q_, V_)                                                                  \
+  cudaFuncSetAttribute(k_forward_tma<S_, Q_, V_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                       (int)forward_tma_smem(V_))
+  FWD_ATTR(true, false, false);
+  FWD_ATTR(false, false, false);
+  FWD_ATTR(true, true, false);
+  FWD_ATTR(false, true, false);
+  FWD_ATTR(true, false, true);
+  FWD_ATTR(false, false, true);
+  FWD_ATTR(true, true, true);
+  FWD_ATTR(false, true, true);
+#undef FWD_ATTR
 #define ADJ_ATTR(P_, T_, S_, K_)                                                          \
   cudaFuncSetAttribute(k_adjoint<P_, T_, S_, K_>,                                        \
                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
