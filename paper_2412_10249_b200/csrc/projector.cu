@@ -221,7 +221,7 @@ k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
 // Singles and the pair (n/4, 3n/4) come as entries with -1 slots; padding
 // entries (all -1) idle. L1-cached loads: the coarse levels, where the images
 // fit on chip and the walks are short.
-template <bool kSaga>
+template <bool kSaga, bool kVal>
 __global__ void __launch_bounds__(256, 4)
 k_forward_quad(const float2* __restrict__ P, const float2* __restrict__ PT,
                const float2* __restrict__ PM, const float2* __restrict__ PTM, int n, int pitch,
@@ -267,14 +267,23 @@ k_forward_quad(const float2* __restrict__ P, const float2* __restrict__ PT,
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       v[k] = __ldg(P + Y.hi);
-      vd[k] = __ldg(PM + Y.hi);
       vt[k] = __ldg(PT + Y.hi);
-      vdt[k] = __ldg(PTM + Y.hi);
+      if (kVal) {  // difference pairs as P[c+1] - P[c] (k_prepare's subtraction)
+        vd[k] = __ldg(P + Y.hi + 1);
+        vdt[k] = __ldg(PT + Y.hi + 1);
+      } else {
+        vd[k] = __ldg(PM + Y.hi);
+        vdt[k] = __ldg(PTM + Y.hi);
+      }
       g[k] = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
       fix_add(Y, dY);
     }
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
+      if (kVal) {
+        vd[k] = fsub2(vd[k], v[k]);
+        vdt[k] = fsub2(vdt[k], vt[k]);
+      }
       acc2 = fadd2(acc2, v[k]);
       acc2 = ffma2(g[k], vd[k], acc2);
       accT = fadd2(accT, vt[k]);
@@ -283,10 +292,13 @@ k_forward_quad(const float2* __restrict__ P, const float2* __restrict__ PT,
   }
   if (b < whi) {
     const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
-    acc2 = fadd2(acc2, __ldg(P + Y.hi));
-    acc2 = ffma2(g, __ldg(PM + Y.hi), acc2);
-    accT = fadd2(accT, __ldg(PT + Y.hi));
-    accT = ffma2(g, __ldg(PTM + Y.hi), accT);
+    const float2 v = __ldg(P + Y.hi), vt = __ldg(PT + Y.hi);
+    const float2 vd = kVal ? fsub2(__ldg(P + Y.hi + 1), v) : __ldg(PM + Y.hi);
+    const float2 vdt = kVal ? fsub2(__ldg(PT + Y.hi + 1), vt) : __ldg(PTM + Y.hi);
+    acc2 = fadd2(acc2, v);
+    acc2 = ffma2(g, vd, acc2);
+    accT = fadd2(accT, vt);
+    accT = ffma2(g, vdt, accT);
   }
   if (j < n_det) {
     const float vals[4] = {acc2.x, acc2.y, accT.x, accT.y};
@@ -1020,12 +1032,21 @@ cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, 
   SinoSaga none{};
   if (quad_entries) {
     dim3 grid((n_det + 31) / 32, (n_quad_entries + 7) / 8);
-    if (saga)
-      launch_pdl(k_forward_quad<true>, grid, dim3(256), 0, stream, P, PT, PM, PTM, n,
-                 pair_pitch(n), ang, quad_entries, n_quad_entries, n_det, (float*)nullptr, *saga);
-    else
-      launch_pdl(k_forward_quad<false>, grid, dim3(256), 0, stream, P, PT, PM, PTM, n,
-                 pair_pitch(n), ang, quad_entries, n_quad_entries, n_det, sino, none);
+    static const bool val = [] {
+      // difference pairs from the value planes: half the L1 footprint (f=16 step
+      // 93.5 -> 91.5 us on one GPU)
+      const char* e = std::getenv("IMASK_FWD_VAL_L1");  // tuning / A-B runs: 0 or 1
+      return e ? std::atoi(e) == 1 : true;
+    }();
+#define FWD_QUAD(S_, V_, OUT_, SG_)                                                        \
+  launch_pdl(k_forward_quad<S_, V_>, grid, dim3(256), 0, stream, P, PT, PM, PTM, n, pair_pitch(n), \
+             ang, quad_entries, n_quad_entries, n_det, OUT_, SG_)
+    if (saga) {
+      if (val) FWD_QUAD(true, true, (float*)nullptr, *saga); else FWD_QUAD(true, false, (float*)nullptr, *saga);
+    } else {
+      if (val) FWD_QUAD(false, true, sino, none); else FWD_QUAD(false, false, sino, none);
+    }
+#undef FWD_QUAD
     return cudaGetLastError();
   }
   if (sym_entries) {
