@@ -321,11 +321,16 @@ int run_adjoint(imask_plan* pl, int f, const float* sino, float* out, const AdjA
 // between steps): f = 1/2/4 steps -3/-4/-3% on one GPU and -21/-15/-14% on an
 // eighth-angle shard; at coarse levels (n < 256) the staging delay costs more
 // than the overlap gains, so the two chains start together there.
+// With value-plane staging the whole-set forward's CTAs are small enough to
+// share the SMs at n = 256 as well (f=4 step on one GPU 238 -> 229 us without
+// the wait), so there the order applies from n = 512; an angle shard keeps it
+// from n = 256 (1/8 shard, f=4: 53 us with the wait, 63 us without).
 bool adjoint_after_staging(const imask_plan* pl, int level0) {
-  static const int min_n = [] {
+  static const int forced = [] {
     const char* e = std::getenv("IMASK_ADJ_AFTER_STAGE_MIN_N");  // tuning / A-B runs
-    return e ? std::atoi(e) : 256;
+    return e ? std::atoi(e) : 0;
   }();
+  const int min_n = forced > 0 ? forced : (2 * pl->n_loc > pl->n_angles ? 512 : 256);
   return pl->side / pl->factors[level0] >= min_n;
 }
 
@@ -425,10 +430,14 @@ int forward_saga(imask_plan* pl, const imask_state* st, int level0, const imask_
   sg.p_i = (float)pl->probs[level0];
   sg.sigma = (float)prm->sigma;
   sg.inv_1ps = (float)(1.0 / (1.0 + prm->sigma));
-  static const int split_min_n = [] {
+  static const int split_forced = [] {
     const char* e = std::getenv("IMASK_SAGA_SPLIT_MIN_N");  // tuning / A-B runs
-    return e ? std::atoi(e) : 1024;  // measured: a win at n = 1024, a loss at 256-512
+    return e ? std::atoi(e) : 0;
   }();
+  // measured: a win from n = 1024 with the two-plane forward; with value-plane
+  // staging (the whole angle set) from n = 512 too (f=2 step 401 -> 378 us)
+  const int split_min_n =
+      split_forced > 0 ? split_forced : (2 * pl->n_loc > pl->n_angles ? 512 : 1024);
   if (pl->side / f >= split_min_n) {
     // large levels: projection into scratch, then the update as its own pass
     if ((rc = run_forward(pl, f, t, pl->sino_tmp, nullptr, S(stream)))) return rc;
