@@ -1123,7 +1123,9 @@ void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_o
   // angle splits: ~16-20 CTAs per SM. (At f >= 16 a lighter grid, ~4 per SM,
   // makes an L2-warm step faster by leaving room for the concurrent forward
   // chain, but a cold-L2 step slower: the windows' HBM latency needs the CTAs.)
-  int per_sm = factor == 1 ? 20 : 16;
+  // (factor 1 with many angles: 28 per SM, measured -1% on the whole-set step
+  // with the value-plane forward beside it; a 1/4 or 1/8 shard is slower so)
+  int per_sm = factor == 1 ? (n_loc >= 512 ? 28 : 20) : 16;
   if (const char* e = getenv("IMASK_ADJ_CTAS")) {  // tuning: "f:ctas_per_sm,..."
     for (const char* q = e; *q;) {
       int ff = 0, cc = 0;
