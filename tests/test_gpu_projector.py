@@ -232,19 +232,24 @@ def test_mirror_closed_shards_match_full(n_angles, world):
 @pytest.mark.parametrize("geom_args", [(1024, 1440, 1449, 1), (256, 360, 363, 1), (256, 360, 363, 2)])
 def test_forward_paths_bit_identical(geom_args, tmp_path):
     """The four-ray (quad) TMA forward, the pair TMA forward and the L1 forward
-    trace the same rays with the same arithmetic: bit-identical sinograms. The
-    path switches are read once per process, so each runs in a subprocess."""
+    trace the same rays with the same arithmetic: bit-identical sinograms, with
+    the difference pairs read from the difference planes or formed from the
+    value planes (P[c+1] - P[c]). The path switches are read once per process,
+    so each runs in a subprocess."""
     import subprocess
     import sys
 
     script = os.path.join(REPO, "tools", "repro_quad.py")
     outs = {}
     for name, env_extra in (("quad", {}), ("pair", {"IMASK_NO_QUAD": "1"}),
-                            ("l1", {"IMASK_NO_TMA": "1"})):
+                            ("l1", {"IMASK_NO_TMA": "1"}),
+                            ("quad_planes", {"IMASK_FWD_VAL": "0"}),
+                            ("pair_planes", {"IMASK_NO_QUAD": "1", "IMASK_FWD_VAL": "0"}),
+                            ("l1_planes", {"IMASK_NO_TMA": "1", "IMASK_FWD_VAL_L1": "0"})):
         out = str(tmp_path / f"{name}.npy")
         env = dict(os.environ, OUT=out, **env_extra)
         subprocess.run([sys.executable, script, *map(str, geom_args)], env=env, check=True,
                        capture_output=True, timeout=300)
         outs[name] = np.load(out)
-    assert np.array_equal(outs["quad"], outs["pair"])
-    assert np.array_equal(outs["quad"], outs["l1"])
+    for name in outs:
+        assert np.array_equal(outs["quad"], outs[name]), name
