@@ -37,7 +37,9 @@ cudaError_t launch_prolong(const float* u, float* x, int side, int f, float alph
 cudaError_t launch_compensate(const float* x, float* out, int side, const CompParams& cp,
                               cudaStream_t s);
 cudaError_t launch_prepare(const float* u, int n, float2* P, float2* PT, float2* PM,
-                           float2* PTM, cudaStream_t s);
+                           float2* PTM, bool diff, cudaStream_t s);
+bool forward_tma_val_grid(int n_det, int n_entries);
+bool forward_l1_val();
 cudaError_t launch_saga_image_coarse(const float* bp, int side, int f, const ImageSaga& sg,
                                      cudaStream_t s);
 cudaError_t launch_saga_image_full(const float* bp, int side, const CompParams& cp,
@@ -334,23 +336,48 @@ bool adjoint_after_staging(const imask_plan* pl, int level0) {
   return pl->side / pl->factors[level0] >= min_n;
 }
 
+// TMA staging pays off where the band walks are long; coarse grids use L1 loads
+bool forward_uses_tma(const imask_plan* pl, const LevelTables* t, int n) {
+  static const int tma_min_n = [] {
+    const char* e = std::getenv("IMASK_TMA_MIN_N");  // tuning / A-B runs
+    return e ? std::atoi(e) : 128;
+  }();
+  return t->tma && pl->tma_entries && n >= tma_min_n;
+}
+
+bool forward_quad_l1(const imask_plan* pl) {
+  static const bool no_quad_l1 = std::getenv("IMASK_NO_QUAD_L1") != nullptr;  // A-B runs
+  return pl->tma_quad && !no_quad_l1;
+}
+
+// Whether the forward run_forward picks at this level reads the difference
+// planes PM / PTM: the value-plane kernels form the differences from P / PT,
+// so k_prepare skips those two planes for them (half its writes).
+bool forward_reads_diff(const imask_plan* pl, const LevelTables* t, int n) {
+  if (!pl->sym) return false;  // plain layout: P holds (u, d) pairs itself
+  if (forward_uses_tma(pl, t, n)) return !forward_tma_val_grid(pl->n_det, pl->n_tma_entries);
+  if (forward_quad_l1(pl)) return !forward_l1_val();
+  return true;  // k_forward_sym
+}
+
+int prepare_for_forward(imask_plan* pl, const LevelTables* t, const float* u, int n,
+                        cudaStream_t s) {
+  LAUNCH(launch_prepare(u, n, pl->P, pl->PT, pl->PM, pl->PTM, forward_reads_diff(pl, t, n), s),
+         "prepare");
+  return IMASK_OK;
+}
+
 int run_forward(imask_plan* pl, int f, const LevelTables* t, float* sino, const SinoSaga* saga,
                 cudaStream_t s) {
   const int n = pl->side / f;
   ++g_launches;
   cudaError_t e;
-  // TMA staging pays off where the band walks are long; coarse grids use L1 loads
-  static const int tma_min_n = [] {
-    const char* e = std::getenv("IMASK_TMA_MIN_N");  // tuning / A-B runs
-    return e ? std::atoi(e) : 128;
-  }();
-  if (t->tma && pl->tma_entries && n >= tma_min_n)
+  if (forward_uses_tma(pl, t, n))
     e = launch_forward_tma(t->maps, pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->tma_entries,
                            pl->n_tma_entries, pl->tma_row_ctas, pl->tma_quad, pl->n_det, sino,
                            saga, s);
   else {
-    static const bool no_quad_l1 = std::getenv("IMASK_NO_QUAD_L1") != nullptr;  // A-B runs
-    const bool quad = pl->tma_quad && !no_quad_l1;
+    const bool quad = forward_quad_l1(pl);
     e = launch_forward(pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->n_loc, pl->n_det,
                        pl->fwd_entries, pl->n_entries, quad ? pl->tma_entries : nullptr,
                        pl->n_tma_entries, sino, saga, s);
@@ -410,8 +437,10 @@ int stage_forward_input(imask_plan* pl, const float* x, int level0, cudaStream_t
   else
     LAUNCH(launch_compensate(x, pl->u, pl->side, pl->cp, s), "compensate");
   if (pl->n_loc == 0) return IMASK_OK;
-  LAUNCH(launch_prepare(pl->u, n, pl->P, pl->PT, pl->PM, pl->PTM, s), "prepare");
-  return IMASK_OK;
+  LevelTables* t;
+  int rc;
+  if ((rc = get_tables(pl, f, &t))) return rc;
+  return prepare_for_forward(pl, t, pl->u, n, s);
 }
 
 // psi_new = K_i u on this slab fused with the sinogram-side SAGA update.
@@ -729,7 +758,7 @@ int imask_project(imask_plan* pl, int factor, const float* u, int64_t u_len, flo
   LevelTables* t;
   if ((rc = get_tables(pl, factor, &t))) return rc;
   if (pl->n_loc == 0) return IMASK_OK;
-  LAUNCH(launch_prepare(u, n, pl->P, pl->PT, pl->PM, pl->PTM, S(stream)), "prepare");
+  if ((rc = prepare_for_forward(pl, t, u, n, S(stream)))) return rc;
   if ((rc = run_forward(pl, factor, t, sino, nullptr, S(stream)))) return rc;
   return IMASK_OK;
 }
@@ -811,7 +840,7 @@ int imask_sketch_forward(imask_plan* pl, int level, const float* x, float* sino,
   else
     LAUNCH(launch_compensate(x, pl->u, pl->side, pl->cp, S(stream)), "compensate");
   if (pl->n_loc == 0) return IMASK_OK;
-  LAUNCH(launch_prepare(pl->u, n, pl->P, pl->PT, pl->PM, pl->PTM, S(stream)), "prepare");
+  if ((rc = prepare_for_forward(pl, t, pl->u, n, S(stream)))) return rc;
   if ((rc = run_forward(pl, f, t, sino, nullptr, S(stream)))) return rc;
   return IMASK_OK;
 }
@@ -1138,7 +1167,7 @@ int imask_pdhg_step(imask_plan* pl, const imask_pdhg_state* st, const imask_pdhg
   const cudaStream_t s = S(stream);
   if (pl->n_loc > 0) {
     // dual step: K xbar fused with the conjugate prox in the forward epilogue
-    LAUNCH(launch_prepare(st->xbar, n, pl->P, pl->PT, pl->PM, pl->PTM, s), "prepare");
+    if ((rc = prepare_for_forward(pl, t, st->xbar, n, s))) return rc;
     SinoSaga sg{};
     sg.psi_tab = nullptr;  // no SAGA tables: zeta = K xbar
     sg.psi_sum = nullptr;

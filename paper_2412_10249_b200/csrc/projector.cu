@@ -538,11 +538,13 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
       const Fix32 dY = fix_from(dYl);
       for (int b = wlo; b < whi; ++b) {
         const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
-        acc2 = fadd2(acc2, __ldg(img + Y.hi));
-        acc2 = ffma2(g, __ldg(imgd + Y.hi), acc2);
+        const float2 v = __ldg(img + Y.hi);
+        acc2 = fadd2(acc2, v);
+        acc2 = ffma2(g, kVal ? fsub2(__ldg(img + Y.hi + 1), v) : __ldg(imgd + Y.hi), acc2);
         if (kQuad) {
-          accT = fadd2(accT, __ldg(PT + Y.hi));
-          accT = ffma2(g, __ldg(PTM + Y.hi), accT);
+          const float2 vt = __ldg(PT + Y.hi);
+          accT = fadd2(accT, vt);
+          accT = ffma2(g, kVal ? fsub2(__ldg(PT + Y.hi + 1), vt) : __ldg(PTM + Y.hi), accT);
         }
         fix_add(Y, dY);
       }
@@ -700,6 +702,10 @@ bool forward_tma_val(int ctas) {
   }();
   if (forced == 0 || forced == 1) return forced == 1;
   return ctas >= 6 * sm_count();
+}
+
+bool forward_tma_val_grid(int n_det, int n_entries) {
+  return forward_tma_val(((n_det + 31) / 32) * ((n_entries + kFE - 1) / kFE));
 }
 
 cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float2* PT,
@@ -1024,6 +1030,16 @@ __global__ void k_adjoint_reduce(const float* __restrict__ part, float* __restri
 
 // ---- launchers ----------------------------------------------------------
 
+// The L1 quad forward forms the difference pairs from the value planes: half
+// the L1 footprint (f=16 step 93.5 -> 91.5 us on one GPU).
+bool forward_l1_val() {
+  static const bool val = [] {
+    const char* e = std::getenv("IMASK_FWD_VAL_L1");  // tuning / A-B runs: 0 or 1
+    return e ? std::atoi(e) == 1 : true;
+  }();
+  return val;
+}
+
 cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, const float2* PTM,
                            int n, const FwdAngle* ang, int n_loc, int n_det,
                            const int2* sym_entries, int n_entries, const int4* quad_entries,
@@ -1032,12 +1048,7 @@ cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, 
   SinoSaga none{};
   if (quad_entries) {
     dim3 grid((n_det + 31) / 32, (n_quad_entries + 7) / 8);
-    static const bool val = [] {
-      // difference pairs from the value planes: half the L1 footprint (f=16 step
-      // 93.5 -> 91.5 us on one GPU)
-      const char* e = std::getenv("IMASK_FWD_VAL_L1");  // tuning / A-B runs: 0 or 1
-      return e ? std::atoi(e) == 1 : true;
-    }();
+    const bool val = forward_l1_val();
 #define FWD_QUAD(S_, V_, OUT_, SG_)                                                        \
   launch_pdl(k_forward_quad<S_, V_>, grid, dim3(256), 0, stream, P, PT, PM, PTM, n, pair_pitch(n), \
              ang, quad_entries, n_quad_entries, n_det, OUT_, SG_)

@@ -294,7 +294,7 @@ k_saga_image_coarse32(const float* __restrict__ bp, int side, int lg, float inv_
 // in shared memory so the row-major and the transposed writes are coalesced.
 __global__ void __launch_bounds__(256)
 k_prepare(const float* __restrict__ u, int n, float2* __restrict__ P, float2* __restrict__ PT,
-          float2* __restrict__ PM, float2* __restrict__ PTM) {
+          float2* __restrict__ PM, float2* __restrict__ PTM, bool diff) {
   // t[rr][cc] = u[r0 + rr][c0 - 1 + cc]; for the symmetric layout also the tile
   // of the mirrored image um[R][C] = u[R][n-1-C] at the same coordinates, so
   // every output is one coalesced float2 (a value of u, the same of um)
@@ -323,10 +323,11 @@ k_prepare(const float* __restrict__ u, int n, float2* __restrict__ P, float2* __
         if (!sym) {
           P[o] = make_float2(v, dv);
         } else {
-          // value planes (u, um) in P, difference planes (d, dm) in PM
+          // value planes (u, um) in P, difference planes (d, dm) in PM (only
+          // when the forward reads them; the value-plane kernels subtract)
           const float vm = tm[rr][cc + 1];
           P[o] = make_float2(v, vm);
-          PM[o] = make_float2(dv, tm[rr][cc + 2] - vm);
+          if (diff) PM[o] = make_float2(dv, tm[rr][cc + 2] - vm);
         }
       }
     }
@@ -343,7 +344,7 @@ k_prepare(const float* __restrict__ u, int n, float2* __restrict__ P, float2* __
           // (= band n-1-C of the transposed image)
           const float vm = tm[cc][rr + 1];
           PT[o] = make_float2(v, vm);
-          PTM[o] = make_float2(dv, tm[cc + 1][rr + 1] - vm);
+          if (diff) PTM[o] = make_float2(dv, tm[cc + 1][rr + 1] - vm);
         }
       }
     }
@@ -557,10 +558,10 @@ cudaError_t launch_compensate(const float* x, float* out, int side, const CompPa
 }
 
 cudaError_t launch_prepare(const float* u, int n, float2* P, float2* PT, float2* PM,
-                           float2* PTM, cudaStream_t s) {
+                           float2* PTM, bool diff, cudaStream_t s) {
   const int tiles = (pair_pitch(n) + 31) / 32;
   dim3 grid(tiles, tiles);
-  launch_pdl(k_prepare, grid, dim3(256), 0, s, u, n, P, PT, PM, PTM);
+  launch_pdl(k_prepare, grid, dim3(256), 0, s, u, n, P, PT, PM, PTM, diff);
   return cudaGetLastError();
 }
 
