@@ -1111,12 +1111,17 @@ void init_kernel_attributes() {
 }
 
 // Tile / split choice of the adjoint at one level (shared with the plan's
-// scratch sizing): T = 32 at factor 1, 32 at factor 2, 16 at factor 4, else 8;
+// scratch sizing): T = 32 at factors 1-2, 16 at factors 4-8 and, for plans of
+// >= 512 angles, 16; else 8;
 // T shrinks to the next power of two >= n (>= 8) for small images. The angle
 // splits S give the grid ~16-20 CTAs per SM; with mirror symmetry (sym) the
 // grid covers half the tiles and one extra partial plane holds angle 0.
 void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_out) {
-  int T = factor <= 2 ? 32 : (factor == 4 ? 16 : 8);
+  // (measured beside the value-plane forward: 16 at f = 8 -> step -4% on the
+  // whole set and on shards; 16 at f = 16 -> -1..2% on the whole set, slower
+  // on 1/4 and 1/8 shards, which keep 8; at f = 32 16 is faster with the L2
+  // warm (60.5 -> 54.8 us) but slower after an L2 flush (67 -> 70 us), so 8)
+  int T = factor <= 2 ? 32 : (factor <= 8 || (factor <= 16 && n_loc >= 512) ? 16 : 8);
   if (const char* e = getenv("IMASK_ADJ_TILE")) {  // tuning: "f:T,f:T,..."
     for (const char* q = e; *q;) {
       int ff = 0, tt = 0;
