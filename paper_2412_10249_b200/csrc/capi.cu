@@ -28,8 +28,11 @@ cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, 
                            cudaStream_t stream);
 cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n, int factor,
                            int n_loc, int n_det, const AdjAngle* ang, int sym_s,
-                           cudaStream_t stream, const SideStream& side, int* launches);
+                           cudaStream_t stream, const SideStream& side, int* launches,
+                           int* defer_planes = nullptr);
 int adjoint_planes(int n, int factor, int n_loc, bool sym, int sym_s);
+cudaError_t launch_adjoint_reduce(const float* partial, float* out, int npix, int S,
+                                  cudaStream_t stream);
 bool adjoint_sym_ok(int n, int factor, int n_loc, bool full_even_set);
 cudaError_t launch_restrict(const float* x, float* u, int side, int f, cudaStream_t s);
 cudaError_t launch_prolong(const float* u, float* x, int side, int f, float alpha,
@@ -306,10 +309,11 @@ int ensure_partial(imask_plan* pl, int f) {
 }
 
 int run_adjoint(imask_plan* pl, int f, const float* sino, float* out, const AdjAngle* ang,
-                cudaStream_t s) {
+                cudaStream_t s, int* defer_planes = nullptr) {
   int launches = 0;
   cudaError_t e = launch_adjoint(sino, out, pl->adj_partial, pl->side / f, f, pl->n_loc, pl->n_det,
-                                 ang, pl->sym ? pl->sym_s : -1, s, pl->aux, &launches);
+                                 ang, pl->sym ? pl->sym_s : -1, s, pl->aux, &launches,
+                                 defer_planes);
   g_launches += launches;
   return cuda_check(e, "adjoint");
 }
@@ -425,7 +429,7 @@ constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
 namespace {
 
 int step_image(imask_plan* pl, const imask_state* st, int level0, const imask_step_params* prm,
-               float* xbar, double theta, void* stream);
+               float* xbar, double theta, void* stream, int planes = 0);
 
 // Restriction (or compensation at the full level) of x into pl->u, then the
 // pair images of the forward projector.
@@ -967,7 +971,7 @@ int imask_seq_step(imask_plan* pl, const imask_state* st, int level0,
 namespace {
 
 int step_image(imask_plan* pl, const imask_state* st, int level0, const imask_step_params* prm,
-               float* xbar, double theta, void* stream) {
+               float* xbar, double theta, void* stream, int planes) {
   g_err.clear();
   g_launches = 0;
   int rc = check_level0(pl, level0);
@@ -981,6 +985,18 @@ int step_image(imask_plan* pl, const imask_state* st, int level0, const imask_st
   sg.phi_tab = st->phi_tab + pl->phi_off[level0];
   sg.phi_sum = st->phi_sum;
   sg.x = st->x;
+  if (planes > 0) {
+    const int n = pl->side / f;
+    const bool fused = pl->side % 32 == 0 &&
+                       (level0 < pl->r - 1 ? (f <= 32 && 32 % f == 0) : pl->r <= 6);
+    if (fused) {  // the adjoint's split planes, reduced inside the image kernel
+      sg.planes = pl->adj_partial;
+      sg.n_planes = planes;
+      sg.plane_len = (long long)n * n;
+    } else {
+      LAUNCH(launch_adjoint_reduce(pl->adj_partial, st->bp, n * n, planes, S(stream)), "reduce");
+    }
+  }
   sg.p_i = (float)pl->probs[level0];
   const double s = prm->sigma / prm->mu;
   const bool tv = prm->g_kind == 1;
@@ -1018,6 +1034,7 @@ int imask_sketch_step(imask_plan* pl, const imask_state* st, int level0,
   LevelTables* t;
   if ((rc = get_tables(pl, f, &t))) return rc;
   const cudaStream_t s = S(stream);
+  int planes = 0;  // > 0: the adjoint's split planes are left for the image kernel to sum
   if (pl->n_loc == 0) {
     LAUNCH(cudaMemsetAsync(st->bp, 0, sizeof(float) * n * n, s), "memset");
   } else if (st->y_next) {
@@ -1032,10 +1049,10 @@ int imask_sketch_step(imask_plan* pl, const imask_state* st, int level0,
     cudaEventRecord(pl->aux2.join, pl->aux2.stream);
     const bool after = adjoint_after_staging(pl, level0);
     if (after) cudaStreamWaitEvent(s, pl->ev_staged, 0);
-    if ((rc = run_adjoint(pl, f, st->y, st->bp, t->adj, s))) return rc;
+    if ((rc = run_adjoint(pl, f, st->y, st->bp, t->adj, s, &planes))) return rc;
     if (!after) cudaStreamWaitEvent(s, pl->ev_staged, 0);
     const int launches = g_launches;
-    if ((rc = imask_step_image(pl, st, level0, prm, stream))) return rc;
+    if ((rc = step_image(pl, st, level0, prm, nullptr, 0.0, stream, planes))) return rc;
     g_launches += launches;
     cudaStreamWaitEvent(s, pl->aux2.join, 0);
     return cuda_check(cudaGetLastError(), "fork/join");
@@ -1045,14 +1062,14 @@ int imask_sketch_step(imask_plan* pl, const imask_state* st, int level0,
     cudaEventRecord(pl->aux.fork, s);
     cudaStreamWaitEvent(pl->aux.stream, pl->aux.fork, 0);
     if ((rc = stage_forward_input(pl, st->x, level0, pl->aux.stream))) return rc;
-    if ((rc = run_adjoint(pl, f, st->y, st->bp, t->adj, s))) return rc;
+    if ((rc = run_adjoint(pl, f, st->y, st->bp, t->adj, s, &planes))) return rc;
     cudaEventRecord(pl->aux.join, pl->aux.stream);
     cudaStreamWaitEvent(s, pl->aux.join, 0);
     if ((rc = cuda_check(cudaGetLastError(), "fork/join"))) return rc;
     if ((rc = forward_saga(pl, st, level0, prm, t, s))) return rc;
   }
   const int launches = g_launches;
-  if ((rc = imask_step_image(pl, st, level0, prm, stream))) return rc;
+  if ((rc = step_image(pl, st, level0, prm, nullptr, 0.0, stream, planes))) return rc;
   g_launches += launches;
   return IMASK_OK;
 }

@@ -192,6 +192,12 @@ struct ImageSaga {
   float inv_den;  // 1 / (1 + s*mu_g)
   float* xbar = nullptr;  // sketch_seq_step: xbar = x' + theta (x' - x) (nullptr: none)
   float theta = 0.f;
+  // n_planes > 0: the backprojection is the sum of n_planes partial planes of
+  // the adjoint's angle splits (plane stride plane_len), reduced here in the
+  // order of k_adjoint_reduce / k_adjoint_reduce_warp instead of read from bp
+  const float* planes = nullptr;
+  int n_planes = 0;
+  long long plane_len = 0;
 };
 
 // Primal extrapolation of sketch_seq_step (solvers.py:296-300) for one pixel /

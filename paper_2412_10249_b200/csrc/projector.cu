@@ -1219,8 +1219,14 @@ static size_t adj_smem(bool pair, bool sym, int T, int W, int* CA_io) {
          (size_t)CA * W * elem;
 }
 
+// Reduction mode of the split planes, shared by the reduce kernels and the
+// image-side kernels that fold the reduction in (k_saga_image_coarse32 repeats
+// the predicate): warp per pixel (lane-strided
+// planes, xor tree) for many planes and few pixels, else planes in order.
+static bool adjoint_reduce_warp(int npix, int planes) { return planes >= 32 && npix <= 65536; }
+
 static void adj_reduce(const float* partial, float* out, int npix, int S, cudaStream_t stream) {
-  if (S >= 32 && npix <= 65536)
+  if (adjoint_reduce_warp(npix, S))
     launch_pdl(k_adjoint_reduce_warp, dim3((npix * 32 + 255) / 256), dim3(256), 0, stream,
                partial, out, npix, S);
   else
@@ -1228,9 +1234,19 @@ static void adj_reduce(const float* partial, float* out, int npix, int S, cudaSt
                npix, S);
 }
 
+// defer_planes != nullptr: the split planes are left unreduced (the consumer
+// sums them) and their count is returned there (0: the result is in out).
+cudaError_t launch_adjoint_reduce(const float* partial, float* out, int npix, int S,
+                                  cudaStream_t stream) {
+  adj_reduce(partial, out, npix, S, stream);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n, int factor,
                            int n_loc, int n_det, const AdjAngle* ang, int sym_s,
-                           cudaStream_t stream, const SideStream& side, int* launches) {
+                           cudaStream_t stream, const SideStream& side, int* launches,
+                           int* defer_planes) {
+  if (defer_planes) *defer_planes = 0;
   const bool sym = adjoint_sym_ok(n, factor, n_loc, sym_s >= 0);
   int T, S;
   adjoint_layout(n, factor, n_loc, sym, &T, &S);
@@ -1266,8 +1282,12 @@ cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n,
     ++*launches;
     if (sym_s > 0 && side.stream) cudaStreamWaitEvent(stream, side.join, 0);
     if (planes > 1) {
-      adj_reduce(partial, out, n * n, planes, stream);
-      ++*launches;
+      if (defer_planes) {
+        *defer_planes = planes;
+      } else {
+        adj_reduce(partial, out, n * n, planes, stream);
+        ++*launches;
+      }
     }
     return cudaGetLastError();
   }
@@ -1278,8 +1298,12 @@ cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n,
                per_split, n_loc, n_loc, n_det, ang);
   *launches = 1;
   if (S > 1) {
-    adj_reduce(partial, out, n * n, S, stream);
-    *launches = 2;
+    if (defer_planes) {
+      *defer_planes = S;
+    } else {
+      adj_reduce(partial, out, n * n, S, stream);
+      *launches = 2;
+    }
   }
   return cudaGetLastError();
 }

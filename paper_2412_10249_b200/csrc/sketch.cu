@@ -205,6 +205,21 @@ k_restrict32(const float* __restrict__ x, float* __restrict__ u, int side, int l
   }
 }
 
+// The adjoint's split planes summed for four consecutive pixels, planes in
+// order (k_adjoint_reduce's order; used where the planes are many pixels).
+__device__ __forceinline__ float4 planes_sum4(const ImageSaga& sg, size_t g) {
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* p = sg.planes + g;
+  for (int s = 0; s < sg.n_planes; ++s, p += sg.plane_len) {
+    const float4 w = __ldg(reinterpret_cast<const float4*>(p));
+    v.x += w.x;
+    v.y += w.y;
+    v.z += w.z;
+    v.w += w.w;
+  }
+  return v;
+}
+
 __device__ __forceinline__ float saga_px(float pn, float& tab, float& sum, float& xv,
                                          const ImageSaga& sg) {
   const float d = pn - tab;
@@ -224,7 +239,9 @@ k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, Image
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
   const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
   const size_t g = (size_t)(y0 + py) * side + x0 + px;
-  const float4 v = __ldg(reinterpret_cast<const float4*>(bp + g));
+  // the full level has side^2 > 65536 pixels: the planes are summed in order
+  const float4 v = sg.n_planes > 0 ? planes_sum4(sg, g)
+                                   : __ldg(reinterpret_cast<const float4*>(bp + g));
   float4 tab = *reinterpret_cast<const float4*>(sg.phi_tab + g);
   float4 sum = *reinterpret_cast<const float4*>(sg.phi_sum + g);
   float4 xv = *reinterpret_cast<const float4*>(sg.x + g);
@@ -244,9 +261,35 @@ k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, Image
 // tile, four contiguous pixels per thread, 128-bit accesses to x / phi_sum.
 __global__ void __launch_bounds__(256)
 k_saga_image_coarse32(const float* __restrict__ bp, int side, int lg, float inv_f2, ImageSaga sg) {
-  griddep_wait();  // bp comes from the stream predecessor (the adjoint reduction)
+  __shared__ float cv[256];  // the tile's (32/f)^2 coarse backprojection values (planes mode)
+  griddep_wait();  // bp (or the split planes) come from the stream predecessor (the adjoint)
   const int n = side >> lg;
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const int lt = 5 - lg, tc = 1 << lt;  // coarse pixels per tile side
+  if (sg.n_planes > 0) {
+    // sum the adjoint's split planes for this tile's coarse pixels in the order of
+    // k_adjoint_reduce_warp (many planes, few pixels) or k_adjoint_reduce
+    const int P = sg.n_planes;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (P >= 32 && n * n <= 65536) {
+      for (int c = warp; c < tc * tc; c += 8) {
+        const int q = ((y0 >> lg) + (c >> lt)) * n + (x0 >> lg) + (c & (tc - 1));
+        float v = 0.f;
+        for (int s = lane; s < P; s += 32) v += __ldg(sg.planes + (size_t)s * sg.plane_len + q);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) cv[c] = v;
+      }
+    } else {
+      for (int c = threadIdx.x; c < tc * tc; c += blockDim.x) {
+        const int q = ((y0 >> lg) + (c >> lt)) * n + (x0 >> lg) + (c & (tc - 1));
+        float v = 0.f;
+        for (int s = 0; s < P; ++s) v += __ldg(sg.planes + (size_t)s * sg.plane_len + q);
+        cv[c] = v;
+      }
+    }
+    __syncthreads();
+  }
   const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
   const int row = y0 + py, col = x0 + px;
   const size_t g = (size_t)row * side + col;
@@ -258,7 +301,10 @@ k_saga_image_coarse32(const float* __restrict__ bp, int side, int lg, float inv_
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int q = qrow + ((col + k) >> lg);
-    pn[k] = __ldg(bp + q) * inv_f2;
+    const float b = sg.n_planes > 0
+                        ? cv[(((row >> lg) - (y0 >> lg)) << lt) + ((col + k) >> lg) - (x0 >> lg)]
+                        : __ldg(bp + q);
+    pn[k] = b * inv_f2;
     po[k] = sg.phi_tab[q];
   }
   float d;
@@ -270,10 +316,9 @@ k_saga_image_coarse32(const float* __restrict__ bp, int side, int lg, float inv_
   *reinterpret_cast<float4*>(sg.x + g) = xv;
   extrapolate4(sg, g, xo, xv);
   __syncthreads();  // every old table value of this tile's blocks has been read
-  const int lt = 5 - lg, tc = 1 << lt;  // coarse pixels per tile side
   if ((int)threadIdx.x < tc * tc) {
     const int q = ((y0 >> lg) + (threadIdx.x >> lt)) * n + (x0 >> lg) + (threadIdx.x & (tc - 1));
-    sg.phi_tab[q] = __ldg(bp + q) * inv_f2;
+    sg.phi_tab[q] = (sg.n_planes > 0 ? cv[threadIdx.x] : __ldg(bp + q)) * inv_f2;
   }
 }
 
