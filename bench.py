@@ -562,7 +562,8 @@ def main():
             dt = float(t.item())
         if rank == 0:
             print(f"[bench] e2e: setup {1e3 * (t1 - t0):.1f} ms, run {1e3 * (t2 - t1):.1f} ms, "
-                  f"read-back {1e3 * (time.perf_counter() - t2):.1f} ms", file=sys.stderr)
+                  f"read-back {1e3 * (time.perf_counter() - t2):.1f} ms, step-graph re-targets "
+                  f"{prob2.engine.graph_updates}", file=sys.stderr)
         e2e = {"value": e2e_steps / dt, "unit": "iter/s",
                "h2d_bytes_per_step": round((b_host.numel() + xref_host.numel()) * 4 / e2e_steps),
                "d2h_bytes_per_step": round(8 + x_out.numel() * 4 / e2e_steps),

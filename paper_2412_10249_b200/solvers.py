@@ -106,6 +106,7 @@ class Engine:
         self._sharded: dict = {}  # angle-sharded step graphs (torch CUDA graphs with NCCL)
         self._comm_ready = False
         self.use_graphs = True
+        self.graph_updates = 0  # re-targets of cached step graphs to another state's buffers
 
     def graph(self, state: "SaddleState", level0: int, prm) -> tuple:
         """(graph handle, kernels per replay) of one step at ``level0`` on ``state``.
@@ -129,6 +130,7 @@ class Engine:
             hit = [h, n.value, ptrs]
             self._graphs[key] = hit
         elif hit[2] != ptrs:
+            self.graph_updates += 1
             _lib.check(_lib.lib().imask_step_graph_update(
                 hit[0], self.plan.handle, ctypes.byref(cst), level0, ctypes.byref(prm)))
             hit[2] = ptrs

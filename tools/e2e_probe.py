@@ -43,3 +43,15 @@ for _ in range(2):
         solvers._device_step(prob.engine, st, int(i), prm)
     torch.cuda.synchronize()
     print(f"200 bare graph steps: {1e3 * (time.perf_counter() - t0):7.2f} ms", flush=True)
+# host cost of re-targeting the cached step graphs to a new state's buffers
+st2 = solvers.init_state(prob, seed=2)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for lv in range(r):
+    prob.engine.graph(st2, lv, prm)
+t1 = time.perf_counter()
+for lv in range(r):
+    prob.engine.graph(st2, lv, prm)
+t2 = time.perf_counter()
+print(f"re-target {r} step graphs to a new state: {1e3 * (t1 - t0):.2f} ms; "
+      f"cached lookups: {1e3 * (t2 - t1):.3f} ms", flush=True)
