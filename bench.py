@@ -474,7 +474,12 @@ def main():
                             "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                             "frac": round(gbs / hbm_peak, 4),
                             "traffic": traffic_tab.get("saga_image_full" if f == 1 else
-                                                       "saga_image_coarse")})
+                                                       "saga_image_coarse"),
+                            "traffic_note": "ncu DRAM bytes of the launch inside the fused step "
+                                            "(profiles/traffic.json), which reads the adjoint's "
+                                            "split planes (4 B x planes x n^2, L2-resident in the "
+                                            "real step, cold under ncu) in place of bp; the timed "
+                                            "launch here reads bp"})
 
     # dominant kernel of the step: the level-1 projector (forward or adjoint, whichever
     # is slower). It is FP32-issue bound; the HBM figure uses its compulsory
