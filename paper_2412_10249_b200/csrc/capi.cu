@@ -987,8 +987,11 @@ int step_image(imask_plan* pl, const imask_state* st, int level0, const imask_st
   sg.x = st->x;
   if (planes > 0) {
     const int n = pl->side / f;
+    // the full-level kernel sums planes in order only; many planes over few
+    // pixels (the reduce kernels' warp-tree order) keep the explicit reduction
+    const bool warp_order = planes >= 32 && (long long)n * n <= 65536;
     const bool fused = pl->side % 32 == 0 &&
-                       (level0 < pl->r - 1 ? (f <= 32 && 32 % f == 0) : pl->r <= 6);
+                       (level0 < pl->r - 1 ? (f <= 32 && 32 % f == 0) : (pl->r <= 6 && !warp_order));
     if (fused) {  // the adjoint's split planes, reduced inside the image kernel
       sg.planes = pl->adj_partial;
       sg.n_planes = planes;

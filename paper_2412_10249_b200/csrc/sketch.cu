@@ -239,7 +239,8 @@ k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, Image
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
   const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
   const size_t g = (size_t)(y0 + py) * side + x0 + px;
-  // the full level has side^2 > 65536 pixels: the planes are summed in order
+  // planes summed in order (step_image fuses the reduction here only when the
+  // reduce kernels would use that order too)
   const float4 v = sg.n_planes > 0 ? planes_sum4(sg, g)
                                    : __ldg(reinterpret_cast<const float4*>(bp + g));
   float4 tab = *reinterpret_cast<const float4*>(sg.phi_tab + g);

@@ -149,6 +149,39 @@ def test_sharded_phases_match_single_gpu(world):
         assert rel_l2(host(st.y).reshape(len(idx), nd), y1[idx]) <= 1e-5
 
 
+@pytest.mark.parametrize("side,na,nd,r", [(64, 90, 91, 3), (256, 360, 363, 4)])
+def test_folded_plane_reduction_matches_explicit(side, na, nd, r):
+    """The single-GPU step lets the image-side kernel sum the adjoint's split
+    planes (in the reduce kernels' order); the phase entry points reduce them
+    into bp first. Both give bit-identical iterates at every level, including
+    the warp-tree order of many planes (256^2 / 360 angles, f = 8)."""
+    import ctypes
+
+    from paper_2412_10249_b200 import _lib
+    from paper_2412_10249_b200 import dist as dist_mod
+
+    geom = ctmodel.Geometry(side, na, nd)
+    probs = [1.0 / r] * r
+    b = np.random.default_rng(8).random(geom.m)
+    fam = mrsketch.make_family(r, side, probs, mode="coarse")
+    pr = dist_mod.make_sharded_problem(geom, b, fam, 1e-2)
+    st_f, st_p = solvers.init_state(pr, seed=4), solvers.init_state(pr, seed=4)
+    prm = solvers._params(2e-4, 1e-2, 1e-2)
+    L = _lib.lib()
+    h, stream = pr.engine.plan.handle, pr.engine.plan.stream
+    for lv in list(range(r)) * 2:
+        solvers._device_step(pr.engine, st_f, lv, prm)
+        cst = ctypes.byref(st_p.c_state(pr.engine.b))
+        _lib.check(L.imask_step_adjoint(h, cst, lv, stream))
+        _lib.check(L.imask_step_forward(h, cst, lv, ctypes.byref(prm), stream))
+        _lib.check(L.imask_step_image(h, cst, lv, ctypes.byref(prm), stream))
+        st_p.swap_dual()
+    torch.cuda.synchronize()
+    for a, c in ((st_f.x, st_p.x), (st_f.y, st_p.y), (st_f.phi_sum, st_p.phi_sum),
+                 (st_f.phi_tab, st_p.phi_tab)):
+        assert np.array_equal(host(a), host(c))
+
+
 @pytest.mark.parametrize("side,na,nd", [(64, 90, 91), (256, 180, 363)])
 def test_sharded_device_step_stream_ordering(monkeypatch, side, na, nd):
     """solvers._device_step's multi-GPU branch (forward chain on a side stream,
