@@ -19,6 +19,25 @@
 #include "imask_b200.h"
 #include "imask_common.cuh"
 #include "sketch.cuh"
+// Stream priorities for the step DAG (A/B knob IMASK_PRIO: 0 = none, 1 = side
+// streams (forward chain) first, 2 = capture stream (adjoint) first). Captured
+// kernels keep their stream's priority when instantiated with node priorities.
+static int prio_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("IMASK_PRIO");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+static cudaError_t make_stream(cudaStream_t* s, bool high) {
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  return cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, high ? greatest : least);
+}
+static unsigned long long graph_flags() {
+  return prio_mode() ? cudaGraphInstantiateFlagUseNodePriority : 0ull;
+}
+
 
 namespace imask {
 cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, const float2* PTM,
@@ -688,11 +707,11 @@ int imask_plan_create_list(int side, int n_angles, int n_det, int n_loc, const i
     imask_plan_destroy(pl);
     return rc;
   }
-  if ((rc = cuda_check(cudaStreamCreateWithFlags(&pl->aux.stream, cudaStreamNonBlocking),
+  if ((rc = cuda_check(make_stream(&pl->aux.stream, prio_mode() == 1),
                        "side stream")) ||
       (rc = cuda_check(cudaEventCreateWithFlags(&pl->aux.fork, cudaEventDisableTiming), "event")) ||
       (rc = cuda_check(cudaEventCreateWithFlags(&pl->aux.join, cudaEventDisableTiming), "event")) ||
-      (rc = cuda_check(cudaStreamCreateWithFlags(&pl->aux2.stream, cudaStreamNonBlocking),
+      (rc = cuda_check(make_stream(&pl->aux2.stream, prio_mode() == 1),
                        "side stream")) ||
       (rc = cuda_check(cudaEventCreateWithFlags(&pl->aux2.fork, cudaEventDisableTiming), "event")) ||
       (rc = cuda_check(cudaEventCreateWithFlags(&pl->aux2.join, cudaEventDisableTiming), "event")) ||
@@ -1084,7 +1103,7 @@ int capture_step(imask_plan* pl, const imask_state* st, int level0, const imask_
                  cudaGraph_t* graph, int* launches) {
   cudaStream_t s;
   int rc;
-  if ((rc = cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create")))
+  if ((rc = cuda_check(make_stream(&s, prio_mode() == 2), "stream create")))
     return rc;
   *graph = nullptr;
   rc = cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
@@ -1117,7 +1136,7 @@ int imask_step_graph_create(imask_plan* pl, const imask_state* st, int level0,
   gr->device = pl->device;
   int n_launch = 0;
   rc = capture_step(pl, st, level0, prm, &gr->graph, &n_launch);
-  if (!rc) rc = cuda_check(cudaGraphInstantiate(&gr->exec, gr->graph, 0), "graph instantiate");
+  if (!rc) rc = cuda_check(cudaGraphInstantiate(&gr->exec, gr->graph, graph_flags()), "graph instantiate");
   if (rc) {
     imask_graph_destroy(gr);
     return rc;
@@ -1142,7 +1161,7 @@ int imask_step_graph_update(imask_graph* gr, imask_plan* pl, const imask_state* 
   if (cudaGraphExecUpdate(gr->exec, fresh, &info) != cudaSuccess) {
     cudaGetLastError();  // clear the update failure; instantiate afresh
     cudaGraphExec_t exec = nullptr;
-    rc = cuda_check(cudaGraphInstantiate(&exec, fresh, 0), "graph instantiate");
+    rc = cuda_check(cudaGraphInstantiate(&exec, fresh, graph_flags()), "graph instantiate");
     if (rc) {
       cudaGraphDestroy(fresh);
       return rc;
