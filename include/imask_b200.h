@@ -37,7 +37,12 @@ extern "C" {
 #define IMASK_ECUDA 4  /* CUDA runtime error                     -> RuntimeError      */
 #define IMASK_MAX_LEVELS 12
 
-typedef struct imask_plan imask_plan; /* opaque; owns per-angle tables + scratch */
+/* Opaque plan; owns the per-angle tables and device scratch (staged pair
+ * images, sinogram staging, adjoint split planes). The scratch is shared by
+ * every call on the plan, so calls on one plan must be stream-ordered with
+ * respect to each other (one stream, or caller-ordered streams); use one plan
+ * per concurrent stream. */
+typedef struct imask_plan imask_plan;
 
 /* Solver state of one rank: every pointer is a device buffer.
  * Mirrors SaddleState (solvers.py:119-140) with compact coarse phi rows:

@@ -19,25 +19,6 @@
 #include "imask_b200.h"
 #include "imask_common.cuh"
 #include "sketch.cuh"
-// Stream priorities for the step DAG (A/B knob IMASK_PRIO: 0 = none, 1 = side
-// streams (forward chain) first, 2 = capture stream (adjoint) first). Captured
-// kernels keep their stream's priority when instantiated with node priorities.
-static int prio_mode() {
-  static const int m = [] {
-    const char* e = std::getenv("IMASK_PRIO");
-    return e ? std::atoi(e) : 0;
-  }();
-  return m;
-}
-static cudaError_t make_stream(cudaStream_t* s, bool high) {
-  int least = 0, greatest = 0;
-  cudaDeviceGetStreamPriorityRange(&least, &greatest);
-  return cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, high ? greatest : least);
-}
-static unsigned long long graph_flags() {
-  return prio_mode() ? cudaGraphInstantiateFlagUseNodePriority : 0ull;
-}
-
 
 namespace imask {
 cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, const float2* PTM,
@@ -175,6 +156,7 @@ struct imask_plan {
   SideStream aux2;               // forward chain of imask_sketch_step, concurrent with the adjoint
   cudaEvent_t ev_staged = nullptr;  // aux2: x has been read (restriction / compensation done)
   size_t adj_partial_len = 0;
+  std::vector<float*> retired;   // replaced scratch buffers, freed with the plan
   int64_t scratch = 0;
   CompParams cp{};
   ResumParams rp{};
@@ -316,7 +298,10 @@ int ensure_partial(imask_plan* pl, int f) {
   const bool sym = adjoint_sym_ok(n, f, pl->n_loc, pl->sym);
   const size_t need = (size_t)adjoint_planes(n, f, pl->n_loc, sym, pl->sym_s) * n * n;
   if (need > pl->adj_partial_len) {
-    if (pl->adj_partial) cudaFree(pl->adj_partial);
+    // the plan is created with room for every factor of its family; a larger
+    // factor served later (backproject at another f) gets a new buffer, and the
+    // old one is retired, not freed: captured step graphs may still point at it
+    if (pl->adj_partial) pl->retired.push_back(pl->adj_partial);
     pl->adj_partial = nullptr;
     pl->adj_partial_len = 0;
     int rc = cuda_check(cudaMalloc(&pl->adj_partial, need * sizeof(float)), "cudaMalloc partial");
@@ -707,11 +692,11 @@ int imask_plan_create_list(int side, int n_angles, int n_det, int n_loc, const i
     imask_plan_destroy(pl);
     return rc;
   }
-  if ((rc = cuda_check(make_stream(&pl->aux.stream, prio_mode() == 1),
+  if ((rc = cuda_check(cudaStreamCreateWithFlags(&pl->aux.stream, cudaStreamNonBlocking),
                        "side stream")) ||
       (rc = cuda_check(cudaEventCreateWithFlags(&pl->aux.fork, cudaEventDisableTiming), "event")) ||
       (rc = cuda_check(cudaEventCreateWithFlags(&pl->aux.join, cudaEventDisableTiming), "event")) ||
-      (rc = cuda_check(make_stream(&pl->aux2.stream, prio_mode() == 1),
+      (rc = cuda_check(cudaStreamCreateWithFlags(&pl->aux2.stream, cudaStreamNonBlocking),
                        "side stream")) ||
       (rc = cuda_check(cudaEventCreateWithFlags(&pl->aux2.fork, cudaEventDisableTiming), "event")) ||
       (rc = cuda_check(cudaEventCreateWithFlags(&pl->aux2.join, cudaEventDisableTiming), "event")) ||
@@ -747,6 +732,7 @@ int imask_plan_destroy(imask_plan* pl) {
   cudaFree(pl->u);
   cudaFree(pl->sino_tmp);
   cudaFree(pl->adj_partial);
+  for (float* p : pl->retired) cudaFree(p);
   if (pl->aux.stream) cudaStreamDestroy(pl->aux.stream);
   if (pl->aux.fork) cudaEventDestroy(pl->aux.fork);
   if (pl->aux.join) cudaEventDestroy(pl->aux.join);
@@ -1103,7 +1089,7 @@ int capture_step(imask_plan* pl, const imask_state* st, int level0, const imask_
                  cudaGraph_t* graph, int* launches) {
   cudaStream_t s;
   int rc;
-  if ((rc = cuda_check(make_stream(&s, prio_mode() == 2), "stream create")))
+  if ((rc = cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream create")))
     return rc;
   *graph = nullptr;
   rc = cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
@@ -1136,7 +1122,7 @@ int imask_step_graph_create(imask_plan* pl, const imask_state* st, int level0,
   gr->device = pl->device;
   int n_launch = 0;
   rc = capture_step(pl, st, level0, prm, &gr->graph, &n_launch);
-  if (!rc) rc = cuda_check(cudaGraphInstantiate(&gr->exec, gr->graph, graph_flags()), "graph instantiate");
+  if (!rc) rc = cuda_check(cudaGraphInstantiate(&gr->exec, gr->graph, 0), "graph instantiate");
   if (rc) {
     imask_graph_destroy(gr);
     return rc;
@@ -1161,7 +1147,7 @@ int imask_step_graph_update(imask_graph* gr, imask_plan* pl, const imask_state* 
   if (cudaGraphExecUpdate(gr->exec, fresh, &info) != cudaSuccess) {
     cudaGetLastError();  // clear the update failure; instantiate afresh
     cudaGraphExec_t exec = nullptr;
-    rc = cuda_check(cudaGraphInstantiate(&exec, fresh, graph_flags()), "graph instantiate");
+    rc = cuda_check(cudaGraphInstantiate(&exec, fresh, 0), "graph instantiate");
     if (rc) {
       cudaGraphDestroy(fresh);
       return rc;

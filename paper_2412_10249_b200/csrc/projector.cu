@@ -134,7 +134,7 @@ k_forward(const float2* __restrict__ P, const float2* __restrict__ PT, int n, in
 // angle 0 is traced alone (its tie rule is not mirror-invariant) and so is
 // the self-mirrored angle n/2.
 template <bool kSaga>
-__global__ void __launch_bounds__(256, 8)
+__global__ void __launch_bounds__(256, 6)  // (256, 8) caps it at 32 registers and spills
 k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
               const float2* __restrict__ PM, const float2* __restrict__ PTM, int n, int pitch,
               const FwdAngle* __restrict__ ang, const int2* __restrict__ entries, int n_entries,
@@ -1150,7 +1150,7 @@ void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_o
       if (*q) ++q;
     }
   }
-  const int target = per_sm * 148;
+  const int target = per_sm * sm_count();
   int S = (target + tiles - 1) / tiles;
   const int max_s = n_loc / 8 > 1 ? n_loc / 8 : 1;
   if (S > max_s) S = max_s;

@@ -69,6 +69,11 @@ def draw_level(seed: int, k: int, cum_probs: np.ndarray) -> int:
     return int(draw_levels(seed, k, 1, cum_probs)[0])
 
 
+def _prm_key(prm) -> tuple:
+    """All fields of an ImaskStepParams (what a captured step graph bakes in)."""
+    return tuple(getattr(prm, name) for name, _ in prm._fields_)
+
+
 @dataclass(frozen=True)
 class Shard:
     """This rank's angle shard (ctmodel.shard_angles) and the process group the
@@ -117,7 +122,9 @@ class Engine:
         A graph is only launched after its pointers were checked against the
         state's, so it never holds the state alive.
         """
-        key = (level0, prm.sigma, prm.mu, prm.mu_g, prm.g_kind, state.parity)
+        # every scalar the capture bakes in is part of the key (the TV weight,
+        # inner iterations, tolerance and scratch pointer included)
+        key = (level0, state.parity, _prm_key(prm))
         cst = state.c_state(self.b)
         ptrs = tuple(getattr(cst, name) for name, _ in cst._fields_)
         hit = self._graphs.get(key)
@@ -143,7 +150,7 @@ class Engine:
         step scalars, dual-buffer parity, buffers), so a multi-GPU step is one
         host launch like the single-GPU one (NCCL collectives are capturable)."""
         cst = state.c_state(self.b)
-        key = ("sharded", level0, prm.sigma, prm.mu, prm.mu_g, prm.g_kind, state.parity,
+        key = ("sharded", level0, state.parity, _prm_key(prm),
                tuple(getattr(cst, name) for name, _ in cst._fields_))
         hit = self._sharded.get(key)
         if hit is None:
