@@ -140,6 +140,23 @@ def _shard_quads(n_angles: int, rank: int, world: int) -> tuple:
     return tuple(([0] if rank == 0 else []) + low + mirrors)
 
 
+def quad_subset(n_angles: int, bases: Sequence[int]) -> tuple:
+    """A sparse-view angle subset closed under the mirror a -> n - a and the
+    transpose a -> n/2 - a (so the plan runs the four-ray forward and the
+    mirror-symmetric adjoint): the quads {a, n/2-a, n/2+a, n-a} of the base
+    angles 0 < a < n/4, plus 0, n/4, n/2 and 3n/4. Rows in the layout
+    imask_plan_create_list recognises: [0] + low angles ascending + mirrors."""
+    if n_angles % 4 != 0 or n_angles < 8:
+        raise ValueError("quad subsets need n_angles divisible by 4 (and >= 8)")
+    h, q = n_angles // 2, n_angles // 4
+    bases = {int(a) for a in bases}
+    if any(not 0 < a < q for a in bases):
+        raise ValueError(f"base angles must lie in (0, {q})")
+    low = sorted(bases | {h - a for a in bases} | {q, h})
+    mirrors = sorted(n_angles - a for a in low if a != h)
+    return tuple([0] + low + mirrors)
+
+
 def _stream_ptr(device: torch.device) -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
@@ -332,35 +349,90 @@ def _projector_linop(geom: Geometry, factor: int, scale: float = 1.0, angles=Non
     )
 
 
+class _WidthProjector:
+    """K of a grid of ``side`` pixels of width h = p/q, q = 2^k <= 64 (any
+    multiple of 1/64; ctmodel.py:73-154 with
+    pixel_width h), evaluated exactly by the unit-offset kernels through two
+    identities of the chord matrix:
+      ray_matrix(N, p/q, th, t) = (1/q) ray_matrix(N, p, th, q t)   (scale by q)
+    and the offsets q t_j = q j - q (n-1)/2 are every q-th offset of a detector
+    row of n' = q (n-1) + 1 unit-spaced bins. A grid of N pixels of width p is
+    level factor p of the N p side plan, so the projection is that plan's
+    factor-p projection of n' bins, every q-th bin kept, scaled by 1/q; the
+    adjoint spreads the sinogram onto every q-th bin (zeros between) and
+    backprojects. h = 1 is the plain plan (p = q = 1). The denominator is a
+    power of two, so q t and the gridlines scale exactly in binary floating
+    point and the reference's half-open tie rule picks the same pixels (with
+    q = 3 it would not: ray_matrix itself decides those ties by rounding)."""
+
+    MAX_DEN = 64
+
+    def __init__(self, geom: Geometry, pixel_width: float):
+        from fractions import Fraction
+
+        h = float(pixel_width)
+        if not h > 0.0 or not math.isfinite(h):
+            raise ValueError("pixel_width must be positive")
+        fr = Fraction(h)  # exact: a binary64 value is p / 2^k
+        if fr.denominator > self.MAX_DEN:
+            raise ValueError(f"pixel_width {h!r} is not a multiple of 1/{self.MAX_DEN}")
+        self.geom, self.p, self.q = geom, fr.numerator, fr.denominator
+        self.n_wide = self.q * (geom.n_detectors - 1) + 1
+        self.wide = Geometry(geom.side * self.p, geom.n_angles, self.n_wide)
+
+    def _plan(self) -> "Plan":
+        return get_plan(self.wide, scale=1.0 / self.q)
+
+    def project(self, x: torch.Tensor) -> torch.Tensor:
+        g = self.geom
+        full = self._plan().project(x, self.p)
+        if self.q == 1:
+            return full
+        return full.reshape(g.n_angles, self.n_wide)[:, ::self.q].contiguous().reshape(-1)
+
+    def backproject(self, y: torch.Tensor) -> torch.Tensor:
+        g = self.geom
+        if self.q > 1:
+            wide = torch.zeros(g.n_angles, self.n_wide, device=y.device, dtype=torch.float32)
+            wide[:, ::self.q] = y.reshape(g.n_angles, g.n_detectors)
+            y = wide.reshape(-1)
+        return self._plan().backproject(y, self.p)
+
+
 def project(geom: Geometry, x, pixel_width: float = 1.0) -> torch.Tensor:
-    """(n_angles, n_detectors) sinogram of an image (ctmodel.py:170-176)."""
-    if pixel_width != 1.0:
-        raise NotImplementedError("only unit pixel width is on the B200 path")
+    """(n_angles, n_detectors) sinogram of an image (ctmodel.py:170-176); any
+    pixel width that is a multiple of 1/64, through _WidthProjector."""
     t = to_device(x)
     if t.numel() != geom.side * geom.side:
         raise ValueError(f"image has {t.numel()} pixels, geometry expects {geom.side}^2")
-    return get_plan(geom).project(t, 1).reshape(geom.n_angles, geom.n_detectors)
+    return _WidthProjector(geom, pixel_width).project(t).reshape(geom.n_angles, geom.n_detectors)
 
 
 def backproject(geom: Geometry, y, pixel_width: float = 1.0) -> torch.Tensor:
     """Exact adjoint of project; (side, side) image (ctmodel.py:179-185)."""
-    if pixel_width != 1.0:
-        raise NotImplementedError("only unit pixel width is on the B200 path")
     t = to_device(y)
     if t.numel() != geom.m:
         raise ValueError(f"sinogram has {t.numel()} bins, geometry expects {geom.m}")
-    return get_plan(geom).backproject(t, 1).reshape(geom.side, geom.side)
+    return _WidthProjector(geom, pixel_width).backproject(t).reshape(geom.side, geom.side)
 
 
-def projector_op(geom: Geometry, pixel_width: float = 1.0) -> LinOp:
-    """Full-resolution forward model as a flat LinOp (ctmodel.py:188-191)."""
-    if pixel_width != 1.0:
-        raise NotImplementedError("only unit pixel width is on the B200 path")
-    return _projector_linop(geom, 1)
+def projector_op(geom: Geometry, pixel_width: float = 1.0, angles=None) -> LinOp:
+    """Full-resolution forward model as a flat LinOp (ctmodel.py:188-191).
+
+    ``angles`` (extension): global indices of the rows to keep, in row order
+    (e.g. ``quad_subset`` for a sparse-view scan); all angles by default.
+    """
+    if float(pixel_width) != 1.0:
+        if angles is not None:
+            raise ValueError("angle subsets take the unit pixel width")
+        wp = _WidthProjector(geom, pixel_width)
+        return LinOp(geom.side * geom.side, geom.m, lambda x: wp.project(to_device(x)),
+                     lambda y: wp.backproject(to_device(y)))
+    return _projector_linop(geom, 1, angles=angles)
 
 
-def coarse_projector(geom: Geometry, factor: int) -> LinOp:
+def coarse_projector(geom: Geometry, factor: int, angles=None) -> LinOp:
     """Forward model on the grid coarsened by ``factor`` (ctmodel.py:194-204)."""
     if geom.side % factor != 0:
         raise ValueError(f"side {geom.side} not divisible by factor {factor}")
-    return _projector_linop(geom, factor)
+    return _projector_linop(geom, factor, angles=angles)

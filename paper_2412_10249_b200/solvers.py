@@ -112,6 +112,7 @@ class Engine:
         self._comm_ready = False
         self.use_graphs = True
         self.graph_updates = 0  # re-targets of cached step graphs to another state's buffers
+        self.tv = None  # (mu, inner_iters, inner_tol) when g is TV + nonnegativity
 
     def graph(self, state: "SaddleState", level0: int, prm) -> tuple:
         """(graph handle, kernels per replay) of one step at ``level0`` on ``state``.
@@ -187,7 +188,7 @@ class Engine:
 
     def params(self, sigma: float, mu: float) -> _lib.ImaskStepParams:
         """Step scalars for this engine's g (ridge or TV + nonnegativity)."""
-        tv = getattr(self, "tv", None)
+        tv = self.tv
         if tv is None:
             return _params(sigma, mu, self.mu_g)
         if sigma <= 0:
@@ -342,20 +343,19 @@ class SaddleState:
             self.parity ^= 1
 
 
-def _require_engine(prob: Problem) -> Engine:
-    if prob.engine is None:
-        raise TypeError(
-            "the B200 sketch_step needs a coarse-mode problem built by make_problem from this "
-            "package's projector_op / coarse_projector, with ridge g and the quadratic-data "
-            "conjugate f*"
-        )
-    return prob.engine
-
-
 def init_state(prob: Problem, seed: int = 0, x0=None, y0=None, exact_memory: bool = False,
+               sum_weights=None, ops: Optional[Sequence[LinOp]] = None,
                resum_every: int = 1000) -> SaddleState:
-    """Fresh device state: zero start with zero memory unless told otherwise (solvers.py:143-181)."""
-    eng = _require_engine(prob)
+    """Fresh device state: zero start with zero memory unless told otherwise (solvers.py:143-181).
+
+    A problem the fused engine runs gets the engine's layout (compact coarse
+    phi rows in one table, a second dual buffer); any other problem, or an
+    explicit ``ops`` / ``sum_weights``, gets the reference layout: one
+    full-length device row per operator (the generic device path).
+    """
+    if prob.engine is None or ops is not None or sum_weights is not None:
+        return _init_generic(prob, seed, x0, y0, exact_memory, sum_weights, ops, resum_every)
+    eng = prob.engine
     dev = eng.device
     d, m, r = eng.d, eng.m_loc, prob.r
     x = torch.zeros(d, device=dev) if x0 is None else to_device(x0, dev).clone()
@@ -395,9 +395,67 @@ def _allreduce(eng: Engine, t: torch.Tensor, async_op: bool = False):
     return dist.all_reduce(t, op=dist.ReduceOp.SUM, group=eng.shard.group, async_op=async_op)
 
 
+def _init_generic(prob: Problem, seed, x0, y0, exact_memory, sum_weights, ops,
+                  resum_every) -> SaddleState:
+    """init_state in the reference layout (solvers.py:143-181) on device tensors."""
+    ops = list(ops if ops is not None else prob.ops)
+    dev = prob.b.device
+    d, m = ops[0].domain_dim, ops[0].range_dim
+    x = torch.zeros(d, device=dev) if x0 is None else to_device(x0, dev).clone()
+    y = torch.zeros(m, device=dev) if y0 is None else to_device(y0, dev).clone()
+    weights = prob.probs if sum_weights is None else np.asarray(sum_weights, dtype=float)
+    if exact_memory:
+        phi = [to_device(op.adjoint_apply(y), dev).clone() for op in ops]
+        psi = [to_device(op.apply(x), dev).clone() for op in ops]
+        phi_sum = float(weights[0]) * phi[0]
+        psi_sum = float(weights[0]) * psi[0]
+        for i in range(1, len(ops)):
+            phi_sum = phi_sum + float(weights[i]) * phi[i]
+            psi_sum = psi_sum + float(weights[i]) * psi[i]
+    else:
+        phi = [torch.zeros(d, device=dev) for _ in ops]
+        psi = [torch.zeros(m, device=dev) for _ in ops]
+        phi_sum = torch.zeros(d, device=dev)
+        psi_sum = torch.zeros(m, device=dev)
+    return SaddleState(x=x, y=y, phi=phi, psi=psi, phi_sum=phi_sum, psi_sum=psi_sum, seed=seed,
+                       xbar=x.clone(), resum_every=resum_every)
+
+
+def _resum_weights(state: SaddleState, weights) -> None:
+    """_resum (solvers.py:184-191) on reference-layout device rows, index order."""
+    phi_sum = float(weights[0]) * state.phi[0]
+    psi_sum = float(weights[0]) * state.psi[0]
+    for i in range(1, len(state.phi)):
+        phi_sum = phi_sum + float(weights[i]) * state.phi[i]
+        psi_sum = psi_sum + float(weights[i]) * state.psi[i]
+    state.phi_sum = phi_sum
+    state.psi_sum = psi_sum
+
+
+def _fused(prob: Problem, state: SaddleState) -> bool:
+    """The fused engine runs this (problem, state) pair."""
+    return prob.engine is not None and state.phi_tab is not None
+
+
+def _to_generic(state: SaddleState, family: Optional[SketchFamily]) -> None:
+    """Convert an engine-layout state to the reference layout in place (full
+    phi rows, single dual buffer), for the generic steps."""
+    if state.phi_tab is None:
+        return
+    state.phi = [state.phi_full(i, family).clone() for i in range(len(state.phi))]
+    state.psi = [p.clone() for p in state.psi]
+    state.phi_sum = state.phi_sum.clone()
+    state.psi_sum = state.psi_sum.clone()
+    state.phi_tab = state.psi_tab = state.bp = state.y_alt = None
+    state._cstates.clear()
+
+
 def _resum(state: SaddleState, prob: Problem) -> None:
     """Recompute phi_sum / psi_sum from the tables in index order (solvers.py:184-191)."""
-    eng = _require_engine(prob)
+    if not _fused(prob, state):
+        _resum_weights(state, prob.probs)
+        return
+    eng = prob.engine
     _lib.check(_lib.lib().imask_resum(eng.plan.handle, ctypes.byref(state.c_state(eng.b)),
                                       eng.plan.stream))
 
@@ -469,16 +527,72 @@ def _sharded_step_eager(eng: Engine, state: SaddleState, level0: int, prm,
     return launches + _lib.last_launch_count()
 
 
-def sketch_step(state: SaddleState, prob: Problem, sigma: float, mu: float) -> SaddleState:
-    """One parallel-update sketched iteration (solvers.py:194-221), on the device."""
-    eng = _require_engine(prob)
-    i = draw_level(state.seed, state.k, prob.cum_probs)
-    _device_step(eng, state, i, eng.params(sigma, mu))
+def _generic_sketch_step(state: SaddleState, prob: Problem, i: int, sigma: float,
+                         mu: float) -> None:
+    """sketch_step's update (solvers.py:203-215) with the problem's LinOp and
+    ProxFn callables on device tensors: any operator family (exact mode
+    compose(K, S_i), dense or sparse matrices) and any prox."""
+    op = prob.ops[i]
+    phi_new = to_device(op.adjoint_apply(state.y), state.x.device)
+    psi_new = to_device(op.apply(state.x), state.x.device)
+    xi = (phi_new - state.phi[i]) + state.phi_sum
+    zeta = (psi_new - state.psi[i]) + state.psi_sum
+    p_i = float(prob.probs[i])
+    state.phi_sum = state.phi_sum + p_i * (phi_new - state.phi[i])
+    state.psi_sum = state.psi_sum + p_i * (psi_new - state.psi[i])
+    state.phi[i] = phi_new
+    state.psi[i] = psi_new
+    s = sigma / mu
+    state.x = to_device(prob.g.prox(state.x - s * xi, s), state.x.device)
+    state.y = to_device(prob.f_conj.prox(state.y + sigma * zeta, sigma), state.x.device)
+
+
+def _generic_seq_step(state: SaddleState, prob: Problem, i: int, sigma: float, mu: float,
+                      theta_extrap: float) -> None:
+    """sketch_seq_step's update (solvers.py:278-298) on device tensors."""
+    dev = state.x.device
+    op = prob.ops[i]
+    p_i = float(prob.probs[i])
+    psi_new = to_device(op.apply(state.xbar), dev)
+    zeta = (psi_new - state.psi[i]) + state.psi_sum
+    state.psi_sum = state.psi_sum + p_i * (psi_new - state.psi[i])
+    state.psi[i] = psi_new
+    y_new = to_device(prob.f_conj.prox(state.y + sigma * zeta, sigma), dev)
+    phi_new = to_device(op.adjoint_apply(y_new), dev)
+    xi = (phi_new - state.phi[i]) + state.phi_sum
+    state.phi_sum = state.phi_sum + p_i * (phi_new - state.phi[i])
+    state.phi[i] = phi_new
+    s = sigma / mu
+    x_new = to_device(prob.g.prox(state.x - s * xi, s), dev)
+    state.xbar = x_new if theta_extrap == 0.0 else x_new + theta_extrap * (x_new - state.x)
+    state.x = x_new
+    state.y = y_new
+
+
+def _advance(state: SaddleState, prob: Problem, i: int) -> None:
+    """Host bookkeeping shared by every step: counter, cost ledger, resum cadence."""
     state.k += 1
     state.cost += 2.0 * prob.fractions[i]
     state.last_level = i + 1
     if state.k % state.resum_every == 0:
         _resum(state, prob)
+
+
+def sketch_step(state: SaddleState, prob: Problem, sigma: float, mu: float) -> SaddleState:
+    """One parallel-update sketched iteration (solvers.py:194-221), on the device.
+
+    The fused engine (one CUDA graph) runs coarse-mode problems built from this
+    package's projectors with the ridge or TV g and the quadratic-data f*;
+    every other problem runs the same update through its own LinOp / ProxFn
+    callables on device tensors."""
+    i = draw_level(state.seed, state.k, prob.cum_probs)
+    if not _fused(prob, state):
+        _generic_sketch_step(state, prob, i, sigma, mu)
+        _advance(state, prob, i)
+        return state
+    eng = prob.engine
+    _device_step(eng, state, i, eng.params(sigma, mu))
+    _advance(state, prob, i)
     return state
 
 
@@ -490,19 +604,67 @@ def sketch_seq_step(state: SaddleState, prob: Problem, sigma: float, mu: float,
     the primal step and the extrapolation (one native call, imask_seq_step)."""
     if not 0.0 <= theta_extrap <= 1.0:
         raise ValueError("theta_extrap must lie in [0, 1]")
-    eng = _require_engine(prob)
+    i = draw_level(state.seed, state.k, prob.cum_probs)
+    if not _fused(prob, state) or prob.engine.tv is not None:
+        _to_generic(state, prob.engine.family if prob.engine is not None else None)
+        _generic_seq_step(state, prob, i, sigma, mu, theta_extrap)
+        _advance(state, prob, i)
+        return state
+    eng = prob.engine
     if eng.shard.world > 1:
         raise NotImplementedError("sketch_seq_step runs on one GPU")
-    i = draw_level(state.seed, state.k, prob.cum_probs)
     _lib.check(_lib.lib().imask_seq_step(
         eng.plan.handle, ctypes.byref(state.c_state(eng.b)), i,
         ctypes.byref(eng.params(sigma, mu)), float(theta_extrap), eng.plan.stream))
+    _advance(state, prob, i)
+    return state
+
+
+def saga_saddle_step(state: SaddleState, ops: Sequence[LinOp], probs, g: ProxFn,
+                     f_conj: ProxFn, sigma_x: float, sigma_y: float, cum_probs=None,
+                     fractions=None) -> SaddleState:
+    """One saddle-point SAGA iteration for blocks A_i with sum_i A_i = A
+    (solvers.py:224-263), on device tensors: memory rows hold A_i products, the
+    estimates carry the 1/p_i correction and the unweighted memory sums, and
+    the resum uses unit weights. With A_i = p_i K_i, sigma_x = sigma/mu and
+    sigma_y = sigma this reproduces sketch_step.
+
+    A state from init_state of a fused-engine problem is converted to the
+    reference layout (full-length rows) on first use."""
+    probs = np.asarray(probs, dtype=float)
+    cum = np.cumsum(probs) if cum_probs is None else np.asarray(cum_probs, dtype=float)
+    if state.phi_tab is not None:
+        _to_generic(state, _family_of(ops))
+    i = draw_level(state.seed, state.k, cum)
+    dev = state.x.device
+    op = ops[i]
+    phi_new = to_device(op.adjoint_apply(state.y), dev)
+    psi_new = to_device(op.apply(state.x), dev)
+    inv_p = 1.0 / float(probs[i])
+    xi = (phi_new - state.phi[i]) * inv_p + state.phi_sum
+    zeta = (psi_new - state.psi[i]) * inv_p + state.psi_sum
+    state.phi_sum = state.phi_sum + (phi_new - state.phi[i])
+    state.psi_sum = state.psi_sum + (psi_new - state.psi[i])
+    state.phi[i] = phi_new
+    state.psi[i] = psi_new
+    state.x = to_device(g.prox(state.x - sigma_x * xi, sigma_x), dev)
+    state.y = to_device(f_conj.prox(state.y + sigma_y * zeta, sigma_y), dev)
     state.k += 1
-    state.cost += 2.0 * prob.fractions[i]
+    state.cost += 2.0 * float(fractions[i]) if fractions is not None else 2.0
     state.last_level = i + 1
     if state.k % state.resum_every == 0:
-        _resum(state, prob)
+        _resum_weights(state, np.ones(len(ops)))
     return state
+
+
+def _family_of(ops) -> SketchFamily:
+    """Sketch family behind an engine-layout state's compact rows."""
+    for op in ops:
+        fam = getattr(getattr(op, "meta", None), "family", None)
+        if fam is not None:
+            return fam
+    raise TypeError("saga_saddle_step: an engine-layout state needs sketched operators "
+                    "(or a state from init_state(prob, ops=...))")
 
 
 def psnr(x: torch.Tensor, ref: torch.Tensor, peak: float = 1.0) -> float:
@@ -714,41 +876,57 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
         return _run_pdhg(prob, mu, iters, record_every, seed, x_ref, snapshot_costs)
     if algorithm == "sketch-seq" and not 0.0 <= theta_extrap <= 1.0:
         raise ValueError("theta_extrap must lie in [0, 1]")
+    saga_ops = None
     if algorithm == "saga-saddle":
-        # A_i = p_i K_i with sigma_x = sigma/mu, sigma_y = sigma reproduces the
-        # sketched parallel step (solvers.py:233-237); the blocks must sum to K
-        # (solvers.py:463-467, checked here in float32)
-        gap = verify_decomposition(prob)
-        if gap > 1e-5:
+        # blocks A_i = p_i K_i must sum to K (solvers.py:458-467; float32 bound)
+        from .linops import scale as _scale
+
+        saga_ops = [_scale(prob.ops[i], float(prob.probs[i])) for i in range(prob.r)]
+        gap = verify_decomposition(prob.K, saga_ops, trials=1, seed=0)
+        if gap > DECOMPOSITION_TOL:
             raise ValueError(f"operator blocks do not sum to the full map (gap {gap:.2e})")
-    eng = _require_engine(prob)
-    x_ref_t = None if x_ref is None else to_device(x_ref, eng.device)
+    seq = algorithm == "sketch-seq"
+    eng = prob.engine
+    # the fused engine runs the parallel step and, with the ridge g, the
+    # sequential one; saga-saddle with A_i = p_i K_i, sigma_x = sigma/mu and
+    # sigma_y = sigma is the parallel step (solvers.py:233-237)
+    fused = eng is not None and not (seq and eng.tv is not None)
+    dev = eng.device if eng is not None else prob.b.device
+    x_ref_t = None if x_ref is None else to_device(x_ref, dev)
     t0 = time.perf_counter()
     snapshots: dict = {}
     budgets = sorted(float(cb) for cb in snapshot_costs)
     state = init_state(prob, seed=seed, resum_every=resum_every)
-    prm = eng.params(sigma, mu)
+    if not fused:
+        _to_generic(state, eng.family if eng is not None else None)
+    prm = eng.params(sigma, mu) if fused else None
     schedule = draw_levels(seed, 0, iters, prob.cum_probs)
 
     n_rows = 2 + iters // max(record_every, 1)
-    rec = _Recorder(x_ref_t, eng.device, n_rows, t0)
+    rec = _Recorder(x_ref_t, dev, n_rows, t0)
     record = rec.record
 
     record(0, 0.0, 0, state.x)
-    seq = algorithm == "sketch-seq"
     for k in range(1, iters + 1):
         i = int(schedule[k - 1])
-        if seq:
-            _lib.check(_lib.lib().imask_seq_step(
-                eng.plan.handle, ctypes.byref(state.c_state(eng.b)), i, ctypes.byref(prm),
-                float(theta_extrap), eng.plan.stream))
+        if not fused:
+            if saga_ops is not None:
+                saga_saddle_step(state, saga_ops, prob.probs, prob.g, prob.f_conj, sigma / mu,
+                                 sigma, cum_probs=prob.cum_probs, fractions=prob.fractions)
+            else:
+                if seq:
+                    _generic_seq_step(state, prob, i, sigma, mu, theta_extrap)
+                else:
+                    _generic_sketch_step(state, prob, i, sigma, mu)
+                _advance(state, prob, i)
         else:
-            _device_step(eng, state, i, prm)
-        state.k += 1
-        state.cost += 2.0 * prob.fractions[i]
-        state.last_level = i + 1
-        if state.k % state.resum_every == 0:
-            _resum(state, prob)
+            if seq:
+                _lib.check(_lib.lib().imask_seq_step(
+                    eng.plan.handle, ctypes.byref(state.c_state(eng.b)), i, ctypes.byref(prm),
+                    float(theta_extrap), eng.plan.stream))
+            else:
+                _device_step(eng, state, i, prm)
+            _advance(state, prob, i)
         while budgets and state.cost >= budgets[0]:
             snapshots[budgets.pop(0)] = state.x.clone()
         if k % record_every == 0 or k == iters:
@@ -758,18 +936,24 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
                        snapshots=snapshots)
 
 
-def verify_decomposition(prob: Problem, trials: int = 1, seed: int = 0) -> float:
-    """max relative gap of sum_i p_i K_i x against K x over random x
-    (the check run() makes for saga-saddle, solvers.py:463-467)."""
+# float32 counterpart of run()'s 1e-8 gap bound (solvers.py:465-467): the blocks
+# are applied in float32 (rounding ~1e-7 relative per product)
+DECOMPOSITION_TOL = 1e-5
+
+
+def verify_decomposition(A: LinOp, blocks: Sequence[LinOp], trials: int = 3, seed: int = 0) -> float:
+    """Max relative gap of sum_i A_i x vs A x over seeded random probes
+    (solvers.py:105-116), with the products reduced in float64."""
     gen = np.random.default_rng(seed)
     worst = 0.0
     for _ in range(trials):
-        x = to_device(gen.standard_normal(prob.K.domain_dim))
-        full = prob.K.apply(x).double()
-        acc = torch.zeros_like(full)
-        for p_i, op in zip(prob.probs, prob.ops):
-            acc += float(p_i) * op.apply(x).double()
-        worst = max(worst, float(torch.linalg.norm(acc - full) / torch.linalg.norm(full)))
+        x = gen.standard_normal(A.domain_dim)
+        xd = to_device(x)
+        ax = to_device(A.apply(xd), xd.device).double()
+        sx = to_device(blocks[0].apply(xd), xd.device).double()
+        for blk in blocks[1:]:
+            sx = sx + to_device(blk.apply(xd), xd.device).double()
+        worst = max(worst, float(torch.linalg.norm(sx - ax)) / (float(torch.linalg.norm(ax)) + 1e-30))
     return worst
 
 

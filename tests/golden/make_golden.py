@@ -25,6 +25,24 @@ Fixtures:
   solver_A.npz sketch_step trajectory on config A (coarse mode, ridge
                mu_g = 1e-2, sigma = 3e-5, mu = mu_g): x, y, sums after
                18 iterations (= 20 epochs) and after 200 iterations
+  solver_A_long.npz  config A, 1100 iterations at sigma = 1e-5 (stable; a
+               1e-7 perturbation of b grows to ~3e-7 by k = 1100): x, y,
+               sums at k = 999, 1000 (after the resum of solvers.py:219-220)
+               and 1100
+  solver_C.npz sketch_step on config C (512^2 / 720 / 725, r = 5, uniform
+               probs, sigma = 2.5e-6): x, y after 26 and 52 iterations
+               (52 = 40 epochs); b is rounded to float32 before the run, so
+               both sides see identical data
+  solver_D_subset.npz  sketch_step at the D grid (1024^2, 6 levels, 1449
+               bins) on a quad-closed subset of 64 of the 1440 angles (rows
+               in the layout ctmodel.quad_subset returns): the reference
+               solver on LinOps built from ray_matrix on those rows, 77
+               iterations (= 50 epochs), sigma = 5e-6
+  proj_C_sampled.npz / proj_E_sampled.npz  configs C and E on sampled
+               angles (incl. theta = 0, pi/4, pi/2 and their neighbours) at
+               every level factor: forward rows of the decimated phantom and
+               the adjoint of a seeded sinogram on those rows (at 4096 sampled
+               pixels on fine grids, whole images on coarse ones)
 """
 
 from __future__ import annotations
@@ -165,6 +183,177 @@ def gen_solver_A():
             out[f"cost_{k}"] = st.cost
     out["levels"] = np.array(levels, dtype=np.int8)
     save("solver_A.npz", **out)
+
+
+def _ref_problem(side, n_det, angles_rows, n_angles, b, r, mu_g):
+    """Reference coarse-mode ridge problem whose operators are ray_matrix on the
+    given angle rows (the reference's own Siddon matrices and solver)."""
+    from mrtomo import linops
+
+    g = ctmodel.Geometry(side, n_angles, n_det)
+    th = g.angles[np.asarray(angles_rows)]
+
+    def op(f):
+        mat = ctmodel.ray_matrix(side // f, float(f), th, g.offsets)
+        mt = mat.T.tocsr()
+        return linops.LinOp(mat.shape[1], mat.shape[0], lambda x, m=mat: m @ x,
+                            lambda y, m=mt: m @ y)
+
+    K = op(1)
+    fam = mrsketch.make_family(r, side, [1.0 / r] * r, mode="coarse")
+    prob = solvers.make_problem(K, b, fam, proxlib.ridge_fn(mu_g), proxlib.quadratic_conjugate_fn(b),
+                                coarse_projector=op)
+    return K, prob
+
+
+def _trajectory(prob, sigma, mu, seed, stops, extra=()):
+    st = solvers.init_state(prob, seed=seed)
+    out, levels = {}, []
+    for k in range(1, max(stops) + 1):
+        solvers.sketch_step(st, prob, sigma, mu)
+        levels.append(st.last_level)
+        if k in stops:
+            out[f"x_{k}"] = st.x.astype(np.float32)
+            out[f"y_{k}"] = st.y.astype(np.float32)
+            out[f"cost_{k}"] = st.cost
+            for name in extra:
+                out[f"{name}_{k}"] = getattr(st, name).astype(np.float32)
+    out["levels"] = np.array(levels, dtype=np.int8)
+    return out
+
+
+def gen_solver_A_long():
+    cfg = CONFIGS["A"]
+    g = ctmodel.Geometry(cfg.side, cfg.n_angles, cfg.n_det)
+    K = ctmodel.projector_op(g)
+    b = add_gaussian_noise(K.apply(ellipse_phantom(cfg.side, 0).ravel()), cfg.kappa, 1)
+    b = b.astype(np.float32).astype(float)
+    fam = mrsketch.make_family(3, cfg.side, [1.0 / 3] * 3, mode="coarse")
+    prob = solvers.make_problem(K, b, fam, proxlib.ridge_fn(cfg.mu_g),
+                                proxlib.quadratic_conjugate_fn(b),
+                                coarse_projector=lambda f: ctmodel.coarse_projector(g, f))
+    out = _trajectory(prob, 1e-5, cfg.mu_g, 5, (999, 1000, 1100), ("phi_sum", "psi_sum"))
+    save("solver_A_long.npz", b=b.astype(np.float32), sigma=1e-5, mu=cfg.mu_g, seed=5, **out)
+
+
+def gen_solver_C():
+    cfg = CONFIGS["C"]
+    g = ctmodel.Geometry(cfg.side, cfg.n_angles, cfg.n_det)
+    K = ctmodel.projector_op(g)
+    b = add_gaussian_noise(K.apply(ellipse_phantom(cfg.side, 0).ravel()), cfg.kappa, 1)
+    b = b.astype(np.float32).astype(float)
+    fam = mrsketch.make_family(cfg.levels, cfg.side, [1.0 / cfg.levels] * cfg.levels,
+                               mode="coarse")
+    prob = solvers.make_problem(K, b, fam, proxlib.ridge_fn(cfg.mu_g),
+                                proxlib.quadratic_conjugate_fn(b),
+                                coarse_projector=lambda f: ctmodel.coarse_projector(g, f))
+    out = _trajectory(prob, 2.5e-6, cfg.mu_g, 17, (26, cfg.iters_for_epochs()))
+    save("solver_C.npz", b=b.astype(np.float32), sigma=2.5e-6, mu=cfg.mu_g, seed=17, **out)
+
+
+D_SUBSET_BASES = (1, 2, 5, 17, 44, 89, 120, 150, 179, 211, 250, 301, 333, 358, 359)
+
+
+def gen_solver_D_subset():
+    from paper_2412_10249_b200.ctmodel import quad_subset
+
+    cfg = CONFIGS["D"]
+    rows = quad_subset(cfg.n_angles, D_SUBSET_BASES)
+    assert len(rows) == 64
+    x_true = ellipse_phantom(cfg.side, 0).ravel()
+    g = ctmodel.Geometry(cfg.side, cfg.n_angles, cfg.n_det)
+    mat = ctmodel.ray_matrix(cfg.side, 1.0, g.angles[np.asarray(rows)], g.offsets)
+    b = add_gaussian_noise(mat @ x_true, cfg.kappa, 1).astype(np.float32).astype(float)
+    del mat
+    _, prob = _ref_problem(cfg.side, cfg.n_det, rows, cfg.n_angles, b, cfg.levels, cfg.mu_g)
+    out = _trajectory(prob, 5e-6, cfg.mu_g, 23, (cfg.iters_for_epochs(),))
+    save("solver_D_subset.npz", rows=np.asarray(rows), bases=np.asarray(D_SUBSET_BASES),
+         b=b.astype(np.float32), sigma=5e-6, mu=cfg.mu_g, seed=23, **out)
+
+
+def _proj_sampled(cfg, sel, name):
+    g = ctmodel.Geometry(cfg.side, cfg.n_angles, cfg.n_det)
+    x = ellipse_phantom(cfg.side, 0)
+    rng = np.random.default_rng(11)
+    ys = rng.standard_normal(len(sel) * g.n_detectors)
+    out = {"angles": np.asarray(sel), "y": ys.astype(np.float32)}
+    ysf = ys.astype(np.float32).astype(float)
+    for lv in range(cfg.levels):
+        f = 2 ** lv
+        low = cfg.side // f
+        mat = ctmodel.ray_matrix(low, float(f), g.angles[np.asarray(sel)], g.offsets)
+        xl = mrsketch.decimate(x, f).ravel() if f > 1 else x.ravel()
+        out[f"fwd_f{f}"] = mat @ xl
+        bp = mat.T @ ysf
+        if low * low > 65536:
+            pix = np.sort(rng.choice(low * low, size=4096, replace=False))
+            out[f"pix_f{f}"] = pix
+            out[f"adj_f{f}"] = bp[pix]
+        else:
+            out[f"adj_f{f}"] = bp
+        del mat
+    save(name, **out)
+
+
+def gen_proj_C_sampled():
+    _proj_sampled(CONFIGS["C"], [0, 1, 179, 180, 181, 359, 360, 361, 540, 719], "proj_C_sampled.npz")
+
+
+def gen_proj_E_sampled():
+    _proj_sampled(CONFIGS["E"], [0, 1, 511, 512, 1023, 1024, 1025, 1536, 2047],
+                  "proj_E_sampled.npz")
+
+
+def gen_proj_width():
+    """project / backproject with pixel_width != 1 (ctmodel.py:170-191)."""
+    out = {}
+    rng = np.random.default_rng(5)
+    cases = [(16, 20, 23, 0.5), (16, 20, 23, 1.5), (32, 36, 47, 2.0), (16, 24, 23, 0.25),
+             (24, 28, 35, 3.0), (16, 20, 22, 0.75)]
+    for idx, (side, na, nd, h) in enumerate(cases):
+        g = ctmodel.Geometry(side, na, nd)
+        x = rng.standard_normal(side * side)
+        y = rng.standard_normal(g.m)
+        out[f"c{idx}_meta"] = np.array([side, na, nd, h])
+        out[f"c{idx}_x"] = x
+        out[f"c{idx}_y"] = y
+        out[f"c{idx}_fwd"] = ctmodel.project(g, x.reshape(side, side), pixel_width=h).ravel()
+        out[f"c{idx}_adj"] = ctmodel.backproject(g, y.reshape(na, nd), pixel_width=h).ravel()
+    save("proj_width.npz", **out)
+
+
+RATE_CASES = ((1492.0, 861.3, 1492.0, 1 / 3), (2.0, 1.5, 3.0, 0.25), (5.0, 3.0, 6.0, 0.1),
+              (1.0, 1.0, 1.0, 1.0), (40.0, 10.0, 35.0, 0.2))
+
+
+def gen_rates():
+    """Step-size theory of rates.py:122-301 on fixed constants (scalar host math)."""
+    from mrtomo import rates
+
+    out = {"cases": np.array(RATE_CASES)}
+    for idx, (L, Lb, Lbp, mp) in enumerate(RATE_CASES):
+        rc = rates.RateConstants(L=L, Lbar=Lb, Lbar_p=Lbp, min_p=mp, mu_g=1.0, mu_fstar=1.0)
+        rows = []
+        c_bar = 1.0 / (1.0 + (L * 1.01) ** 2 + (Lbp * 1.01) ** 2)
+        for cf in (1e-3, 0.1, 0.5, 0.9):
+            for rho in (0.05, 0.5, 0.95):
+                pl = rates.plan_for(rc, cf * c_bar, rho)
+                lo, hi = rates.admissible_interval(pl)
+                rows.append([pl.a, pl.b, pl.c, pl.c_bar, pl.rho, pl.alpha, pl.eta_star,
+                             pl.sigma_star, pl.theta_star, lo, hi,
+                             float(pl.theta_of(0.5 * pl.eta_star))])
+        out[f"plans_{idx}"] = np.array(rows)
+        best = rates.optimal_step(rc)
+        free = rates.optimal_step(rc, rho=None, num_c=25, num_rho=20)
+        out[f"opt_{idx}"] = np.array([[p.c, p.rho, p.eta_star, p.sigma_star, p.theta_star]
+                                      for p in (best, free)])
+        grid = rates.step_plan_grid(rc, num_c=7, num_rho=5)
+        out[f"grid_{idx}"] = np.array([[p.c, p.rho, p.theta_star] for p in grid])
+        out[f"base_{idx}"] = np.array([rates.sigma_baseline(L, Lb)])
+        out[f"unnorm_{idx}"] = np.array([rates.theta_unnormalized(s, mu, L, Lbp, Lb, mp, a, b)
+                                         for s, mu, a, b in ((1e-3, 1.0, 2.0, 0.5),
+                                                             (0.2, 0.1, 0.7, 3.0))])
+    save("rates.npz", **out)
 
 
 def gen_tv():

@@ -1,0 +1,151 @@
+"""Parity at the large BASELINE configurations, against fixtures the REFERENCE
+produced (tests/golden/make_golden.py imports /root/reference).
+
+- Projections at configs C (512^2 / 720 / 725) and E (2048^2 / 2048 / 2897)
+  on sampled angles (theta = 0, pi/4, pi/2, 3pi/4 and their neighbours) at
+  every level factor, forward and adjoint (ctmodel.py:73-154,194-204);
+  budget 1e-4 relative L2 per level.
+- pixel_width != 1 (ctmodel.py:170-191).
+- sketch_step iterates (solvers.py:194-221; budget 1e-3 relative L2) on
+  config C (40 epochs), on the 1024^2 / 6-level grid of config D restricted
+  to a quad-closed subset of 64 angles (50 epochs; the reference solver on
+  ray_matrix of those rows), and on config A over 1100 iterations, across the
+  resum of the memory sums at k = 1000 (solvers.py:219-220).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden, rel_l2
+from oracle import sketch_oracle
+from paper_2412_10249_b200 import ctmodel, mrsketch, proxlib, solvers
+from paper_2412_10249_b200.synth import CONFIGS, ellipse_phantom
+
+pytestmark = pytest.mark.gpu
+TOL_PROJ = 1e-4
+TOL_ITER = 1e-3
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.double().cpu().numpy().ravel()
+
+
+def _sampled_levels(cfg, g):
+    geom = ctmodel.Geometry(cfg.side, cfg.n_angles, cfg.n_det)
+    sel = g["angles"].astype(np.int64)
+    x = ellipse_phantom(cfg.side, 0)
+    y_sel = g["y"].astype(np.float64).reshape(len(sel), cfg.n_det)
+    y_full = np.zeros((cfg.n_angles, cfg.n_det), dtype=np.float32)
+    y_full[sel] = y_sel
+    yd = dev(y_full)
+    worst = {}
+    for lv in range(cfg.levels):
+        f = 2 ** lv
+        op = ctmodel.coarse_projector(geom, f)
+        xl = sketch_oracle.decimate(x, f).ravel() if f > 1 else x.ravel()
+        fwd = host(op.apply(dev(xl))).reshape(cfg.n_angles, cfg.n_det)[sel]
+        e_f = rel_l2(fwd, g[f"fwd_f{f}"])
+        bp = host(op.adjoint_apply(yd))
+        if f"pix_f{f}" in g:
+            bp = bp[g[f"pix_f{f}"]]
+        e_a = rel_l2(bp, g[f"adj_f{f}"])
+        worst[f] = (e_f, e_a)
+        # the axis-parallel rows (every ray on a gridline: the tie rule decides)
+        for a in (0, cfg.n_angles // 2):
+            k = int(np.nonzero(sel == a)[0][0])
+            ref_row = g[f"fwd_f{f}"].reshape(len(sel), cfg.n_det)[k]
+            assert rel_l2(fwd[k], ref_row) <= 1e-6, (f, a)
+    return worst
+
+
+@pytest.mark.parametrize("name", ["C", "E"])
+def test_sampled_angles_every_level(name):
+    worst = _sampled_levels(CONFIGS[name], golden(f"proj_{name}_sampled.npz"))
+    for f, (e_f, e_a) in worst.items():
+        assert e_f <= TOL_PROJ and e_a <= TOL_PROJ, (name, f, e_f, e_a)
+
+
+def test_pixel_width():
+    g = golden("proj_width.npz")
+    idx = 0
+    while f"c{idx}_meta" in g:
+        side, na, nd, h = g[f"c{idx}_meta"]
+        geom = ctmodel.Geometry(int(side), int(na), int(nd))
+        fwd = ctmodel.project(geom, dev(g[f"c{idx}_x"]), pixel_width=float(h))
+        adj = ctmodel.backproject(geom, dev(g[f"c{idx}_y"]), pixel_width=float(h))
+        assert tuple(fwd.shape) == (int(na), int(nd)) and tuple(adj.shape) == (int(side),) * 2
+        assert rel_l2(host(fwd), g[f"c{idx}_fwd"]) <= TOL_PROJ, h
+        assert rel_l2(host(adj), g[f"c{idx}_adj"]) <= TOL_PROJ, h
+        op = ctmodel.projector_op(geom, pixel_width=float(h))
+        assert rel_l2(host(op.apply(dev(g[f"c{idx}_x"]))), g[f"c{idx}_fwd"]) <= TOL_PROJ
+        idx += 1
+    assert idx == 6
+    with pytest.raises(ValueError, match="multiple of 1/64"):
+        ctmodel.projector_op(ctmodel.Geometry(16, 20, 23), pixel_width=0.3)
+
+
+def _problem(cfg, b, angles=None):
+    geom = ctmodel.Geometry(cfg.side, cfg.n_angles, cfg.n_det)
+    K = ctmodel.projector_op(geom, angles=angles)
+    fam = mrsketch.make_family(cfg.levels, cfg.side, [1.0 / cfg.levels] * cfg.levels,
+                               mode="coarse")
+    prob = solvers.make_problem(
+        K, b, fam, proxlib.ridge_fn(cfg.mu_g), proxlib.quadratic_conjugate_fn(b),
+        coarse_projector=lambda f: ctmodel.coarse_projector(geom, f, angles=angles))
+    assert prob.engine is not None
+    return prob
+
+
+def _check_trajectory(prob, g, stops, extra=()):
+    sigma, mu = float(g["sigma"]), float(g["mu"])
+    st = solvers.init_state(prob, seed=int(g["seed"]))
+    levels = []
+    for k in range(1, max(stops) + 1):
+        solvers.sketch_step(st, prob, sigma, mu)
+        levels.append(st.last_level)
+        if k in stops:
+            errs = {"x": rel_l2(host(st.x), g[f"x_{k}"]), "y": rel_l2(host(st.y), g[f"y_{k}"])}
+            for name in extra:
+                errs[name] = rel_l2(host(getattr(st, name)), g[f"{name}_{k}"])
+            assert all(v <= TOL_ITER for v in errs.values()), (k, errs)
+            assert st.cost == float(g[f"cost_{k}"]), k
+    assert levels == g["levels"].astype(int).tolist()
+    return st
+
+
+def test_iterates_config_A_across_resum():
+    """1100 iterations at a stable sigma: the device tables and sums follow the
+    reference through the k = 1000 resum (solvers.py:184-191,219-220)."""
+    g = golden("solver_A_long.npz")
+    cfg = CONFIGS["A"]
+    prob = _problem(cfg, g["b"])
+    _check_trajectory(prob, g, (999, 1000, 1100), ("phi_sum", "psi_sum"))
+
+
+def test_iterates_config_C():
+    """Config C (r = 5: the fused compensation S_5 over 16-pixel blocks) for 40
+    epochs against the reference's own sketch_step."""
+    g = golden("solver_C.npz")
+    cfg = CONFIGS["C"]
+    prob = _problem(cfg, g["b"])
+    assert prob.engine.plan.quad_forward
+    _check_trajectory(prob, g, (26, cfg.iters_for_epochs()))
+
+
+def test_iterates_config_D_grid_on_angle_subset():
+    """The 1024^2 grid with all six levels (factors 1..32, the r = 6
+    compensation) on a quad-closed subset of 64 of the 1440 angles, 50 epochs:
+    the reference solver on ray_matrix of the same rows."""
+    g = golden("solver_D_subset.npz")
+    cfg = CONFIGS["D"]
+    rows = tuple(int(a) for a in g["rows"])
+    assert rows == ctmodel.quad_subset(cfg.n_angles, g["bases"].astype(int).tolist())
+    prob = _problem(cfg, g["b"], angles=rows)
+    assert prob.engine.plan.quad_forward
+    _check_trajectory(prob, g, (cfg.iters_for_epochs(),))

@@ -338,14 +338,14 @@ def test_long_run_config_B_levels_and_iterates():
     assert rel_l2(host(st.y), ost.y) <= 1e-3
 
 
-def test_rejects_unsupported_problems():
+def test_rejects_bad_arguments():
     geom = ctmodel.Geometry(16, 20, 23)
     K = ctmodel.projector_op(geom)
     fam = mrsketch.make_family(2, 16, [0.5, 0.5], mode="exact")
     b = np.zeros(geom.m)
     prob = solvers.make_problem(K, b, fam, proxlib.ridge_fn(1.0), proxlib.quadratic_conjugate_fn(b))
-    with pytest.raises(TypeError, match="coarse-mode"):
-        solvers.init_state(prob)
+    assert prob.engine is None  # exact mode: the generic device path (test_gpu_dropin.py)
+    assert solvers.init_state(prob).phi_tab is None
     fam = mrsketch.make_family(2, 16, [0.5, 0.5], mode="coarse")
     with pytest.raises(ValueError, match="coarse_projector factory"):
         solvers.make_problem(K, b, fam, proxlib.ridge_fn(1.0), proxlib.quadratic_conjugate_fn(b))
@@ -449,7 +449,8 @@ def test_run_sketch_seq_and_saga_saddle():
     assert np.array_equal(host(rep.x), host(st.x))
     assert [r[0] for r in rep.rows] == [0, 4, 8, 12]
     assert rep.rows[-1][1] == st.cost and rep.rows[-1][2] == st.last_level
-    assert solvers.verify_decomposition(prob) <= 1e-5
+    blocks = [linops.scale(op, float(p)) for op, p in zip(prob.ops, prob.probs)]
+    assert solvers.verify_decomposition(prob.K, blocks, trials=1) <= solvers.DECOMPOSITION_TOL
     rep_s = solvers.run(prob, "saga-saddle", 1e-3, 1e-2, 12, record_every=4, seed=3)
     rep_p = solvers.run(prob, "sketch", 1e-3, 1e-2, 12, record_every=4, seed=3)
     assert np.array_equal(host(rep_s.x), host(rep_p.x))

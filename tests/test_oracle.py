@@ -139,3 +139,44 @@ def test_tv_oracle_pinned_to_reference(g_tv):
         assert np.max(np.abs(out - g_tv[f"out_{side}"])) <= 1e-12
     out = po.prox_tv_nonneg(g_tv["xp_step"], 0.8, 0.5, inner_iters=4000, inner_tol=1e-13)
     assert np.max(np.abs(out - g_tv["out_step"])) <= 1e-12
+
+
+@pytest.mark.parametrize("name,min_f", [("C", 2), ("E", 16)])
+def test_sampled_angles_large_configs(name, min_f):
+    """The oracle against the reference's ray_matrix rows at configs C and E
+    (coarse levels: the fine ones take minutes on one core)."""
+    from conftest import golden
+
+    cfg = CONFIGS[name]
+    g = golden(f"proj_{name}_sampled.npz")
+    sel = g["angles"].astype(np.int64)
+    x = ellipse_phantom(cfg.side, 0)
+    y = g["y"].astype(np.float64)
+    for lv in range(cfg.levels):
+        f = 2 ** lv
+        if f < min_f:
+            continue
+        op = ct_oracle.ProjectorOracle(cfg.side, cfg.n_angles, cfg.n_det, f, sel)
+        xl = sketch_oracle.decimate(x, f).ravel()
+        assert rel_l2(op.apply(xl), g[f"fwd_f{f}"]) <= 1e-12, (name, f)
+        bp = op.adjoint_apply(y)
+        if f"pix_f{f}" in g:
+            bp = bp[g[f"pix_f{f}"]]
+        assert rel_l2(bp, g[f"adj_f{f}"]) <= 1e-12, (name, f)
+
+
+def test_solver_trajectory_C_first_steps():
+    """The oracle's sketch_step against the reference trajectory at config C
+    (golden solver_C.npz), through the first 26 iterations."""
+    from conftest import golden
+
+    g = golden("solver_C.npz")
+    cfg = CONFIGS["C"]
+    orc = solver_oracle.SketchedCT(cfg.side, cfg.n_angles, cfg.n_det, [1.0 / cfg.levels] * cfg.levels,
+                                   csr=False)
+    b = g["b"].astype(np.float64)
+    st = solver_oracle.init_state(orc, seed=int(g["seed"]))
+    for _ in range(26):
+        solver_oracle.sketch_step(st, orc, b, float(g["sigma"]), float(g["mu"]), cfg.mu_g)
+    assert [lv + 1 for lv in st.levels] == g["levels"][:26].astype(int).tolist()
+    assert rel_l2(st.x, g["x_26"]) <= 1e-6 and rel_l2(st.y, g["y_26"]) <= 1e-6
