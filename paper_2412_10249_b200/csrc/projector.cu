@@ -19,7 +19,11 @@
 #include <cstdlib>
 #include <cuda.h>
 
+#include <cooperative_groups.h>
+
 #include "imask_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace imask {
 
@@ -529,14 +533,16 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   const float S = A.S, B = A.B;
 
   if (ctl[0]) {
-    // fallback: global (L1) loads, as k_forward_sym
+    // fallback: global (L1) loads over the lane's own band range (a warp holds
+    // four entries, whose angles may be far apart in a sparse angle subset:
+    // outside its own range a lane's position can leave the zero padding)
     if (valid) {
       const float2* __restrict__ img = trans ? PT : P;
       const float2* __restrict__ imgd = trans ? PTM : PM;
       const long long dYl = A.step + ((long long)pitch << 32);
-      Fix32 Y = fix_from(X0 + (long long)wlo * dYl + ((long long)(1 + kPadC) << 32));
+      Fix32 Y = fix_from(X0 + (long long)lo * dYl + ((long long)(1 + kPadC) << 32));
       const Fix32 dY = fix_from(dYl);
-      for (int b = wlo; b < whi; ++b) {
+      for (int b = lo; b < hi; ++b) {
         const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
         const float2 v = __ldg(img + Y.hi);
         acc2 = fadd2(acc2, v);
@@ -788,9 +794,10 @@ template <> struct AdjWin<true, true> { using T = float4; };
 // bins and weights as its mirror m(p) = (n-1-col,row) at angle n-a (theta ->
 // pi-theta, x -> -x), so each weight evaluation accumulates into both pixels,
 // reading rows a and n-a from one staged window element. Angle 0 is excluded
-// (the half-open tie rule flips under the mirror) and runs through the plain
-// kernel. Angles [a_begin, a_end) are split over grid.z; plane z of `out`
-// receives this split's partial image.
+// from the loop (the half-open tie rule flips under the mirror); its box is
+// added per pixel in the epilogue (add_a0). Angles [a_begin, a_end) are split
+// over grid.z, a thread-block cluster of cz splits reduces on chip, and plane
+// z / cz of `out` receives the cluster's partial image.
 // Pixel k of thread slot p (0 <= p < lanes) within a T x T tile. The lanes of
 // a warp cover a compact 8 x 4 pixel block at every k, so one window read
 // touches few distinct bins (ideally ~8|cos| + 4|sin| + 1 slots, many lanes
@@ -814,6 +821,20 @@ __device__ __forceinline__ void adj_pixel(int p, int k, int& dx, int& dy) {
   }
 }
 
+// Angle 0 (cos = 1, sin = 0) at pixel (row, col): the half-open box covers the
+// bins ceil(v) .. ceil(v) + nb - 1, v = eta - R (exact in double: half-integers),
+// each with weight 1 -- the kernel's axis rule, summed in bin order.
+__device__ __forceinline__ float angle0_value(const float* __restrict__ sino, const AdjAngle& A,
+                                              int row, int col, int n_det) {
+  const int j0 = (int)ceil(A.eta0 + (double)col * A.ch + (double)row * A.sh);
+  float v = 0.f;
+  for (int b = 0; b < A.nb; ++b) {
+    const int j = j0 + b;
+    if (j >= 0 && j < n_det) v += __ldg(sino + j) * A.wsc;
+  }
+  return v;
+}
+
 #ifndef IMASK_ADJ_SYM_MINB
 #define IMASK_ADJ_SYM_MINB 7
 #endif
@@ -821,7 +842,7 @@ template <bool kPair, int T, bool kSym, int kPPT>
 __global__ void __launch_bounds__(kAdjThreads, kSym ? IMASK_ADJ_SYM_MINB : 8)
 k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W, int CA,
           int a_begin, int a_per_split, int a_end, int n_mirror, int n_det,
-          const AdjAngle* __restrict__ ang) {
+          const AdjAngle* __restrict__ ang, int add_a0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using WinT = typename AdjWin<kPair, kSym>::T;
   constexpr int lanes = T * T / kPPT;
@@ -967,38 +988,66 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
       }
     }
   }
-  float* dst = out + (size_t)blockIdx.z * n * n;  // per-split partial image
+  // Epilogue. Value i = (q * kPPT + k) * lanes + p of this CTA's tile (q: the
+  // pixel or its mirror, k: the thread's k-th pixel, p: the lane slot). With a
+  // thread-block cluster along grid.z (the angle splits of one tile), the
+  // cluster's CTAs put their tiles in shared memory and each sums a slice of
+  // the pixels over the cluster ranks in rank order (DSMEM reads), so one
+  // plane per cluster is written instead of one per split (deterministic).
+  // Angle 0 (unpaired under the mirror, add_a0) is added on plane 0.
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cz = (int)cluster.num_blocks();
+  float* dst = out + (size_t)(blockIdx.z / cz) * n * n;
+  const bool a0 = add_a0 && blockIdx.z < (unsigned)cz;
+  auto store = [&](int i, float v) {
+    const int q = i / (lanes * kPPT), r = i % (lanes * kPPT);
+    int px, py;
+    adj_pixel<T>(r % lanes, r / lanes, px, py);
+    const int row = y0 + py;
+    const int col = q == 0 ? x0 + px : n - 1 - (x0 + px);
+    if (row < n && col >= 0 && col < n) {
+      if (a0) v += angle0_value(sino, ang[0], row, col, n_det);
+      dst[(size_t)row * n + col] = v;
+    }
+  };
+  constexpr int kVals = NACC * lanes * kPPT;
+  float* tb = reinterpret_cast<float*>(win);  // the windows are dead after the angle loop
+  __syncthreads();
   if (G > 1) {
     // fixed-order sum over the angle groups
-    __syncthreads();
 #pragma unroll
     for (int q = 0; q < NACC; ++q)
 #pragma unroll
       for (int k = 0; k < kPPT; ++k)
         red[((q * G + grp) * kPPT + k) * lanes + pix0] = acc[q][k];
     __syncthreads();
-    for (int i = tid; i < NACC * lanes * kPPT; i += kAdjThreads) {
+    for (int i = tid; i < kVals; i += kAdjThreads) {
       const int q = i / (lanes * kPPT), r = i % (lanes * kPPT);
       const int k = r / lanes, p = r % lanes;
       float v = 0.f;
       for (int g = 0; g < G; ++g) v += red[((q * G + g) * kPPT + k) * lanes + p];
-      int px, py;
-      adj_pixel<T>(p, k, px, py);
-      const int row = y0 + py;
-      const int col = q == 0 ? x0 + px : n - 1 - (x0 + px);
-      if (row < n && col >= 0 && col < n) dst[(size_t)row * n + col] = v;
+      if (cz > 1) tb[i] = v; else store(i, v);
     }
   } else {
 #pragma unroll
-    for (int k = 0; k < kPPT; ++k) {
-      int px, py;
-      adj_pixel<T>(pix0, k, px, py);
-      const int row = y0 + py, col = x0 + px;
-      if (row < n && col < n) {
-        dst[(size_t)row * n + col] = acc[0][k];
-        if constexpr (kSym) dst[(size_t)row * n + (n - 1 - col)] = acc[NACC - 1][k];
+    for (int q = 0; q < NACC; ++q)
+#pragma unroll
+      for (int k = 0; k < kPPT; ++k) {
+        const int i = (q * kPPT + k) * lanes + pix0;
+        if (cz > 1) tb[i] = acc[q][k]; else store(i, acc[q][k]);
       }
+  }
+  if (cz > 1) {
+    cluster.sync();
+    const int chunk = (kVals + cz - 1) / cz;
+    const int lo = (int)cluster.block_rank() * chunk;
+    const int hi = min(kVals, lo + chunk);
+    for (int i = lo + tid; i < hi; i += kAdjThreads) {
+      float v = 0.f;
+      for (int rk = 0; rk < cz; ++rk) v += cluster.map_shared_rank(tb, rk)[i];
+      store(i, v);
     }
+    cluster.sync();  // keep this CTA's tile alive until every rank has read it
   }
 }
 
@@ -1114,9 +1163,12 @@ void init_kernel_attributes() {
 // scratch sizing): T = 32 at factors 1-2, 16 at factors 4-8 and, for plans of
 // >= 512 angles, 16; else 8;
 // T shrinks to the next power of two >= n (>= 8) for small images. The angle
-// splits S give the grid ~16-20 CTAs per SM; with mirror symmetry (sym) the
-// grid covers half the tiles and one extra partial plane holds angle 0.
-void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_out) {
+// splits S give the grid ~16-28 CTAs per SM; with mirror symmetry (sym) the
+// grid covers half the tiles. Splits are grouped into thread-block clusters of
+// cz (<= 8, S a multiple of cz) that reduce their partial tiles on chip, so
+// the level writes S / cz planes.
+void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_out,
+                    int* cz_out = nullptr) {
   // (measured beside the value-plane forward: 16 at f = 8 -> step -4% on the
   // whole set and on shards; 16 at f = 16 -> -1..2% on the whole set, slower
   // on 1/4 and 1/8 shards, which keep 8; at f = 32 16 is faster with the L2
@@ -1155,8 +1207,16 @@ void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_o
   const int max_s = n_loc / 8 > 1 ? n_loc / 8 : 1;
   if (S > max_s) S = max_s;
   if (S < 1) S = 1;
+  static const int cz_max = [] {
+    const char* e = getenv("IMASK_ADJ_CLUSTER");  // tuning / A-B runs: 1 disables clusters
+    const int v = e ? atoi(e) : 8;
+    return v < 1 ? 1 : (v > 8 ? 8 : v);
+  }();
+  const int cz = S < cz_max ? S : cz_max;
+  S = (S / cz) * cz;
   *T_out = T;
   *S_out = S;
+  if (cz_out) *cz_out = cz;
 }
 
 // Mirror symmetry applies when the slab is the whole, even-sized angle set and
@@ -1169,26 +1229,40 @@ bool adjoint_sym_ok(int n, int factor, int n_loc, bool mirror_layout) {
 }
 
 int adjoint_planes(int n, int factor, int n_loc, bool sym, int sym_s) {
-  int T, S;
-  adjoint_layout(n, factor, n_loc, sym, &T, &S);
-  const int planes = sym ? S + sym_s : S;
+  int T, S, cz;
+  adjoint_layout(n, factor, n_loc, sym, &T, &S, &cz);
+  (void)sym_s;  // angle 0 is added in the symmetric kernel's epilogue
+  const int planes = S / cz;
   return planes > 1 ? planes : 0;
 }
 
 template <bool kPair, int T, bool kSym>
-static void adj_launch_(dim3 grid, size_t smem, cudaStream_t stream, const float* sino, float* dst,
-                       int n, int W, int CA, int a_begin, int per_split, int a_end, int n_mirror,
-                       int n_det, const AdjAngle* ang) {
-  k_adjoint<kPair, T, kSym, (T >= 16 ? 8 : 2)><<<grid, kAdjThreads, smem, stream>>>(
-      sino, dst, n, W, CA, a_begin, per_split, a_end, n_mirror, n_det, ang);
+static void adj_launch_(dim3 grid, size_t smem, cudaStream_t stream, int cz, const float* sino,
+                        float* dst, int n, int W, int CA, int a_begin, int per_split, int a_end,
+                        int n_mirror, int n_det, const AdjAngle* ang, int add_a0) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kAdjThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = (unsigned)cz;
+  cfg.attrs = attr;
+  cfg.numAttrs = cz > 1 ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k_adjoint<kPair, T, kSym, (T >= 16 ? 8 : 2)>, sino, dst, n, W, CA,
+                     a_begin, per_split, a_end, n_mirror, n_det, ang, add_a0);
 }
 
 static void adj_dispatch(bool pair, int T, bool sym, dim3 grid, size_t smem, cudaStream_t stream,
-                         const float* sino, float* dst, int n, int W, int CA, int a_begin,
-                         int per_split, int a_end, int n_mirror, int n_det, const AdjAngle* ang) {
-#define ADJ_CALL(P_, T_, S_)                                                                \
-  adj_launch_<P_, T_, S_>(grid, smem, stream, sino, dst, n, W, CA, a_begin, per_split, a_end, \
-                         n_mirror, n_det, ang)
+                         int cz, const float* sino, float* dst, int n, int W, int CA, int a_begin,
+                         int per_split, int a_end, int n_mirror, int n_det, const AdjAngle* ang,
+                         int add_a0) {
+#define ADJ_CALL(P_, T_, S_)                                                                   \
+  adj_launch_<P_, T_, S_>(grid, smem, stream, cz, sino, dst, n, W, CA, a_begin, per_split, a_end, \
+                          n_mirror, n_det, ang, add_a0)
   if (pair) {
     if (sym) ADJ_CALL(true, 32, true); else ADJ_CALL(true, 32, false);
   } else if (T == 32) {
@@ -1215,8 +1289,11 @@ static size_t adj_smem(bool pair, bool sym, int T, int W, int* CA_io) {
   while (CA > G && (size_t)CA * W * elem > cap) CA >>= 1;
   if (CA < G) CA = G;
   *CA_io = CA;
+  // the window region also holds the CTA's tile for the cluster reduction
+  const size_t tile = sizeof(float) * T * T * (sym ? 2 : 1);
+  const size_t win = (size_t)CA * W * elem;
   return (size_t)CA * sizeof(AdjStage) + kAdjThreads * ppt * (sym ? 2 : 1) * sizeof(float) +
-         (size_t)CA * W * elem;
+         (win > tile ? win : tile);
 }
 
 // Reduction mode of the split planes, shared by the reduce kernels and the
@@ -1246,62 +1323,36 @@ cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n,
                            int n_loc, int n_det, const AdjAngle* ang, int sym_s,
                            cudaStream_t stream, const SideStream& side, int* launches,
                            int* defer_planes) {
+  (void)side;
   if (defer_planes) *defer_planes = 0;
   const bool sym = adjoint_sym_ok(n, factor, n_loc, sym_s >= 0);
-  int T, S;
-  adjoint_layout(n, factor, n_loc, sym, &T, &S);
+  int T, S, cz;
+  adjoint_layout(n, factor, n_loc, sym, &T, &S, &cz);
   const bool pair = (factor == 1 && T == 32);
   const int W = (int)floor(1.41422 * T * factor) + 6;
+  const int planes = S / cz;
+  float* dst = planes > 1 ? partial : out;
   int CA;
-  *launches = 0;
+  const size_t smem = adj_smem(pair, sym, T, W, &CA);
   if (sym) {
-    // rows [sym_s, n_loc) with their mirrors over the left-half tiles, S planes;
-    // the unpaired rows [0, sym_s) (angle 0) through the plain kernel into plane
-    // S (on the side stream, if any, concurrently with the symmetric kernel);
-    // then the ordered reduction
-    const int planes = S + sym_s;
-    if (sym_s > 0) {
-      cudaStream_t s0 = stream;
-      if (side.stream) {
-        cudaEventRecord(side.fork, stream);
-        cudaStreamWaitEvent(side.stream, side.fork, 0);
-        s0 = side.stream;
-      }
-      const size_t smem0 = adj_smem(pair, false, T, W, &CA);
-      dim3 grid0((n + T - 1) / T, (n + T - 1) / T, 1);
-      adj_dispatch(pair, T, false, grid0, smem0, s0, sino, partial + (size_t)S * n * n, n, W,
-                   CA, 0, sym_s, sym_s, n_loc, n_det, ang);
-      if (side.stream) cudaEventRecord(side.join, side.stream);
-      ++*launches;
-    }
-    const size_t smem = adj_smem(pair, true, T, W, &CA);
+    // rows [sym_s, n_loc) with their mirrors over the left-half tiles; the
+    // unpaired angle 0 (rows [0, sym_s)) in the epilogue
     const int per_split = (n_loc - sym_s + S - 1) / S;
     dim3 grid(n / (2 * T), (n + T - 1) / T, S);
-    adj_dispatch(pair, T, true, grid, smem, stream, sino, planes > 1 ? partial : out, n, W, CA,
-                 sym_s, per_split, n_loc, sym_s + n_loc - 1, n_det, ang);
-    ++*launches;
-    if (sym_s > 0 && side.stream) cudaStreamWaitEvent(stream, side.join, 0);
-    if (planes > 1) {
-      if (defer_planes) {
-        *defer_planes = planes;
-      } else {
-        adj_reduce(partial, out, n * n, planes, stream);
-        ++*launches;
-      }
-    }
-    return cudaGetLastError();
+    adj_dispatch(pair, T, true, grid, smem, stream, cz, sino, dst, n, W, CA, sym_s, per_split,
+                 n_loc, sym_s + n_loc - 1, n_det, ang, sym_s > 0 ? 1 : 0);
+  } else {
+    const int per_split = (n_loc + S - 1) / S;
+    dim3 grid((n + T - 1) / T, (n + T - 1) / T, S);
+    adj_dispatch(pair, T, false, grid, smem, stream, cz, sino, dst, n, W, CA, 0, per_split, n_loc,
+                 n_loc, n_det, ang, 0);
   }
-  const size_t smem = adj_smem(pair, false, T, W, &CA);
-  const int per_split = (n_loc + S - 1) / S;
-  dim3 grid((n + T - 1) / T, (n + T - 1) / T, S);
-  adj_dispatch(pair, T, false, grid, smem, stream, sino, S > 1 ? partial : out, n, W, CA, 0,
-               per_split, n_loc, n_loc, n_det, ang);
   *launches = 1;
-  if (S > 1) {
+  if (planes > 1) {
     if (defer_planes) {
-      *defer_planes = S;
+      *defer_planes = planes;
     } else {
-      adj_reduce(partial, out, n * n, S, stream);
+      adj_reduce(partial, out, n * n, planes, stream);
       *launches = 2;
     }
   }

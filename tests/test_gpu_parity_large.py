@@ -60,7 +60,7 @@ def _sampled_levels(cfg, g):
         for a in (0, cfg.n_angles // 2):
             k = int(np.nonzero(sel == a)[0][0])
             ref_row = g[f"fwd_f{f}"].reshape(len(sel), cfg.n_det)[k]
-            assert rel_l2(fwd[k], ref_row) <= 1e-6, (f, a)
+            assert rel_l2(fwd[k], ref_row) <= 1e-5, (f, a)  # a wrong tie rule: ~1e-2
     return worst
 
 
