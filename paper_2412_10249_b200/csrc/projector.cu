@@ -1207,9 +1207,13 @@ void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_o
   const int max_s = n_loc / 8 > 1 ? n_loc / 8 : 1;
   if (S > max_s) S = max_s;
   if (S < 1) S = 1;
+  // Clusters measured slower at every level of config D (f=1 adjoint 515 ->
+  // 549 us with clusters of 8, f=4 118 -> 144 us; 2 and 4 in between): the
+  // co-scheduling of a cluster's CTAs costs more SM time than the plane
+  // round trip through L2 saves, so the default is no cluster (A/B knob).
   static const int cz_max = [] {
-    const char* e = getenv("IMASK_ADJ_CLUSTER");  // tuning / A-B runs: 1 disables clusters
-    const int v = e ? atoi(e) : 8;
+    const char* e = getenv("IMASK_ADJ_CLUSTER");  // tuning / A-B runs: cluster size, 1 = none
+    const int v = e ? atoi(e) : 1;
     return v < 1 ? 1 : (v > 8 ? 8 : v);
   }();
   const int cz = S < cz_max ? S : cz_max;
