@@ -57,6 +57,8 @@ def parse():
                     help="skip the projector microbenchmark (config E)")
     ap.add_argument("--collective", action="store_true",
                     help="run the angle-sharded (NCCL) step path even at one rank (path check)")
+    ap.add_argument("--no-full-reference", action="store_true",
+                    help="--impl reference: skip the fully timed config-C reference solve")
     ap.add_argument("--steps-only", action="store_true",
                     help="skip the post-run kernel measurements (launch-list profiling runs)")
     return ap.parse_args()
@@ -64,20 +66,21 @@ def parse():
 
 # ---------------------------------------------------------------- reference arm
 
-def ray_band_count(side: int, n_angles: int, n_det: int, angles=None) -> float:
-    """Ray-band visits of the factor-1 forward (the bands whose left chord partner
-    lies in [-1, n-1], as band_range in projector.cu), summed over all rays."""
+def ray_band_count(side: int, n_angles: int, n_det: int, angles=None, factor: int = 1) -> float:
+    """Ray-band visits of the level-`factor` forward (the bands whose left chord
+    partner lies in [-1, n-1], as band_range in projector.cu), summed over all rays."""
     th = np.arange(n_angles) * (np.pi / n_angles)
     if angles is not None:
         th = th[np.asarray(angles)]
     c, s = np.cos(th), np.sin(th)
     c[np.abs(c) < 1e-14] = 0.0
     s[np.abs(s) < 1e-14] = 0.0
-    n, half, t0 = side, side / 2.0, -(n_det - 1) / 2.0
+    h = float(factor)
+    n, half, t0 = side // factor, side / 2.0, -(n_det - 1) / 2.0
     row = np.abs(c) >= np.abs(s)
     a_, b_ = np.where(row, c, s), np.where(row, s, c)  # band-normal / along-band cosines
-    xi_dj = 1.0 / a_
-    xi_base = t0 / a_ + (half - 0.5) * b_ / a_ + half - 0.5
+    xi_dj = 1.0 / (a_ * h)
+    xi_base = t0 / (a_ * h) + (half - h / 2) * b_ / (a_ * h) + half / h - 0.5
     step = -b_ / a_
     x0 = xi_base[:, None] + np.arange(n_det)[None, :] * xi_dj[:, None]
     st = np.broadcast_to(step[:, None], x0.shape)
@@ -90,11 +93,30 @@ def ray_band_count(side: int, n_angles: int, n_det: int, angles=None) -> float:
     return float(cnt.sum())
 
 
-def projector_microbench(device, reps: int = 20) -> dict:
+def adjoint_window_reads(side: int, n_angles: int, factor: int) -> float:
+    """Shared-memory bytes the level-`factor` adjoint reads: factor 1 one 16-byte
+    element (two bins of a pixel and of its mirror) per pixel pair and angle, i.e.
+    8 B per pixel-angle; coarser levels one 8-byte element (a bin of both mirror
+    rows) per candidate bin (nb = floor(2R) + 1) per pixel pair and angle."""
+    n = side // factor
+    if factor == 1:
+        return 8.0 * n * n * n_angles
+    th = np.arange(n_angles) * (np.pi / n_angles)
+    R = (np.abs(np.cos(th)) + np.abs(np.sin(th))) * factor / 2.0
+    nb = np.floor(2 * R) + 1
+    return 4.0 * n * n * float(nb.sum())
+
+
+def projector_microbench(device, reps: int = 100, shard_reps: int = 20, smem_peak_gbs=None,
+                         hbm_peak_gbs=None) -> dict:
     """Config E: forward K and adjoint K^T alone on the seeded
     2048^2 ellipse image (2048 angles x 2897 bins) at every level f = 1..64,
     median of `reps` CUDA-event timed launches each (L2 warm: a projector's
-    operands are on-chip between launches anyway)."""
+    operands are on-chip between launches anyway); per level the algorithmic
+    HBM GB/s (4 (d_i + m) bytes per apply), the shared-memory bytes the kernels
+    read against the live shared-memory peak, and the angle-sharded runs at
+    2/4/8 ranks (every rank's shard plan timed alone on this GPU, max over
+    ranks: compute only, no collective)."""
     import torch
 
     from paper_2412_10249_b200 import ctmodel, mrsketch
@@ -102,18 +124,15 @@ def projector_microbench(device, reps: int = 20) -> dict:
 
     e = CONFIGS["E"]
     geom = ctmodel.Geometry(e.side, e.n_angles, e.n_det)
-    plan = ctmodel.get_plan(geom)
     x = torch.from_numpy(ellipse_phantom(e.side, 0).astype(np.float32)).to(device)
     y = torch.from_numpy(np.random.default_rng(7).standard_normal(geom.m).astype(np.float32)).to(device)
-    sino = torch.empty(geom.m, device=device)
     stream = torch.cuda.current_stream(device)
-    out = {}
 
-    def med(fn):
+    def med(fn, n_rep):
         for _ in range(3):
             fn()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(reps)]
+              for _ in range(n_rep)]
         for a, b in ev:
             a.record(stream)
             fn()
@@ -121,19 +140,61 @@ def projector_microbench(device, reps: int = 20) -> dict:
         torch.cuda.synchronize()
         return float(np.median([a.elapsed_time(b) for a, b in ev]))
 
-    f = 1
-    while f <= 64:
-        u = (x if f == 1 else mrsketch.decimate(x, f)).reshape(-1).contiguous()
-        bp = torch.empty(u.numel(), device=device)
-        fwd = med(lambda: plan.project(u, f, sino))
-        adj = med(lambda: plan.backproject(y, f, bp))
+    levels = [2 ** k for k in range(7)]
+    us = {f: (x if f == 1 else mrsketch.decimate(x, f)).reshape(-1).contiguous() for f in levels}
+
+    def time_plan(plan, ysl, n_rep):
+        sino = torch.empty(plan.m_loc, device=device)
+        res = {}
+        for f in levels:
+            bp = torch.empty(us[f].numel(), device=device)
+            res[f] = (med(lambda: plan.project(us[f], f, sino), n_rep),
+                      med(lambda: plan.backproject(ysl, f, bp), n_rep))
+        return res
+
+    one = time_plan(ctmodel.get_plan(geom), y, reps)
+    out = {}
+    for f in levels:
+        fwd, adj = one[f]
+        di = (e.side // f) ** 2
+        hbm_bytes = 4.0 * (di + geom.m)
         nnz = 4.0 / np.pi * e.n_angles * e.side * e.side / f
-        out[f"f{f}"] = {"forward_ms": round(fwd, 4), "adjoint_ms": round(adj, 4),
-                        "fwd_adj_pairs_per_s": round(1e3 / (fwd + adj), 1),
-                        "footprint_evals_per_s": round(2 * nnz / ((fwd + adj) * 1e-3), 1)}
-        f *= 2
+        f_smem = 8.0 * ray_band_count(e.side, e.n_angles, e.n_det, factor=f)
+        a_smem = adjoint_window_reads(e.side, e.n_angles, f)
+        row = {"forward_ms": round(fwd, 4), "adjoint_ms": round(adj, 4),
+               "fwd_adj_pairs_per_s": round(1e3 / (fwd + adj), 1),
+               "footprint_evals_per_s": round(2 * nnz / ((fwd + adj) * 1e-3), 1),
+               "hbm_bytes_per_apply": hbm_bytes,
+               "forward_hbm_gbs": round(hbm_bytes / (fwd * 1e-3) / 1e9, 1),
+               "adjoint_hbm_gbs": round(hbm_bytes / (adj * 1e-3) / 1e9, 1)}
+        if hbm_peak_gbs:
+            row["forward_hbm_frac"] = round(row["forward_hbm_gbs"] / hbm_peak_gbs, 5)
+            row["adjoint_hbm_frac"] = round(row["adjoint_hbm_gbs"] / hbm_peak_gbs, 5)
+        if smem_peak_gbs:
+            row["forward_smem_frac"] = round(f_smem / (fwd * 1e-3) / 1e9 / smem_peak_gbs, 4)
+            row["adjoint_smem_frac"] = round(a_smem / (adj * 1e-3) / 1e9 / smem_peak_gbs, 4)
+        out[f"f{f}"] = row
+    sharded = {}
+    for W in (2, 4, 8):
+        worst = {f: [0.0, 0.0] for f in levels}
+        for rank in range(W):
+            rows = ctmodel.shard_angles(e.n_angles, rank, W)
+            plan = ctmodel.Plan(geom, angles=rows, device=device)
+            ysl = y.reshape(e.n_angles, e.n_det)[list(rows)].reshape(-1).contiguous()
+            for f, (fw, ad) in time_plan(plan, ysl, shard_reps).items():
+                worst[f][0] = max(worst[f][0], fw)
+                worst[f][1] = max(worst[f][1], ad)
+            del plan
+        sharded[f"world{W}"] = {
+            f"f{f}": {"forward_ms_max_rank": round(fw, 4), "adjoint_ms_max_rank": round(ad, 4),
+                      "efficiency": round((one[f][0] + one[f][1]) / (W * (fw + ad)), 3)}
+            for f, (fw, ad) in worst.items()}
     return {"config": f"E: {e.side}^2, {e.n_angles} angles x {e.n_det} bins, levels f = 1..64",
-            "reps": reps, "statistic": "median", "levels": out}
+            "reps": reps, "statistic": "median", "levels": out,
+            "sharded": sharded,
+            "sharded_note": f"each rank's mirror-closed shard plan timed alone on this GPU "
+                            f"({shard_reps} reps, median), max over ranks; compute only (no "
+                            "all-reduce); efficiency = T_1 / (W T_W) of forward + adjoint"}
 
 
 def cpu_reference(cfg, steps: int, warmup: int, sample: int = CPU_SAMPLE_ANGLES):
@@ -167,7 +228,7 @@ def cpu_reference(cfg, steps: int, warmup: int, sample: int = CPU_SAMPLE_ANGLES)
     b = rng.standard_normal(ops.m)
     tab = rng.standard_normal(ops.m)
     st = so.init_state(ops, seed=SEED)
-    per_level = []
+    per_level, per_level_1 = [], []
     for i in range(r):
         f = ops.factors[i]
         proj = ops.proj[f]
@@ -204,14 +265,27 @@ def cpu_reference(cfg, steps: int, warmup: int, sample: int = CPU_SAMPLE_ANGLES)
         t_step = (time.perf_counter() - t) / 2
         t_img = max(t_step - t_proj - t_sino, 0.0)
         per_level.append(scale * (t_proj + t_sino) + t_img)
+        # the same CSR matvecs on one core (the reference's own execution)
+        proj.set_threads(pool, 1)
+        t = time.perf_counter()
+        for _ in range(reps):
+            proj.adjoint_apply(y)
+            proj.apply(xl)
+        t_proj1 = (time.perf_counter() - t) / reps
+        proj.set_threads(pool, threads)
+        per_level_1.append(scale * (t_proj1 + t_sino) + t_img)
     sched = so.level_schedule(SEED, warmup, steps, probs)
     t_iter = float(np.mean([per_level[int(i)] for i in sched]))
+    t_iter_1 = float(np.mean([per_level_1[int(i)] for i in sched]))
     detail = {
         "sample": f"{sample} of {cfg.n_angles} angles (every {cfg.n_angles // sample}th), all "
                   f"{r} levels; CSR matvec + sinogram-side time x{scale:g}, image-side work (restriction, "
                   f"compensation, prolongation, primal update; full size) as measured; "
                   f"mean over the timed steps' level schedule",
         "per_level_s": [round(v, 6) for v in per_level],
+        "single_core_per_level_s": [round(v, 6) for v in per_level_1],
+        "single_core_iters_per_s": 1.0 / t_iter_1,
+        "extrapolated": True,
         "csr_build_s_excluded": round(t_build, 3),
         "threads": threads,
         "threading": "CSR matvecs split into row blocks over a thread pool; the numpy "
@@ -219,6 +293,99 @@ def cpu_reference(cfg, steps: int, warmup: int, sample: int = CPU_SAMPLE_ANGLES)
     }
     pool.shutdown()
     return 1.0 / t_iter, detail
+
+
+def cpu_reference_full(key: str = "C", steps: int = 8, warm: int = 2) -> dict:
+    """The reference algorithm (oracle/ restatement: scipy CSR float64, the
+    reference's sketch_step) on the FULL operator of config `key`, every step
+    timed with perf_counter, nothing extrapolated: `steps` iterations of the
+    seeded level schedule after `warm` untimed ones, with the CSR matvecs on
+    every host core, then 3 iterations on one core. CSR build time is reported
+    separately (the reference caches its matrices)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import solver_oracle as so
+    from paper_2412_10249_b200.synth import CONFIGS
+
+    cfg = CONFIGS[key]
+    r = cfg.levels
+    probs = [1.0 / r] * r
+    t0 = time.perf_counter()
+    ops = so.SketchedCT(cfg.side, cfg.n_angles, cfg.n_det, probs)
+    build_s = time.perf_counter() - t0
+    threads = max(1, len(os.sched_getaffinity(0)))
+    pool = ThreadPoolExecutor(threads)
+    rng = np.random.default_rng(1)
+    b = rng.standard_normal(ops.m)
+    st = so.init_state(ops, seed=SEED)
+    sched = so.level_schedule(SEED, 0, warm + steps + 3, probs)
+
+    def run(n_threads, ks):
+        for p in ops.proj.values():
+            p.set_threads(pool, n_threads)
+        out = []
+        for k in ks:
+            t = time.perf_counter()
+            so.sketch_step(st, ops, b, SIGMA, cfg.mu_g, cfg.mu_g)
+            out.append(time.perf_counter() - t)
+        return out
+
+    run(threads, range(warm))
+    times = run(threads, range(warm, warm + steps))
+    times1 = run(1, range(warm + steps, warm + steps + 3))
+    pool.shutdown()
+    lev = [int(v) for v in sched[:warm + steps + 3]]
+    return {"config": f"{cfg.name}: {cfg.side}^2, {cfg.n_angles} angles x {cfg.n_det} bins, "
+                      f"r={r}, full operator (no sampling)",
+            "iters_per_s": steps / sum(times), "threads": threads,
+            "step_s": [round(v, 4) for v in times], "levels": lev[warm:warm + steps],
+            "single_core_iters_per_s": 3 / sum(times1),
+            "single_core_step_s": [round(v, 4) for v in times1],
+            "single_core_levels": lev[warm + steps:],
+            "csr_build_s_excluded": round(build_s, 1), "extrapolated": False}
+
+
+def native_config_c(device, steps: int = 100, warmup: int = 10) -> dict:
+    """The native step on config C (512^2 / 720 / 725, r = 5), timed as the
+    headline (device events, L2 flushed between steps): the configuration the
+    reference's fully timed solve (--impl reference, measured_full_operator) runs."""
+    import torch
+
+    from paper_2412_10249_b200 import dist as dist_mod
+    from paper_2412_10249_b200 import ctmodel, mrsketch, solvers
+    from paper_2412_10249_b200.synth import CONFIGS
+
+    cfg = CONFIGS["C"]
+    r = cfg.levels
+    geom = ctmodel.Geometry(cfg.side, cfg.n_angles, cfg.n_det)
+    b = np.random.default_rng(1).standard_normal(geom.m)
+    fam = mrsketch.make_family(r, cfg.side, [1.0 / r] * r, mode="coarse")
+    prob = dist_mod.make_sharded_problem(geom, b, fam, cfg.mu_g)
+    eng = prob.engine
+    st = solvers.init_state(prob, seed=SEED)
+    prm = solvers._params(SIGMA, cfg.mu_g, cfg.mu_g)
+    eng.capture_all(st, prm)
+    for lv in range(r):
+        for _ in range(2):
+            solvers._device_step(eng, st, lv, prm)
+    sched = solvers.draw_levels(SEED, 0, warmup + steps, prob.cum_probs)
+    for k in range(warmup):
+        solvers._device_step(eng, st, int(sched[k]), prm)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+    stream = torch.cuda.current_stream(device)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    torch.cuda.synchronize()
+    for k, (a, c) in enumerate(ev):
+        flush.zero_()
+        a.record(stream)
+        solvers._device_step(eng, st, int(sched[warmup + k]), prm)
+        c.record(stream)
+    torch.cuda.synchronize()
+    ms = np.array([a.elapsed_time(c) for a, c in ev])
+    return {"config": f"{cfg.name}: {cfg.side}^2, {cfg.n_angles} angles x {cfg.n_det} bins, r={r}",
+            "value": steps / (ms.sum() / 1e3), "unit": "iter/s", "steps": steps,
+            "l2": "flushed between steps"}
 
 
 # ---------------------------------------------------------------- native arm
@@ -296,13 +463,27 @@ def main():
         t0 = time.perf_counter()
         ips, det = cpu_reference(cfg, args.steps, args.warmup)
         cores = det["threads"]
+        # the largest config whose full operator the reference's CSR route builds in
+        # about a minute (and ~28 GB) is C; smaller configs time themselves
+        full_key = args.config if args.config in ("A", "B", "C") else "C"
+        full_c = None if args.no_full_reference else cpu_reference_full(full_key)
         line = dict(base, impl="reference", value=ips, ms_per_step=1e3 / ips,
+                    extrapolated=True,
                     config=dict(workload, l2="n/a (CPU)"),
                     cpu_baseline={"value": ips, "unit": "iter/s", "cores": cores, "kind": "port",
-                                  "sample": det["sample"]},
+                                  "sample": det["sample"], "extrapolated": True,
+                                  "single_core_value": det.get("single_core_iters_per_s")},
                     e2e={"value": ips, "unit": "iter/s", "h2d_bytes_per_step": 0,
                          "d2h_bytes_per_step": 0},
-                    reference_detail=dict(det, wall_s=round(time.perf_counter() - t0, 2)))
+                    measured_full_operator=full_c,
+                    reference_detail=dict(det, wall_s=round(time.perf_counter() - t0, 2),
+                                          timing_note=(
+                                              "value and ms_per_step are the per-step time of the "
+                                              "full config-D step modelled from timed sampled-angle "
+                                              "steps (extrapolated: the full CSR needs ~130 GB and "
+                                              "~5 min to build); measured_full_operator is a "
+                                              "fully timed, non-extrapolated reference solve "
+                                              "(config C for D)")))
         print(json.dumps(line))
         return
 
@@ -355,8 +536,13 @@ def main():
         if world > 1:
             torch.distributed.barrier()
 
-    # warm-up; the per-level CUDA graphs are captured here, never inside the timed region
+    # warm-up; the per-level CUDA graphs are captured (and uploaded) here, never inside
+    # the timed region, and every one of them (each level at both dual-buffer
+    # parities) is launched once before the W schedule steps
     eng.capture_all(st, prm)
+    for lv in range(r):
+        for _ in range(2):
+            solvers._device_step(eng, st, lv, prm)
     for k in range(args.warmup):
         solvers._device_step(eng, st, int(sched[k]), prm)
     torch.cuda.synchronize()
@@ -392,6 +578,10 @@ def main():
     lev = np.asarray(sched[args.warmup:])
     per_level_ms = {f"f{2 ** (r - 1 - i)}": round(float(step_ms[lev == i].mean()), 4)
                     for i in range(r) if np.any(lev == i)}
+    # the sampled schedule's level mix varies with K; the uniform-probability
+    # expectation over the same per-level means does not
+    uniform_ips = (1e3 / float(np.mean(list(per_level_ms.values())))
+                   if len(per_level_ms) == r else None)
 
     if args.steps_only:
         if rank == 0:
@@ -578,13 +768,15 @@ def main():
 
     micro = None
     if not args.no_microbench and world == 1:
-        micro = projector_microbench(device)
+        micro = projector_microbench(device, smem_peak_gbs=smem_peak, hbm_peak_gbs=hbm_peak)
+    config_c = native_config_c(device) if (world == 1 and not args.no_microbench) else None
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0:
         cps, det = cpu_reference(cfg, args.steps, args.warmup)
         cpu = {"value": cps, "unit": "iter/s", "cores": det["threads"], "kind": "port",
-               "sample": det["sample"], "per_level_s": det["per_level_s"]}
+               "sample": det["sample"], "per_level_s": det["per_level_s"], "extrapolated": True,
+               "single_core_value": det["single_core_iters_per_s"]}
 
     clocks = summarize_clocks(clk_path, local) if rank == 0 else None
     if rank == 0:
@@ -593,7 +785,13 @@ def main():
                                              "per-step CUDA events)"),
                     e2e=e2e, roofline=roofline, cpu_baseline=cpu, clocks=clocks,
                     projector_microbench=micro,
-                    gpu_launches=launches, per_level_ms=per_level_ms, level_counts=level_counts)
+                    gpu_launches=launches, per_level_ms=per_level_ms, level_counts=level_counts,
+                    uniform_expectation={
+                        "value": uniform_ips, "unit": "iter/s",
+                        "note": "1 / (mean of per_level_ms over the r levels): the expected rate "
+                                "under the uniform level probabilities, independent of how often "
+                                "this K-step schedule drew each level"},
+                    config_C=config_c)
         print(json.dumps(line))
         try:
             os.remove(clk_path)

@@ -1123,6 +1123,8 @@ int imask_step_graph_create(imask_plan* pl, const imask_state* st, int level0,
   int n_launch = 0;
   rc = capture_step(pl, st, level0, prm, &gr->graph, &n_launch);
   if (!rc) rc = cuda_check(cudaGraphInstantiate(&gr->exec, gr->graph, 0), "graph instantiate");
+  // upload the executable graph now, so its first launch does not pay for it
+  if (!rc) rc = cuda_check(cudaGraphUpload(gr->exec, pl->aux2.stream), "graph upload");
   if (rc) {
     imask_graph_destroy(gr);
     return rc;
@@ -1154,6 +1156,10 @@ int imask_step_graph_update(imask_graph* gr, imask_plan* pl, const imask_state* 
     }
     cudaGraphExecDestroy(gr->exec);
     gr->exec = exec;
+    if ((rc = cuda_check(cudaGraphUpload(gr->exec, pl->aux2.stream), "graph upload"))) {
+      cudaGraphDestroy(fresh);
+      return rc;
+    }
   }
   if (gr->graph) cudaGraphDestroy(gr->graph);
   gr->graph = fresh;
