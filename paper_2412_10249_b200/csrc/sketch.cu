@@ -235,17 +235,20 @@ __device__ __forceinline__ float saga_px(float pn, float& tab, float& sum, float
 __global__ void __launch_bounds__(256)
 k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, ImageSaga sg) {
   __shared__ __align__(16) Pyr32Smem sm;
-  griddep_wait();  // bp comes from the stream predecessor (the adjoint reduction)
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
   const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
   const size_t g = (size_t)(y0 + py) * side + x0 + px;
+  // the table row, the sum and x were last written by the previous step, which
+  // completed before this step's adjoint (a plain launch) started: they are
+  // loaded before the programmatic wait, overlapping the adjoint's tail
+  float4 tab = *reinterpret_cast<const float4*>(sg.phi_tab + g);
+  float4 sum = *reinterpret_cast<const float4*>(sg.phi_sum + g);
+  float4 xv = *reinterpret_cast<const float4*>(sg.x + g);
+  griddep_wait();  // bp (or the split planes) come from the stream predecessor (the adjoint)
   // planes summed in order (step_image fuses the reduction here only when the
   // reduce kernels would use that order too)
   const float4 v = sg.n_planes > 0 ? planes_sum4(sg, g)
                                    : __ldg(reinterpret_cast<const float4*>(bp + g));
-  float4 tab = *reinterpret_cast<const float4*>(sg.phi_tab + g);
-  float4 sum = *reinterpret_cast<const float4*>(sg.phi_sum + g);
-  float4 xv = *reinterpret_cast<const float4*>(sg.x + g);
   const float4 xo = xv;
   const float4 pn = comp32(v, cp, sm);
   saga_px(pn.x, tab.x, sum.x, xv.x, sg);
@@ -263,10 +266,21 @@ k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, Image
 __global__ void __launch_bounds__(256)
 k_saga_image_coarse32(const float* __restrict__ bp, int side, int lg, float inv_f2, ImageSaga sg) {
   __shared__ float cv[256];  // the tile's (32/f)^2 coarse backprojection values (planes mode)
-  griddep_wait();  // bp (or the split planes) come from the stream predecessor (the adjoint)
   const int n = side >> lg;
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
   const int lt = 5 - lg, tc = 1 << lt;  // coarse pixels per tile side
+  const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
+  const int row = y0 + py, col = x0 + px;
+  const size_t g = (size_t)row * side + col;
+  const int qrow = (row >> lg) * n;
+  // state written by the previous step (complete before this step's adjoint, a
+  // plain launch, started): loaded before the programmatic wait
+  float4 sum = *reinterpret_cast<const float4*>(sg.phi_sum + g);
+  float4 xv = *reinterpret_cast<const float4*>(sg.x + g);
+  float po[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) po[k] = sg.phi_tab[qrow + ((col + k) >> lg)];
+  griddep_wait();  // bp (or the split planes) come from the stream predecessor (the adjoint)
   if (sg.n_planes > 0) {
     // sum the adjoint's split planes for this tile's coarse pixels in the order of
     // k_adjoint_reduce_warp (many planes, few pixels) or k_adjoint_reduce
@@ -291,14 +305,8 @@ k_saga_image_coarse32(const float* __restrict__ bp, int side, int lg, float inv_
     }
     __syncthreads();
   }
-  const int py = threadIdx.x >> 3, px = (threadIdx.x & 7) * 4;
-  const int row = y0 + py, col = x0 + px;
-  const size_t g = (size_t)row * side + col;
-  const int qrow = (row >> lg) * n;
-  float4 sum = *reinterpret_cast<const float4*>(sg.phi_sum + g);
-  float4 xv = *reinterpret_cast<const float4*>(sg.x + g);
   const float4 xo = xv;
-  float pn[4], po[4];
+  float pn[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int q = qrow + ((col + k) >> lg);
@@ -306,7 +314,6 @@ k_saga_image_coarse32(const float* __restrict__ bp, int side, int lg, float inv_
                         ? cv[(((row >> lg) - (y0 >> lg)) << lt) + ((col + k) >> lg) - (x0 >> lg)]
                         : __ldg(bp + q);
     pn[k] = b * inv_f2;
-    po[k] = sg.phi_tab[q];
   }
   float d;
   d = pn[0] - po[0]; { const float xi = d + sum.x; sum.x = fmaf(sg.p_i, d, sum.x); xv.x = fmaf(-sg.s, xi, xv.x) * sg.inv_den; }
@@ -463,11 +470,12 @@ k_saga_image_full(const float* __restrict__ bp, int side, CompParams cp, ImageSa
 template <bool kVec>
 __global__ void __launch_bounds__(256)
 k_saga_sino(const float* __restrict__ psi_new, size_t m, SinoSaga sg) {
-  griddep_wait();  // psi_new comes from the stream predecessor (the forward)
   const size_t q4 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (kVec && q4 + 4 <= m) {
-    // every operand 16-byte aligned: one 128-bit access per array and thread
-    const float4 v = __ldg(reinterpret_cast<const float4*>(psi_new + q4));
+    // every operand 16-byte aligned: one 128-bit access per array and thread.
+    // y, b, the table row and the sum were last written by the previous step,
+    // complete before this step's staging (a plain launch) started: loaded
+    // before the programmatic wait
     const float4 yv = *reinterpret_cast<const float4*>(sg.y_in + q4);
     const float4 bv = __ldg(reinterpret_cast<const float4*>(sg.b + q4));
     float4 po = make_float4(0.f, 0.f, 0.f, 0.f), ps = po;
@@ -475,6 +483,8 @@ k_saga_sino(const float* __restrict__ psi_new, size_t m, SinoSaga sg) {
       po = *reinterpret_cast<const float4*>(sg.psi_tab + q4);
       ps = *reinterpret_cast<const float4*>(sg.psi_sum + q4);
     }
+    griddep_wait();  // psi_new comes from the stream predecessor (the forward)
+    const float4 v = __ldg(reinterpret_cast<const float4*>(psi_new + q4));
     const float vals[4] = {v.x, v.y, v.z, v.w}, pos[4] = {po.x, po.y, po.z, po.w},
                 pss[4] = {ps.x, ps.y, ps.z, ps.w}, ys[4] = {yv.x, yv.y, yv.z, yv.w},
                 bs[4] = {bv.x, bv.y, bv.z, bv.w};
@@ -494,6 +504,7 @@ k_saga_sino(const float* __restrict__ psi_new, size_t m, SinoSaga sg) {
     }
     *reinterpret_cast<float4*>(sg.y + q4) = make_float4(ny[0], ny[1], ny[2], ny[3]);
   } else {
+    griddep_wait();
     for (size_t q = q4; q < m && q < q4 + 4; ++q) sino_update(sg, q, sino_load(sg, q), psi_new[q]);
   }
 }
