@@ -735,7 +735,7 @@ def main():
         prob_w = dist_mod.make_sharded_problem(geom, b_host.to(device), fam, cfg.mu_g,
                                                rank, world, group)
         prob_w.engine.capture_all(solvers.init_state(prob_w, seed=SEED), prm)
-        solvers.run(prob_w, "sketch", SIGMA, cfg.mu_g, 3, record_every=1, seed=SEED,
+        solvers.run(prob_w, "sketch", SIGMA, cfg.mu_g, e2e_steps, record_every=1, seed=SEED,
                     x_ref=xref_host.to(device))
         del prob_w
         x_out = torch.empty(cfg.d, dtype=torch.float32).pin_memory()

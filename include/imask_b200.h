@@ -275,6 +275,14 @@ IMASK_API int imask_last_launch_count(void);
 #define IMASK_SQDIST_SCRATCH 298
 IMASK_API int imask_sq_dist(const float* x, const float* ref, int64_t n, double* out,
                             double* result, void* stream);
+/* One metric row of run() (solvers.py:403-405) recorded on the device: with
+ * k = rows[0] read as a uint64 counter, rows[2 + 2k] = ||x - ref||^2 (float64,
+ * fixed order; n = 0 gives 0) and rows[3 + 2k] = the device global timer in ns
+ * when it was final; the counter then advances. `rows` is device memory of
+ * 2 + 2 * capacity doubles with rows[0] = 0 initially; `scratch` as for
+ * imask_sq_dist. A run's rows are read back once at the end. */
+IMASK_API int imask_metric_row(const float* x, const float* ref, int64_t n, double* scratch,
+                               double* rows, void* stream);
 
 /* TV + nonnegativity prox (prox_tv_nonneg, proxlib.py:102-148):
  * out = argmin_u 0.5||u - xp||^2 + sigma mu_g ||grad u||_{1,2} + [u >= 0]

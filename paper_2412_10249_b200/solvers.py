@@ -309,6 +309,7 @@ class SaddleState:
     bp: Optional[torch.Tensor] = None
     y_alt: Optional[torch.Tensor] = None  # second dual buffer: y^{k+1} is written here, then swapped
     parity: int = 0  # how many dual swaps mod 2 (which buffer is current)
+    b_bound: Optional[torch.Tensor] = None  # run()'s private copy of b (stable pointer)
     _cstates: dict = field(default_factory=dict, repr=False)
 
     def phi_full(self, i: int, family: SketchFamily) -> torch.Tensor:
@@ -323,6 +324,8 @@ class SaddleState:
 
     def c_state(self, b: torch.Tensor) -> _lib.ImaskState:
         """The C view of this state for the current dual buffer."""
+        if self.b_bound is not None:
+            b = self.b_bound
         key = (self.y.data_ptr(), b.data_ptr(),
                None if self.xbar is None else self.xbar.data_ptr())
         cs = self._cstates.get(key)
@@ -355,21 +358,58 @@ def init_state(prob: Problem, seed: int = 0, x0=None, y0=None, exact_memory: boo
     """
     if prob.engine is None or ops is not None or sum_weights is not None:
         return _init_generic(prob, seed, x0, y0, exact_memory, sum_weights, ops, resum_every)
+    return _init_engine(prob, seed, x0, y0, exact_memory, resum_every,
+                        torch.empty(_engine_state_len(prob.engine, prob.r), device=prob.engine.device))
+
+
+_ALIGN = 64  # floats: every part of a state buffer starts 256-byte aligned (128-bit kernels)
+
+
+def _state_parts(eng: Engine, r: int) -> list:
+    d, m = eng.d, eng.m_loc
+    return [("x", d), ("xbar", d), ("phi_sum", d), ("bp", d), ("y", m), ("y_alt", m),
+            ("psi_sum", m), ("b", m), ("psi_tab", r * m), ("phi_tab", eng.plan.phi_tab_len)]
+
+
+def _aligned(n: int) -> int:
+    return (n + _ALIGN - 1) // _ALIGN * _ALIGN
+
+
+def _engine_state_len(eng: Engine, r: int) -> int:
+    return sum(_aligned(size) for _, size in _state_parts(eng, r))
+
+
+def _init_engine(prob: Problem, seed, x0, y0, exact_memory, resum_every,
+                 flat: torch.Tensor, bind_b: bool = False) -> SaddleState:
+    """Engine-layout state carved out of one flat device buffer: x, xbar,
+    phi_sum, bp (d each), y, y_alt, psi_sum, b copy (m each), the r psi rows
+    and the compact phi table."""
     eng = prob.engine
     dev = eng.device
     d, m, r = eng.d, eng.m_loc, prob.r
-    x = torch.zeros(d, device=dev) if x0 is None else to_device(x0, dev).clone()
-    y = torch.zeros(m, device=dev) if y0 is None else to_device(y0, dev).clone()
     plan = eng.plan
-    phi_tab = torch.zeros(plan.phi_tab_len, device=dev)
-    psi_tab = torch.zeros(r * m, device=dev)
+    flat.zero_()
+    parts, off = {}, 0
+    for name, size in _state_parts(eng, r):
+        parts[name] = flat[off:off + size]
+        off += _aligned(size)
+    x, y = parts["x"], parts["y"]
+    if x0 is not None:
+        x.copy_(to_device(x0, dev))
+    if y0 is not None:
+        y.copy_(to_device(y0, dev))
+    parts["xbar"].copy_(x)
+    phi_tab, psi_tab = parts["phi_tab"], parts["psi_tab"]
     phi = [phi_tab[o:o + (eng.geom.side // f) ** 2] for o, f in zip(plan.phi_offsets, plan.factors)]
     psi = [psi_tab[i * m:(i + 1) * m] for i in range(r)]
+    b_bound = None
+    if bind_b:
+        b_bound = parts["b"]
+        b_bound.copy_(eng.b)
     st = SaddleState(
-        x=x, y=y, phi=phi, psi=psi, phi_sum=torch.zeros(d, device=dev),
-        psi_sum=torch.zeros(m, device=dev), seed=seed, xbar=x.clone(), resum_every=resum_every,
-        phi_tab=phi_tab, psi_tab=psi_tab, bp=torch.empty(d, device=dev),
-        y_alt=torch.empty(m, device=dev),
+        x=x, y=y, phi=phi, psi=psi, phi_sum=parts["phi_sum"], psi_sum=parts["psi_sum"],
+        seed=seed, xbar=parts["xbar"], resum_every=resum_every, phi_tab=phi_tab,
+        psi_tab=psi_tab, bp=parts["bp"], y_alt=parts["y_alt"], b_bound=b_bound,
     )
     if exact_memory:
         for i in range(r):
@@ -689,12 +729,13 @@ def _metrics(x: torch.Tensor, x_ref: Optional[torch.Tensor]):
 
 
 class _Recorder:
-    """Metric rows of run() without a host synchronisation per row.
+    """Metric rows of run() without host work per row.
 
-    A row's ||x - x_ref||^2 is reduced on the device (imask_sq_dist, float64,
-    fixed order) and read back with an asynchronous 8-byte copy into pinned
-    memory; its time stamp is a CUDA event on the same stream. rows() waits
-    once and evaluates rel_dist / psnr exactly as _metrics does.
+    A row's ||x - x_ref||^2 is reduced on the device (imask_metric_row: float64,
+    fixed order) into the next slot of a device row buffer together with the
+    device's global timer; rows() reads the buffer back once and evaluates
+    rel_dist / psnr exactly as _metrics does (solvers.py:382-390). The seconds
+    column is the host time of the first row plus the device time elapsed since.
     """
 
     def __init__(self, x_ref: Optional[torch.Tensor], device: torch.device, capacity: int,
@@ -705,53 +746,41 @@ class _Recorder:
         self.ref_sq = (float(torch.dot(x_ref.double(), x_ref.double()))
                        if x_ref is not None else float("nan"))
         self.scratch = torch.zeros(_lib.IMASK_SQDIST_SCRATCH, dtype=torch.float64, device=device)
-        self.dev_rows = torch.zeros(max(capacity, 1), dtype=torch.float64, device=device)
-        self.host = torch.zeros(max(capacity, 1), dtype=torch.float64).pin_memory()
-        # read-backs ride a side stream so the solver stream never waits for a copy
-        self.copy_stream = torch.cuda.Stream(device=device)
+        self.dev_rows = torch.zeros(2 + 2 * max(capacity, 1), dtype=torch.float64, device=device)
         self.meta: list = []
-        self.events: list = []
-        self.ev0 = torch.cuda.Event(enable_timing=True)
-        self.ev0.record(torch.cuda.current_stream(device))
-        self.t_ev0 = time.perf_counter() - t0
+        self.t0 = t0
+        self.t_first: Optional[float] = None
+        self._ref_ptr = ctypes.c_void_p(0 if x_ref is None else x_ref.data_ptr())
+        self._scratch_ptr = ctypes.c_void_p(self.scratch.data_ptr())
+        self._rows_ptr = ctypes.c_void_p(self.dev_rows.data_ptr())
+        self._stream = ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
     def record(self, k: int, cost: float, level: int, x: torch.Tensor) -> None:
-        idx = len(self.meta)
-        stream = torch.cuda.current_stream(self.device)
-        if self.ref is not None:
-            if x.numel() != self.ref.numel() or x.dtype != torch.float32:
-                raise ValueError("x_ref must match the iterate's shape")
-            _lib.check(_lib.lib().imask_sq_dist(
-                ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(self.ref.data_ptr()), x.numel(),
-                ctypes.c_void_p(self.scratch.data_ptr()),
-                ctypes.c_void_p(self.dev_rows[idx:idx + 1].data_ptr()),
-                ctypes.c_void_p(stream.cuda_stream)))
-        ev = torch.cuda.Event(enable_timing=True)
-        ev.record(stream)
-        if self.ref is not None:
-            self.copy_stream.wait_event(ev)
-            with torch.cuda.stream(self.copy_stream):
-                self.host[idx:idx + 1].copy_(self.dev_rows[idx:idx + 1], non_blocking=True)
+        if self.t_first is None:
+            self.t_first = time.perf_counter() - self.t0
+        if self.ref is not None and (x.numel() != self.ref.numel() or x.dtype != torch.float32):
+            raise ValueError("x_ref must match the iterate's shape")
+        if len(self.meta) >= (self.dev_rows.numel() - 2) // 2:
+            raise RuntimeError("metric row buffer full")
+        _lib.check(_lib.lib().imask_metric_row(
+            ctypes.c_void_p(x.data_ptr()), self._ref_ptr,
+            0 if self.ref is None else x.numel(), self._scratch_ptr, self._rows_ptr,
+            self._stream))
         self.meta.append((k, cost, level, x.numel()))
-        self.events.append(ev)
 
     def rows(self) -> list:
-        if self.events:
-            self.events[-1].synchronize()
-        self.copy_stream.synchronize()
-        # one numpy view of the pinned read-backs (per-element tensor indexing
-        # costs microseconds a row)
-        host = self.host.numpy()
-        elapsed = self.ev0.elapsed_time
+        host = self.dev_rows[:2 + 2 * len(self.meta)].cpu().numpy()
         out = []
-        for idx, ((k, cost, level, d), ev) in enumerate(zip(self.meta, self.events)):
+        ts0 = host[3] if self.meta else 0.0
+        for idx, (k, cost, level, d) in enumerate(self.meta):
             if self.ref is None:
                 rel = snr = float("nan")
             else:
-                err = float(host[idx])
+                err = float(host[2 + 2 * idx])
                 rel = err / self.ref_sq if self.ref_sq > 0 else float("nan")
                 snr = 300.0 if err == 0.0 else min(300.0, 10.0 * math.log10(d / err))
-            out.append((k, cost, level, rel, snr, self.t_ev0 + elapsed(ev) / 1e3))
+            secs = self.t_first + (float(host[3 + 2 * idx]) - ts0) * 1e-9
+            out.append((k, cost, level, rel, snr, secs))
         return out
 
 
@@ -896,8 +925,21 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
     t0 = time.perf_counter()
     snapshots: dict = {}
     budgets = sorted(float(cb) for cb in snapshot_costs)
-    state = init_state(prob, seed=seed, resum_every=resum_every)
-    if not fused:
+    pooled = None
+    if fused:
+        # run()'s state is private: its buffers come from (and go back to) a pool
+        # kept with the plan, so consecutive solves on one geometry reuse the same
+        # device addresses and the cached step graphs need no re-targeting
+        pool = eng.plan.state_pool
+        need = _engine_state_len(eng, prob.r)
+        pooled = next((t for t in pool if t.numel() == need), None)
+        if pooled is not None:
+            pool.remove(pooled)
+        else:
+            pooled = torch.empty(need, device=dev)
+        state = _init_engine(prob, seed, None, None, False, resum_every, pooled, bind_b=True)
+    else:
+        state = init_state(prob, seed=seed, resum_every=resum_every)
         _to_generic(state, eng.family if eng is not None else None)
     prm = eng.params(sigma, mu) if fused else None
     schedule = draw_levels(seed, 0, iters, prob.cum_probs)
@@ -907,9 +949,26 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
     record = rec.record
 
     record(0, 0.0, 0, state.x)
+    # single-GPU fused steps: the (level, dual parity) -> step graph map is
+    # resolved once per run (the state's buffers do not change within it), so
+    # an iteration is one graph launch plus the ledger
+    fast = (fused and not seq and eng.use_graphs and not eng.shard.collective)
+    graphs: dict = {}
+    launch = _lib.lib().imask_graph_launch
+    stream = eng.plan.stream if eng is not None else None
     for k in range(1, iters + 1):
         i = int(schedule[k - 1])
-        if not fused:
+        if fast:
+            h = graphs.get((i, state.parity))
+            if h is None:
+                h = eng.graph(state, i, prm)[0]
+                graphs[(i, state.parity)] = h
+            rc = launch(h, stream)
+            if rc:
+                _lib.check(rc)
+            state.swap_dual()
+            _advance(state, prob, i)
+        elif not fused:
             if saga_ops is not None:
                 saga_saddle_step(state, saga_ops, prob.probs, prob.g, prob.f_conj, sigma / mu,
                                  sigma, cum_probs=prob.cum_probs, fractions=prob.fractions)
@@ -931,8 +990,11 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
             snapshots[budgets.pop(0)] = state.x.clone()
         if k % record_every == 0 or k == iters:
             record(k, state.cost, state.last_level, state.x)
-    rows = rec.rows()
-    return SolveReport(rows=rows, x=state.x, y=state.y, algorithm=algorithm, seed=seed,
+    x_out, y_out = (state.x.clone(), state.y.clone()) if pooled is not None else (state.x, state.y)
+    rows = rec.rows()  # (synchronises: every step has completed)
+    if pooled is not None:
+        eng.plan.state_pool.append(pooled)
+    return SolveReport(rows=rows, x=x_out, y=y_out, algorithm=algorithm, seed=seed,
                        snapshots=snapshots)
 
 
