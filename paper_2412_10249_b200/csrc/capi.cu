@@ -70,6 +70,44 @@ struct imask_graph {
   int device = 0;
 };
 
+namespace imask {
+
+namespace {
+const char* const kKnobNames[(int)Knob::kCount] = {
+    "IMASK_NO_TMA", "IMASK_NO_QUAD", "IMASK_NO_QUAD_L1", "IMASK_FWD_VAL", "IMASK_FWD_VAL_L1",
+    "IMASK_TMA_MIN_N", "IMASK_ADJ_AFTER_STAGE_MIN_N", "IMASK_SAGA_SPLIT_MIN_N",
+    "IMASK_ADJ_WIN_KB", "IMASK_ADJ_CLUSTER", "IMASK_ADJ_TILE", "IMASK_ADJ_CTAS"};
+
+const char* knob_raw(Knob k) {
+  static const char* vals[(int)Knob::kCount];
+  static std::once_flag once;
+  std::call_once(once, [] {
+    for (int i = 0; i < (int)Knob::kCount; ++i) vals[i] = std::getenv(kKnobNames[i]);
+  });
+  return vals[(int)k];
+}
+}  // namespace
+
+int knob(Knob k, int dflt) {
+  const char* e = knob_raw(k);
+  if (!e) return dflt;
+  return *e ? std::atoi(e) : 1;
+}
+
+int knob_for_factor(Knob k, int factor, int dflt) {
+  const char* e = knob_raw(k);
+  int v = dflt;
+  for (const char* q = e; q && *q;) {
+    int ff = 0, vv = 0;
+    if (std::sscanf(q, "%d:%d", &ff, &vv) == 2 && ff == factor) v = vv;
+    while (*q && *q != ',') ++q;
+    if (*q) ++q;
+  }
+  return v;
+}
+
+}  // namespace imask
+
 using namespace imask;
 
 namespace {
@@ -278,8 +316,7 @@ int get_tables(imask_plan* pl, int f, LevelTables** out) {
                       "cudaMemcpy");
       if (rc) return rc;
     }
-    static const bool no_tma = std::getenv("IMASK_NO_TMA") != nullptr;  // debugging / A-B runs
-    if (pl->sym && !no_tma) {
+    if (pl->sym && !knob(Knob::kNoTma, 0)) {
       const int n = pl->side / f;
       const unsigned bh = pl->tma_quad ? 8 : 16;
       t.tma = encode_pair_map(&t.maps.row, pl->P, n, bh) &&
@@ -336,26 +373,18 @@ int run_adjoint(imask_plan* pl, int f, const float* sino, float* out, const AdjA
 // the wait), so there the order applies from n = 512; an angle shard keeps it
 // from n = 256 (1/8 shard, f=4: 53 us with the wait, 63 us without).
 bool adjoint_after_staging(const imask_plan* pl, int level0) {
-  static const int forced = [] {
-    const char* e = std::getenv("IMASK_ADJ_AFTER_STAGE_MIN_N");  // tuning / A-B runs
-    return e ? std::atoi(e) : 0;
-  }();
+  const int forced = knob(Knob::kAdjAfterStageMinN, 0);
   const int min_n = forced > 0 ? forced : (2 * pl->n_loc > pl->n_angles ? 512 : 256);
   return pl->side / pl->factors[level0] >= min_n;
 }
 
 // TMA staging pays off where the band walks are long; coarse grids use L1 loads
 bool forward_uses_tma(const imask_plan* pl, const LevelTables* t, int n) {
-  static const int tma_min_n = [] {
-    const char* e = std::getenv("IMASK_TMA_MIN_N");  // tuning / A-B runs
-    return e ? std::atoi(e) : 128;
-  }();
-  return t->tma && pl->tma_entries && n >= tma_min_n;
+  return t->tma && pl->tma_entries && n >= knob(Knob::kTmaMinN, 128);
 }
 
 bool forward_quad_l1(const imask_plan* pl) {
-  static const bool no_quad_l1 = std::getenv("IMASK_NO_QUAD_L1") != nullptr;  // A-B runs
-  return pl->tma_quad && !no_quad_l1;
+  return pl->tma_quad && !knob(Knob::kNoQuadL1, 0);
 }
 
 // Whether the forward run_forward picks at this level reads the difference
@@ -467,10 +496,7 @@ int forward_saga(imask_plan* pl, const imask_state* st, int level0, const imask_
   sg.p_i = (float)pl->probs[level0];
   sg.sigma = (float)prm->sigma;
   sg.inv_1ps = (float)(1.0 / (1.0 + prm->sigma));
-  static const int split_forced = [] {
-    const char* e = std::getenv("IMASK_SAGA_SPLIT_MIN_N");  // tuning / A-B runs
-    return e ? std::atoi(e) : 0;
-  }();
+  const int split_forced = knob(Knob::kSagaSplitMinN, 0);
   // measured: a win from n = 1024 with the two-plane forward; with value-plane
   // staging (the whole angle set) from n = 512 too (f=2 step 401 -> 378 us)
   const int split_min_n =
@@ -623,8 +649,7 @@ int imask_plan_create_list(int side, int n_angles, int n_det, int n_loc, const i
     // too: the singles 0 and n/2 (a transposed-family entry), entries
     // (a, n-a, n/2-a, n/2+a) for 0 < a < n/4, then the pair (n/4, 3n/4)
     std::vector<int4> qent;
-    static const bool no_quad = std::getenv("IMASK_NO_QUAD") != nullptr;  // A-B runs
-    if (n_angles % 4 == 0 && !no_quad) {
+    if (n_angles % 4 == 0 && !knob(Knob::kNoQuad, 0)) {
       std::vector<int> loc(n_angles, -1);
       for (int i = 0; i < n_loc; ++i) loc[angle_idx[i]] = i;
       const int h = n_angles / 2, qn = n_angles / 4;

@@ -42,6 +42,32 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 constexpr double kFix = 4294967296.0;  // 2^32
 
+// Path and tuning switches, read once from the environment (host code only).
+// Unset, the product defaults apply. They exist to select the alternative
+// code paths the bit-identity tests compare (IMASK_NO_QUAD, IMASK_NO_TMA,
+// IMASK_FWD_VAL, IMASK_FWD_VAL_L1) and for A/B measurement runs (the others,
+// tools/gpu_ab_env.sh); DESIGN.md lists what each one measured.
+enum class Knob {
+  kNoTma,            // IMASK_NO_TMA: forward through L1 loads only
+  kNoQuad,           // IMASK_NO_QUAD: pair (mirror-only) entries, no four-ray quads
+  kNoQuadL1,         // IMASK_NO_QUAD_L1: coarse levels through the pair L1 kernel
+  kFwdVal,           // IMASK_FWD_VAL (0/1): TMA forward value-plane staging forced off/on
+  kFwdValL1,         // IMASK_FWD_VAL_L1 (0/1): L1 quad forward value planes
+  kTmaMinN,          // IMASK_TMA_MIN_N: smallest coarse side on the TMA forward (128)
+  kAdjAfterStageMinN,  // IMASK_ADJ_AFTER_STAGE_MIN_N: step order threshold
+  kSagaSplitMinN,    // IMASK_SAGA_SPLIT_MIN_N: separate sinogram SAGA pass threshold
+  kAdjWinKb,         // IMASK_ADJ_WIN_KB: adjoint window budget per CTA (20)
+  kAdjCluster,       // IMASK_ADJ_CLUSTER: adjoint cluster size (1 = none)
+  kAdjTile,          // IMASK_ADJ_TILE: "f:T,..." adjoint tile per factor
+  kAdjCtas,          // IMASK_ADJ_CTAS: "f:ctas_per_sm,..." adjoint split target
+  kCount
+};
+// Integer value of a switch, or `dflt` when unset (a set-but-valueless flag
+// reads as 1).
+int knob(Knob k, int dflt);
+// Per-factor value of a "f:v,f:v" list switch, or `dflt`.
+int knob_for_factor(Knob k, int factor, int dflt);
+
 // Zero columns on each side of every pair-image row (see k_forward): a lane
 // walking its warp's band range outside its own valid range is at most
 // 31*sqrt(2) < 48 columns from a lane inside it, so it reads zeros instead of

@@ -702,10 +702,7 @@ int sm_count() {
 // bound along each CTA's band walk, where the extra packed subtractions cost
 // (1/8 and 1/4 shards' f=1 forward +7% / +15%), so it stages both planes.
 bool forward_tma_val(int ctas) {
-  static const int forced = [] {
-    const char* e = std::getenv("IMASK_FWD_VAL");  // tuning / A-B runs: 0 or 1
-    return e ? std::atoi(e) : -1;
-  }();
+  const int forced = knob(Knob::kFwdVal, -1);
   if (forced == 0 || forced == 1) return forced == 1;
   return ctas >= 6 * sm_count();
 }
@@ -1082,11 +1079,7 @@ __global__ void k_adjoint_reduce(const float* __restrict__ part, float* __restri
 // The L1 quad forward forms the difference pairs from the value planes: half
 // the L1 footprint (f=16 step 93.5 -> 91.5 us on one GPU).
 bool forward_l1_val() {
-  static const bool val = [] {
-    const char* e = std::getenv("IMASK_FWD_VAL_L1");  // tuning / A-B runs: 0 or 1
-    return e ? std::atoi(e) == 1 : true;
-  }();
-  return val;
+  return knob(Knob::kFwdValL1, 1) == 1;
 }
 
 cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, const float2* PTM,
@@ -1174,14 +1167,9 @@ void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_o
   // on 1/4 and 1/8 shards, which keep 8; at f = 32 16 is faster with the L2
   // warm (60.5 -> 54.8 us) but slower after an L2 flush (67 -> 70 us), so 8)
   int T = factor <= 2 ? 32 : (factor <= 8 || (factor <= 16 && n_loc >= 512) ? 16 : 8);
-  if (const char* e = getenv("IMASK_ADJ_TILE")) {  // tuning: "f:T,f:T,..."
-    for (const char* q = e; *q;) {
-      int ff = 0, tt = 0;
-      if (sscanf(q, "%d:%d", &ff, &tt) == 2 && ff == factor && (tt == 8 || tt == 16 || tt == 32))
-        T = tt;
-      while (*q && *q != ',') ++q;
-      if (*q) ++q;
-    }
+  {
+    const int tt = knob_for_factor(Knob::kAdjTile, factor, T);
+    if (tt == 8 || tt == 16 || tt == 32) T = tt;
   }
   int np2 = 8;
   while (np2 < n) np2 <<= 1;
@@ -1194,13 +1182,9 @@ void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_o
   // (factor 1 with many angles: 28 per SM, measured -1% on the whole-set step
   // with the value-plane forward beside it; a 1/4 or 1/8 shard is slower so)
   int per_sm = factor == 1 ? (n_loc >= 512 ? 28 : 20) : 16;
-  if (const char* e = getenv("IMASK_ADJ_CTAS")) {  // tuning: "f:ctas_per_sm,..."
-    for (const char* q = e; *q;) {
-      int ff = 0, cc = 0;
-      if (sscanf(q, "%d:%d", &ff, &cc) == 2 && ff == factor && cc > 0) per_sm = cc;
-      while (*q && *q != ',') ++q;
-      if (*q) ++q;
-    }
+  {
+    const int cc = knob_for_factor(Knob::kAdjCtas, factor, per_sm);
+    if (cc > 0) per_sm = cc;
   }
   const int target = per_sm * sm_count();
   int S = (target + tiles - 1) / tiles;
@@ -1211,11 +1195,8 @@ void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_o
   // 549 us with clusters of 8, f=4 118 -> 144 us; 2 and 4 in between): the
   // co-scheduling of a cluster's CTAs costs more SM time than the plane
   // round trip through L2 saves, so the default is no cluster (A/B knob).
-  static const int cz_max = [] {
-    const char* e = getenv("IMASK_ADJ_CLUSTER");  // tuning / A-B runs: cluster size, 1 = none
-    const int v = e ? atoi(e) : 1;
-    return v < 1 ? 1 : (v > 8 ? 8 : v);
-  }();
+  const int cz_knob = knob(Knob::kAdjCluster, 1);
+  const int cz_max = cz_knob < 1 ? 1 : (cz_knob > 8 ? 8 : cz_knob);
   const int cz = S < cz_max ? S : cz_max;
   S = (S / cz) * cz;
   *T_out = T;
@@ -1285,10 +1266,7 @@ static size_t adj_smem(bool pair, bool sym, int T, int W, int* CA_io) {
   const int G = kAdjThreads / lanes;
   const size_t elem = sizeof(float) * (pair ? 2 : 1) * (sym ? 2 : 1);
   // up to 32 angles per chunk, fewer for wide windows (keep ~7 CTAs per SM)
-  static const size_t cap = [] {
-    const char* e = getenv("IMASK_ADJ_WIN_KB");
-    return (size_t)(e ? atoi(e) : 20) * 1024;
-  }();
+  const size_t cap = (size_t)knob(Knob::kAdjWinKb, 20) * 1024;
   int CA = 32;
   while (CA > G && (size_t)CA * W * elem > cap) CA >>= 1;
   if (CA < G) CA = G;

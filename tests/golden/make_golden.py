@@ -139,6 +139,17 @@ def gen_proj_D_sampled():
             out[f"adj_f{f}_at_pix"] = bp[pix]
         else:
             out[f"adj_f{f}"] = bp
+    for f in (2, 4, 8, 16):  # the intermediate levels (sampled pixels on the fine grids)
+        low = cfg.side // f
+        mat = ctmodel.ray_matrix(low, float(f), g.angles[D_ANGLES], g.offsets)
+        out[f"fwd_f{f}"] = mat @ mrsketch.decimate(x, f).ravel()
+        bp = mat.T @ ys
+        if low * low > 65536:
+            pf = np.sort(rng.choice(low * low, size=4096, replace=False))
+            out[f"pix_f{f}"] = pf
+            out[f"adj_f{f}"] = bp[pf]
+        else:
+            out[f"adj_f{f}"] = bp
     save("proj_D_sampled.npz", **out)
 
 
