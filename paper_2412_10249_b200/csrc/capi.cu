@@ -61,7 +61,8 @@ struct TmaMaps {
 cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float2* PT,
                                const float2* PM, const float2* PTM, int n, const FwdAngle* ang,
                                const int4* entries, int n_entries, int row_ctas, bool quad,
-                               int n_det, float* sino, const SinoSaga* saga, cudaStream_t stream);
+                               int n_det, float* sino, const SinoSaga* saga, cudaStream_t stream,
+                               bool two_det);
 }  // namespace imask
 
 struct imask_graph {
@@ -76,7 +77,8 @@ namespace {
 const char* const kKnobNames[(int)Knob::kCount] = {
     "IMASK_NO_TMA", "IMASK_NO_QUAD", "IMASK_NO_QUAD_L1", "IMASK_FWD_VAL", "IMASK_FWD_VAL_L1",
     "IMASK_TMA_MIN_N", "IMASK_ADJ_AFTER_STAGE_MIN_N", "IMASK_SAGA_SPLIT_MIN_N",
-    "IMASK_ADJ_WIN_KB", "IMASK_ADJ_CLUSTER", "IMASK_ADJ_TILE", "IMASK_ADJ_CTAS"};
+    "IMASK_ADJ_WIN_KB", "IMASK_ADJ_CLUSTER", "IMASK_ADJ_TILE", "IMASK_ADJ_CTAS",
+    "IMASK_FWD_TWO_DET"};
 
 const char* knob_raw(Knob k) {
   static const char* vals[(int)Knob::kCount];
@@ -124,6 +126,8 @@ struct LevelTables {
   FwdAngle* fwd = nullptr;  // device
   AdjAngle* adj = nullptr;  // device
   bool tma = false;         // tensor maps of the pair images at this level are valid
+  bool two_det = false;     // every TMA entry's detectors are < 1 column apart (and ascend):
+                            // the two-detectors-per-thread forward applies
   TmaMaps maps{};           // boxes of 96 x 16 (pair mode) or 96 x 8 bands (quad mode)
 };
 
@@ -185,6 +189,7 @@ struct imask_plan {
                                 // quad mode (a, n-a, n/2-a, n/2+a); pair mode (a, n-a, -1, -1)
                                 // grouped by ray family
   int n_tma_entries = 0;
+  std::vector<int4> tma_entries_host;  // host copy of tma_entries
   int tma_row_ctas = 0;         // pair mode: CTAs [0, tma_row_ctas) hold row-family entries
   bool tma_quad = false;        // the local rows are closed under a -> n/2 - a as well
   float* u = nullptr;
@@ -316,6 +321,15 @@ int get_tables(imask_plan* pl, int f, LevelTables** out) {
                       "cudaMemcpy");
       if (rc) return rc;
     }
+    if (pl->sym && pl->tma_entries) {
+      // the two-detector forward needs 0 < xi_dj < 1 for every entry's parameter row
+      bool ok = f >= 2 && knob(Knob::kFwdTwoDet, 1) != 0;
+      for (const int4& e4 : pl->tma_entries_host) {
+        const int row = e4.x >= 0 ? e4.x : e4.z;
+        if (row >= 0 && !(fw[row].xi_dj > 0.0 && fw[row].xi_dj < 0.999)) ok = false;
+      }
+      t.two_det = ok;
+    }
     if (pl->sym && !knob(Knob::kNoTma, 0)) {
       const int n = pl->side / f;
       const unsigned bh = pl->tma_quad ? 8 : 16;
@@ -392,7 +406,8 @@ bool forward_quad_l1(const imask_plan* pl) {
 // so k_prepare skips those two planes for them (half its writes).
 bool forward_reads_diff(const imask_plan* pl, const LevelTables* t, int n) {
   if (!pl->sym) return false;  // plain layout: P holds (u, d) pairs itself
-  if (forward_uses_tma(pl, t, n)) return !forward_tma_val_grid(pl->n_det, pl->n_tma_entries);
+  if (forward_uses_tma(pl, t, n))
+    return !t->two_det && !forward_tma_val_grid(pl->n_det, pl->n_tma_entries);
   if (forward_quad_l1(pl)) return !forward_l1_val();
   return true;  // k_forward_sym
 }
@@ -412,7 +427,7 @@ int run_forward(imask_plan* pl, int f, const LevelTables* t, float* sino, const 
   if (forward_uses_tma(pl, t, n))
     e = launch_forward_tma(t->maps, pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->tma_entries,
                            pl->n_tma_entries, pl->tma_row_ctas, pl->tma_quad, pl->n_det, sino,
-                           saga, s);
+                           saga, s, t->two_det);
   else {
     const bool quad = forward_quad_l1(pl);
     e = launch_forward(pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->n_loc, pl->n_det,
@@ -692,6 +707,7 @@ int imask_plan_create_list(int side, int n_angles, int n_det, int n_loc, const i
       for (const int2& e2 : tent) tent4.push_back(make_int4(e2.x, e2.y, -1, -1));
     }
     pl->n_tma_entries = (int)tent4.size();
+    pl->tma_entries_host = tent4;
     if ((rc = cuda_check(cudaMalloc(&pl->tma_entries, sizeof(int4) * tent4.size()), "cudaMalloc")) ||
         (rc = cuda_check(cudaMemcpy(pl->tma_entries, tent4.data(), sizeof(int4) * tent4.size(),
                                     cudaMemcpyHostToDevice),

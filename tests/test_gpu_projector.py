@@ -231,12 +231,14 @@ def test_mirror_closed_shards_match_full(n_angles, world):
         assert rel_l2(bp_sum, ref) <= 1e-6
 
 
-@pytest.mark.parametrize("geom_args", [(1024, 1440, 1449, 1), (256, 360, 363, 1), (256, 360, 363, 2)])
+@pytest.mark.parametrize("geom_args", [(1024, 1440, 1449, 1), (1024, 1440, 1449, 2),
+                                       (1024, 1440, 1449, 8), (256, 360, 363, 1),
+                                       (256, 360, 363, 2), (256, 360, 363, 4)])
 def test_forward_paths_bit_identical(geom_args, tmp_path):
     """The four-ray (quad) TMA forward, the pair TMA forward and the L1 forward
     trace the same rays with the same arithmetic: bit-identical sinograms, with
     the difference pairs read from the difference planes or formed from the
-    value planes (P[c+1] - P[c]). The path switches are read once per process,
+    value planes (P[c+1] - P[c]), and with one or two detectors per thread. The path switches are read once per process,
     so each runs in a subprocess."""
     import subprocess
     import sys
@@ -247,7 +249,11 @@ def test_forward_paths_bit_identical(geom_args, tmp_path):
                             ("l1", {"IMASK_NO_TMA": "1"}),
                             ("quad_planes", {"IMASK_FWD_VAL": "0"}),
                             ("pair_planes", {"IMASK_NO_QUAD": "1", "IMASK_FWD_VAL": "0"}),
-                            ("l1_planes", {"IMASK_NO_TMA": "1", "IMASK_FWD_VAL_L1": "0"})):
+                            ("l1_planes", {"IMASK_NO_TMA": "1", "IMASK_FWD_VAL_L1": "0"}),
+                            # one detector per thread (f >= 2 default: two)
+                            ("one_det", {"IMASK_FWD_TWO_DET": "0"}),
+                            ("one_det_planes", {"IMASK_FWD_TWO_DET": "0", "IMASK_FWD_VAL": "0"}),
+                            ("pair_one_det", {"IMASK_NO_QUAD": "1", "IMASK_FWD_TWO_DET": "0"})):
         out = str(tmp_path / f"{name}.npy")
         env = dict(os.environ, OUT=out, **env_extra)
         subprocess.run([sys.executable, script, *map(str, geom_args)], env=env, check=True,

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python bench.py --steps 200 --warmup 20 --no-cpu-baseline --no-microbench > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
-timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider --timeout 300 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+bash tools/gpu_bench_env.sh - IMASK_FWD_TWO_DET=0
+timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider --timeout 400 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
