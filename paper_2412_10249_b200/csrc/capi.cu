@@ -62,7 +62,7 @@ cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float
                                const float2* PM, const float2* PTM, int n, const FwdAngle* ang,
                                const int4* entries, int n_entries, int row_ctas, bool quad,
                                int n_det, float* sino, const SinoSaga* saga, cudaStream_t stream,
-                               int dets);
+                               bool two_det);
 }  // namespace imask
 
 struct imask_graph {
@@ -126,8 +126,8 @@ struct LevelTables {
   FwdAngle* fwd = nullptr;  // device
   AdjAngle* adj = nullptr;  // device
   bool tma = false;         // tensor maps of the pair images at this level are valid
-  int dets = 1;             // detectors per thread of the TMA forward: 2 where every entry's
-                            // detectors are < 1 column apart (and ascend), 4 where < 2/3
+  bool two_det = false;     // every TMA entry's detectors are < 1 column apart (and ascend):
+                            // the two-detectors-per-thread forward applies
   TmaMaps maps{};           // boxes of 96 x 16 (pair mode) or 96 x 8 bands (quad mode)
 };
 
@@ -323,18 +323,12 @@ int get_tables(imask_plan* pl, int f, LevelTables** out) {
     }
     if (pl->sym && pl->tma_entries) {
       // the two-detector forward needs 0 < xi_dj < 1 for every entry's parameter row
-      const int want = knob(Knob::kFwdTwoDet, 4);  // 0/1: one detector, 2: at most two
-      double dmax = 0.0;
-      bool pos = true;
+      bool ok = f >= 2 && knob(Knob::kFwdTwoDet, 1) != 0;
       for (const int4& e4 : pl->tma_entries_host) {
         const int row = e4.x >= 0 ? e4.x : e4.z;
-        if (row < 0) continue;
-        pos = pos && fw[row].xi_dj > 0.0;
-        dmax = std::fmax(dmax, fw[row].xi_dj);
+        if (row >= 0 && !(fw[row].xi_dj > 0.0 && fw[row].xi_dj < 0.999)) ok = false;
       }
-      t.dets = 1;
-      if (pos && want >= 2 && dmax < 0.999) t.dets = 2;
-      if (pos && want >= 4 && 3.0 * dmax < 1.99) t.dets = 4;
+      t.two_det = ok;
     }
     if (pl->sym && !knob(Knob::kNoTma, 0)) {
       const int n = pl->side / f;
@@ -413,7 +407,7 @@ bool forward_quad_l1(const imask_plan* pl) {
 bool forward_reads_diff(const imask_plan* pl, const LevelTables* t, int n) {
   if (!pl->sym) return false;  // plain layout: P holds (u, d) pairs itself
   if (forward_uses_tma(pl, t, n))
-    return t->dets == 1 && !forward_tma_val_grid(pl->n_det, pl->n_tma_entries);
+    return !t->two_det && !forward_tma_val_grid(pl->n_det, pl->n_tma_entries);
   if (forward_quad_l1(pl)) return !forward_l1_val();
   return true;  // k_forward_sym
 }
@@ -433,7 +427,7 @@ int run_forward(imask_plan* pl, int f, const LevelTables* t, float* sino, const 
   if (forward_uses_tma(pl, t, n))
     e = launch_forward_tma(t->maps, pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->tma_entries,
                            pl->n_tma_entries, pl->tma_row_ctas, pl->tma_quad, pl->n_det, sino,
-                           saga, s, t->dets);
+                           saga, s, t->two_det);
   else {
     const bool quad = forward_quad_l1(pl);
     e = launch_forward(pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->n_loc, pl->n_det,

@@ -60,8 +60,7 @@ enum class Knob {
   kAdjCluster,       // IMASK_ADJ_CLUSTER: adjoint cluster size (1 = none)
   kAdjTile,          // IMASK_ADJ_TILE: "f:T,..." adjoint tile per factor
   kAdjCtas,          // IMASK_ADJ_CTAS: "f:ctas_per_sm,..." adjoint split target
-  kFwdTwoDet,        // IMASK_FWD_TWO_DET: most detectors per thread in the TMA forward
-                     // (1, 2 or 4; default 4: 2 at f >= 2, 4 at f >= 4)
+  kFwdTwoDet,        // IMASK_FWD_TWO_DET (0/1): two detectors per thread in the TMA forward (f >= 2)
   kCount
 };
 // Integer value of a switch, or `dflt` when unset (a set-but-valueless flag

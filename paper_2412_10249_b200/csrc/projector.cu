@@ -398,9 +398,6 @@ struct FwdWarpInfo {
 #ifndef IMASK_FWD2_MINB
 #define IMASK_FWD2_MINB 4
 #endif
-#ifndef IMASK_FWD4_MINB
-#define IMASK_FWD4_MINB 2
-#endif
 // kK = 2 (value planes, pixel width >= 2): each thread traces two adjacent
 // detectors of its entries. Their positions are < 1 column apart (xi_dj =
 // 1/(max(|c|,|s|) h) <= 1/sqrt2 for h >= 2), so the second ray's pair column is
@@ -409,7 +406,7 @@ struct FwdWarpInfo {
 // (value, difference) is selected by the carry -- the same float operations
 // as kK = 1, so the sinograms are bit-identical. A CTA covers 64 detectors.
 template <bool kSaga, bool kQuad, bool kVal, int kK = 1>
-__global__ void __launch_bounds__(kFThreads, kK == 4 ? IMASK_FWD4_MINB : (kK == 2 ? IMASK_FWD2_MINB : 1))
+__global__ void __launch_bounds__(kFThreads, kK == 2 ? IMASK_FWD2_MINB : 1)
 k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P,
               const float2* __restrict__ PT, const float2* __restrict__ PM,
               const float2* __restrict__ PTM, int n, int pitch, const FwdAngle* __restrict__ ang,
@@ -443,11 +440,10 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   const int rows[4] = {ent.x, ent.y, ent.z, ent.w};
   const int tab = ent.x >= 0 ? ent.x : ent.z;  // the entry's parameter row
   const bool valid = tab >= 0;
-  static_assert(kK == 1 || kVal, "several detectors per thread read value planes");
-  static_assert(kK == 1 || kK == 2 || kK == 4, "1, 2 or 4 detectors per thread");
-  constexpr int KB = kK > 1 ? kK - 1 : 1;  // the thread's further detectors j + 1 .. j + kK - 1
+  static_assert(kK == 1 || kVal, "two detectors per thread read value planes");
   const int j = blockIdx.x * 32 * kK + (warp & 3) * 8 * kK + (lane & 7) * kK;
   const int jr = min(j, n_det - 1);
+  const int j1 = j + 1, jr1 = min(j1, n_det - 1);  // kK = 2: the second detector
   FwdAngle A{};
   if (valid) A = ang[tab];
   SinoIn sin[NR];
@@ -456,7 +452,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
     for (int r = 0; r < NR; ++r)
       if (rows[r] >= 0) sin[r] = sino_load(saga, (size_t)rows[r] * n_det + j);
   }
-  long long X0 = 0, Xb[KB] = {};
+  long long X0 = 0, X1 = 0;
   int lo = n, hi = 0;
   if (valid) {
     X0 = __double2ll_rn(fma((double)jr, A.xi_dj, A.xi_base) * kFix);
@@ -465,12 +461,10 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
       lo = n;
       hi = 0;
     }
-#pragma unroll
-    for (int i = 0; i < kK - 1; ++i) {
-      // the same double expression per detector as kK = 1 (bit-identical positions)
-      Xb[i] = __double2ll_rn(fma((double)min(j + 1 + i, n_det - 1), A.xi_dj, A.xi_base) * kFix);
+    if constexpr (kK == 2) {
+      X1 = __double2ll_rn(fma((double)jr1, A.xi_dj, A.xi_base) * kFix);
       int lo1, hi1;
-      band_range(Xb[i], A.step, A.inv_step, n, &lo1, &hi1);
+      band_range(X1, A.step, A.inv_step, n, &lo1, &hi1);
       if (lo1 < hi1) {
         lo = min(lo, lo1);
         hi = max(hi, hi1);
@@ -501,7 +495,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
     atomicMax(&I.hi, whi);
   }
   {
-    const long long x_last = __shfl_sync(0xffffffffu, kK > 1 ? Xb[KB - 1] : X0, lane | 7);
+    const long long x_last = __shfl_sync(0xffffffffu, kK == 2 ? X1 : X0, lane | 7);
     if ((lane & 7) == 0 && valid && (warp & 3) == 3) info[slot].x0_last = x_last;
   }
   __syncthreads();
@@ -542,9 +536,8 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
       if (cmn > cmx) cmn = cmx = 0;  // no warp walks this chunk
       // TMA needs a 16-byte aligned start in the inner dimension: even pair index
       const int corig = ((cmn + 1 + kPadC) & ~1) - 1 - kPadC;
-      // kVal reads c .. c + 1; kK = 2 / 4 read c .. c + 2 / c + 3 from the first ray's c
-      if (cmx + (kVal ? 1 : 0) + (kK == 1 ? 0 : kK == 2 ? 1 : 2) - corig + 1 > kFWc)
-        atomicExch(&ctl[0], 1);
+      // kVal reads c .. c + 1; kK = 2 reads c .. c + 2 from the first ray's c
+      if (cmx + (kVal ? 1 : 0) + (kK == 2 ? 1 : 0) - corig + 1 > kFWc) atomicExch(&ctl[0], 1);
       cmin_tab[t] = corig;
     }
   }
@@ -559,15 +552,9 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   // layout): (acc, accm) += (u, um) + g * (d, dm) with packed FP32 ops; accT
   // the same for the transpose partners (kQuad)
   float2 acc2 = make_float2(0.f, 0.f), accT = make_float2(0.f, 0.f);
-  float2 accb[KB], accTb[KB];  // the further detectors' rays
-  Fix32 dXb[KB];                // their offsets from the first ray (< 1.1 columns)
-#pragma unroll
-  for (int i = 0; i < KB; ++i) {
-    accb[i] = make_float2(0.f, 0.f);
-    accTb[i] = make_float2(0.f, 0.f);
-    dXb[i] = fix_from(Xb[i] - X0);
-  }
+  float2 acc2b = make_float2(0.f, 0.f), accTb = make_float2(0.f, 0.f);  // kK = 2: 2nd ray
   const float S = A.S, B = A.B;
+  const Fix32 dX1 = fix_from(X1 - X0);  // kK = 2: second ray's offset (< 1 column)
 
   if (ctl[0]) {
     // fallback: global (L1) loads over the lane's own band range (a warp holds
@@ -591,20 +578,19 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
         }
         fix_add(Y, dY);
       }
-#pragma unroll
-      for (int i = 0; i < kK - 1; ++i) {
+      if constexpr (kK == 2) {
         int lo1, hi1;
-        band_range(Xb[i], A.step, A.inv_step, n, &lo1, &hi1);
-        Fix32 Y1 = fix_from(Xb[i] + (long long)lo1 * dYl + ((long long)(1 + kPadC) << 32));
+        band_range(X1, A.step, A.inv_step, n, &lo1, &hi1);
+        Fix32 Y1 = fix_from(X1 + (long long)lo1 * dYl + ((long long)(1 + kPadC) << 32));
         for (int b = lo1; b < hi1; ++b) {
           const float g = __saturatef(fmaf(onep_from_frac(Y1.lo), S, B));
           const float2 v = __ldg(img + Y1.hi);
-          accb[i] = fadd2(accb[i], v);
-          accb[i] = ffma2(g, fsub2(__ldg(img + Y1.hi + 1), v), accb[i]);
+          acc2b = fadd2(acc2b, v);
+          acc2b = ffma2(g, fsub2(__ldg(img + Y1.hi + 1), v), acc2b);
           if (kQuad) {
             const float2 vt = __ldg(PT + Y1.hi);
-            accTb[i] = fadd2(accTb[i], vt);
-            accTb[i] = ffma2(g, fsub2(__ldg(PT + Y1.hi + 1), vt), accTb[i]);
+            accTb = fadd2(accTb, vt);
+            accTb = ffma2(g, fsub2(__ldg(PT + Y1.hi + 1), vt), accTb);
           }
           fix_add(Y1, dY);
         }
@@ -649,53 +635,32 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
         const long long X = X0 + (long long)bs * A.step;
         Fix32 Y = fix_from(X + ((long long)((bs - b0) * kFWc - cmin_tab[i] + s * NI * kBox) << 32));
         int b = bs;
-        if constexpr (kK > 1) {
-          // NV value pairs per plane feed the thread's kK rays; ray i's pair
-          // (value, difference) starts at the first ray's column + its carry
-          // (0 .. NV - 2), the same float operations as kK = 1
-          constexpr int NV = kK == 2 ? 3 : 4;
+        if constexpr (kK == 2) {
+          // three value pairs per plane feed both rays; the second ray's pair
+          // (value, difference) is the first's or the next one's (carry)
           for (; b < be; ++b) {
-            float2 v[NV], t[NV], d[NV - 1], e[NV - 1];
+            float2 v3[3], t3[3];
 #pragma unroll
-            for (int c = 0; c < NV; ++c) {
-              v[c] = win[Y.hi + c];
-              if (kQuad) t[c] = win[Y.hi + kBox + c];
+            for (int c = 0; c < 3; ++c) {
+              v3[c] = win[Y.hi + c];
+              if (kQuad) t3[c] = win[Y.hi + kBox + c];
             }
-#pragma unroll
-            for (int c = 0; c < NV - 1; ++c) {
-              d[c] = fsub2(v[c + 1], v[c]);
-              if (kQuad) e[c] = fsub2(t[c + 1], t[c]);
-            }
+            Fix32 Y1 = Y;
+            fix_add(Y1, dX1);
+            const bool c1 = Y1.hi != Y.hi;
             const float g0 = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
-            acc2 = fadd2(acc2, v[0]);
-            acc2 = ffma2(g0, d[0], acc2);
+            const float g1 = __saturatef(fmaf(onep_from_frac(Y1.lo), S, B));
+            const float2 d0 = fsub2(v3[1], v3[0]), d1 = fsub2(v3[2], v3[1]);
+            acc2 = fadd2(acc2, v3[0]);
+            acc2 = ffma2(g0, d0, acc2);
+            acc2b = fadd2(acc2b, c1 ? v3[1] : v3[0]);
+            acc2b = ffma2(g1, c1 ? d1 : d0, acc2b);
             if (kQuad) {
-              accT = fadd2(accT, t[0]);
-              accT = ffma2(g0, e[0], accT);
-            }
-#pragma unroll
-            for (int i = 0; i < kK - 1; ++i) {
-              Fix32 Yi = Y;
-              fix_add(Yi, dXb[i]);
-              const uint32_t ki = Yi.hi - Y.hi;
-              const float gi = __saturatef(fmaf(onep_from_frac(Yi.lo), S, B));
-              float2 bv = v[0], bd = d[0], bt = t[0], be2 = e[0];
-              if (ki >= 1u) {
-                bv = v[1];
-                bd = d[1];
-                if (kQuad) { bt = t[1]; be2 = e[1]; }
-              }
-              if (NV > 3 && ki >= 2u) {
-                bv = v[NV > 3 ? 2 : 1];
-                bd = d[NV > 3 ? 2 : 1];
-                if (kQuad) { bt = t[NV > 3 ? 2 : 1]; be2 = e[NV > 3 ? 2 : 1]; }
-              }
-              accb[i] = fadd2(accb[i], bv);
-              accb[i] = ffma2(gi, bd, accb[i]);
-              if (kQuad) {
-                accTb[i] = fadd2(accTb[i], bt);
-                accTb[i] = ffma2(gi, be2, accTb[i]);
-              }
+              const float2 e0 = fsub2(t3[1], t3[0]), e1 = fsub2(t3[2], t3[1]);
+              accT = fadd2(accT, t3[0]);
+              accT = ffma2(g0, e0, accT);
+              accTb = fadd2(accTb, c1 ? t3[1] : t3[0]);
+              accTb = ffma2(g1, c1 ? e1 : e0, accTb);
             }
             fix_add(Y, dYw);
           }
@@ -781,16 +746,13 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
       }
     }
   }
-#pragma unroll
-  for (int i = 0; i < kK - 1; ++i) {
-    const int ji = j + 1 + i;
-    if (!valid || ji >= n_det) continue;
-    const float vals[4] = {accb[i].x, accb[i].y, accTb[i].x, accTb[i].y};
+  if (kK == 2 && valid && j1 < n_det) {
+    const float vals[4] = {acc2b.x, acc2b.y, accTb.x, accTb.y};
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       if (rows[r] < 0) continue;
       const float val = vals[r] * A.wsc;
-      const size_t q = (size_t)rows[r] * n_det + ji;
+      const size_t q = (size_t)rows[r] * n_det + j1;
       if (kSaga) {
         sino_update(saga, q, sino_load(saga, q), val);
       } else {
@@ -838,9 +800,8 @@ cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float
                                const float2* PM, const float2* PTM, int n, const FwdAngle* ang,
                                const int4* entries, int n_entries, int row_ctas, bool quad,
                                int n_det, float* sino, const SinoSaga* saga, cudaStream_t stream,
-                               int dets) {
-  const int kk = dets == 4 ? 4 : (dets == 2 ? 2 : 1);
-  const bool two_det = kk > 1;
+                               bool two_det) {
+  const int kk = two_det ? 2 : 1;
   dim3 grid((n_det + 32 * kk - 1) / (32 * kk), (n_entries + kFE - 1) / kFE);
   const bool val = two_det || forward_tma_val((int)(grid.x * grid.y));
   const size_t smem = forward_tma_smem(val);
@@ -851,8 +812,7 @@ cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float
   launch_pdl(k_forward_tma<S_, Q_, V_, K_>, grid, dim3(kFThreads), smem, stream, maps, P, PT, PM, \
              PTM, n, pair_pitch(n), ang, entries, n_entries, row_ctas, n_det, out, sg)
 #define FWD_TMA_V(S_, Q_)                                 \
-  if (kk == 4) FWD_TMA(S_, Q_, true, 4);                  \
-  else if (kk == 2) FWD_TMA(S_, Q_, true, 2);             \
+  if (two_det) FWD_TMA(S_, Q_, true, 2);                  \
   else if (val) FWD_TMA(S_, Q_, true, 1);                 \
   else FWD_TMA(S_, Q_, false, 1)
   if (saga) {
@@ -1267,17 +1227,13 @@ void init_kernel_attributes() {
   FWD_ATTR(true, true, true);
   FWD_ATTR(false, true, true);
 #undef FWD_ATTR
-#define FWD_ATTR2(S_, Q_, K_)                                                                \
-  cudaFuncSetAttribute(k_forward_tma<S_, Q_, true, K_>,                                      \
+#define FWD_ATTR2(S_, Q_)                                                                    \
+  cudaFuncSetAttribute(k_forward_tma<S_, Q_, true, 2>,                                       \
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)forward_tma_smem(true))
-  FWD_ATTR2(true, true, 2);
-  FWD_ATTR2(false, true, 2);
-  FWD_ATTR2(true, false, 2);
-  FWD_ATTR2(false, false, 2);
-  FWD_ATTR2(true, true, 4);
-  FWD_ATTR2(false, true, 4);
-  FWD_ATTR2(true, false, 4);
-  FWD_ATTR2(false, false, 4);
+  FWD_ATTR2(true, true);
+  FWD_ATTR2(false, true);
+  FWD_ATTR2(true, false);
+  FWD_ATTR2(false, false);
 #undef FWD_ATTR2
 #define ADJ_ATTR(P_, T_, S_, K_)                                                          \
   cudaFuncSetAttribute(k_adjoint<P_, T_, S_, K_>,                                        \

@@ -250,9 +250,8 @@ def test_forward_paths_bit_identical(geom_args, tmp_path):
                             ("quad_planes", {"IMASK_FWD_VAL": "0"}),
                             ("pair_planes", {"IMASK_NO_QUAD": "1", "IMASK_FWD_VAL": "0"}),
                             ("l1_planes", {"IMASK_NO_TMA": "1", "IMASK_FWD_VAL_L1": "0"}),
-                            # detectors per thread (default: two at f >= 2, four at f >= 4)
+                            # one detector per thread (f >= 2 default: two)
                             ("one_det", {"IMASK_FWD_TWO_DET": "0"}),
-                            ("two_det", {"IMASK_FWD_TWO_DET": "2"}),
                             ("one_det_planes", {"IMASK_FWD_TWO_DET": "0", "IMASK_FWD_VAL": "0"}),
                             ("pair_one_det", {"IMASK_NO_QUAD": "1", "IMASK_FWD_TWO_DET": "0"})):
         out = str(tmp_path / f"{name}.npy")
