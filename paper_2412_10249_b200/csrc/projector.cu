@@ -398,6 +398,9 @@ struct FwdWarpInfo {
 #ifndef IMASK_FWD2_MINB
 #define IMASK_FWD2_MINB 4
 #endif
+#ifndef IMASK_FWD1_MINB
+#define IMASK_FWD1_MINB 4  // 64 registers, 4 CTAs per SM: f=1 step -1% (A/B)
+#endif
 // kK = 2 (value planes, pixel width >= 2): each thread traces two adjacent
 // detectors of its entries. Their positions are < 1 column apart (xi_dj =
 // 1/(max(|c|,|s|) h) <= 1/sqrt2 for h >= 2), so the second ray's pair column is
@@ -406,7 +409,7 @@ struct FwdWarpInfo {
 // (value, difference) is selected by the carry -- the same float operations
 // as kK = 1, so the sinograms are bit-identical. A CTA covers 64 detectors.
 template <bool kSaga, bool kQuad, bool kVal, int kK = 1>
-__global__ void __launch_bounds__(kFThreads, kK == 2 ? IMASK_FWD2_MINB : 1)
+__global__ void __launch_bounds__(kFThreads, kK == 2 ? IMASK_FWD2_MINB : IMASK_FWD1_MINB)
 k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P,
               const float2* __restrict__ PT, const float2* __restrict__ PM,
               const float2* __restrict__ PTM, int n, int pitch, const FwdAngle* __restrict__ ang,
