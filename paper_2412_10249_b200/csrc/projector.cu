@@ -1281,7 +1281,8 @@ void adjoint_layout(int n, int factor, int n_loc, bool sym, int* T_out, int* S_o
   // chain, but a cold-L2 step slower: the windows' HBM latency needs the CTAs.)
   // (factor 1 with many angles: 28 per SM, measured -1% on the whole-set step
   // with the value-plane forward beside it; a 1/4 or 1/8 shard is slower so)
-  int per_sm = factor == 1 ? (n_loc >= 512 ? 28 : 20) : 16;
+  // (factor 2 on plans of >= 512 angles: 24 per SM, f=2 step 377 -> 373 us)
+  int per_sm = factor == 1 ? (n_loc >= 512 ? 28 : 20) : (factor == 2 && n_loc >= 512 ? 24 : 16);
   {
     const int cc = knob_for_factor(Knob::kAdjCtas, factor, per_sm);
     if (cc > 0) per_sm = cc;
