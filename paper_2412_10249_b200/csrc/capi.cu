@@ -41,6 +41,9 @@ cudaError_t launch_compensate(const float* x, float* out, int side, const CompPa
                               cudaStream_t s);
 cudaError_t launch_prepare(const float* u, int n, float2* P, float2* PT, float2* PM,
                            float2* PTM, bool diff, cudaStream_t s);
+bool stage32_ok(int side, int f, int r);
+cudaError_t launch_stage32(const float* x, int side, int f, const CompParams& cp, float2* P,
+                           float2* PT, cudaStream_t s);
 bool forward_tma_val_grid(int n_det, int n_entries);
 bool forward_l1_val();
 cudaError_t launch_saga_image_coarse(const float* bp, int side, int f, const ImageSaga& sg,
@@ -78,7 +81,7 @@ const char* const kKnobNames[(int)Knob::kCount] = {
     "IMASK_NO_TMA", "IMASK_NO_QUAD", "IMASK_NO_QUAD_L1", "IMASK_FWD_VAL", "IMASK_FWD_VAL_L1",
     "IMASK_TMA_MIN_N", "IMASK_ADJ_AFTER_STAGE_MIN_N", "IMASK_SAGA_SPLIT_MIN_N",
     "IMASK_ADJ_WIN_KB", "IMASK_ADJ_CLUSTER", "IMASK_ADJ_TILE", "IMASK_ADJ_CTAS",
-    "IMASK_FWD_TWO_DET"};
+    "IMASK_FWD_TWO_DET", "IMASK_FUSED_STAGE"};
 
 const char* knob_raw(Knob k) {
   static const char* vals[(int)Knob::kCount];
@@ -484,6 +487,18 @@ int step_image(imask_plan* pl, const imask_state* st, int level0, const imask_st
 int stage_forward_input(imask_plan* pl, const float* x, int level0, cudaStream_t s) {
   const int f = pl->factors[level0];
   const int n = pl->side / f;
+  if (pl->n_loc > 0 && pl->sym && knob(Knob::kFusedStage, 1) != 0 &&
+      stage32_ok(pl->side, f, pl->r)) {
+    LevelTables* t;
+    int rc;
+    if ((rc = get_tables(pl, f, &t))) return rc;
+    if (!forward_reads_diff(pl, t, n)) {
+      // value-plane forwards: x -> P, PT in one kernel (restriction or
+      // compensation fused into the pair-plane staging)
+      LAUNCH(launch_stage32(x, pl->side, f, pl->cp, pl->P, pl->PT, s), "stage");
+      return IMASK_OK;
+    }
+  }
   if (level0 < pl->r - 1)
     LAUNCH(launch_restrict(x, pl->u, pl->side, f, s), "restrict");
   else

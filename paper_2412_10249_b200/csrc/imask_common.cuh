@@ -61,6 +61,7 @@ enum class Knob {
   kAdjTile,          // IMASK_ADJ_TILE: "f:T,..." adjoint tile per factor
   kAdjCtas,          // IMASK_ADJ_CTAS: "f:ctas_per_sm,..." adjoint split target
   kFwdTwoDet,        // IMASK_FWD_TWO_DET (0/1): two detectors per thread in the TMA forward (f >= 2)
+  kFusedStage,       // IMASK_FUSED_STAGE (0/1): x -> value planes in one kernel
   kCount
 };
 // Integer value of a switch, or `dflt` when unset (a set-but-valueless flag

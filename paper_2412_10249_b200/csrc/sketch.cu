@@ -404,6 +404,96 @@ k_prepare(const float* __restrict__ u, int n, float2* __restrict__ P, float2* __
   }
 }
 
+// Fused staging for the value-plane forwards (the mirror-symmetric plans of
+// the whole angle set): x goes to the value planes P, PT of level f = 2^lg
+// in one kernel. Each CTA loads a 32 x 32 tile of x (128-bit loads), forms its
+// (32/f)^2 values of u = T_f x (the restriction pyramid of k_restrict32) or,
+// at the full level, u = S_r x (comp32 of k_compensate32) -- the same float
+// operations, so P and PT are bit-identical to restriction / compensation +
+// k_prepare -- and writes each value twice per plane: P[R][c].x = u[R][c] and
+// P[R][n-1-c].y = u[R][c] (the mirror pairing), likewise along the transpose.
+// Tiles on the image edge write the rows' zero padding; every entry of the
+// n x pitch planes is written, so the planes need no clearing between levels.
+__global__ void __launch_bounds__(256)
+k_stage32(const float* __restrict__ x, int side, int lg, CompParams cp, float2* __restrict__ P,
+          float2* __restrict__ PT) {
+  __shared__ __align__(16) Pyr32Smem sm;
+  __shared__ float ut[32][33];  // the tile's u values, w x w (w = 32 >> lg)
+  const int n = side >> lg, w = 32 >> lg;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const int py = threadIdx.x >> 3, c8 = threadIdx.x & 7;
+  const float4 v =
+      __ldg(reinterpret_cast<const float4*>(x + (size_t)(y0 + py) * side + x0 + c8 * 4));
+  if (lg == 0) {
+    const float4 o = comp32(v, cp, sm);
+    ut[py][4 * c8] = o.x;
+    ut[py][4 * c8 + 1] = o.y;
+    ut[py][4 * c8 + 2] = o.z;
+    ut[py][4 * c8 + 3] = o.w;
+  } else {
+    float l1a, l1b, l2;
+    pyr32_low(v, l1a, l1b, l2);
+    if (lg == 1) {
+      if ((py & 1) == 0) {
+        ut[py >> 1][2 * c8] = l1a;
+        ut[py >> 1][2 * c8 + 1] = l1b;
+      }
+    } else if (lg == 2) {
+      if ((py & 3) == 0) ut[py >> 2][c8] = l2;
+    } else {
+      if ((py & 3) == 0) sm.l2[(py >> 2) * 8 + c8] = l2;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        float L3, L4, L4a, L5;
+        pyr32_high(sm, L3, L4, L4a, L5);
+        const int l = threadIdx.x;
+        if (lg == 3 && l < 16) ut[l >> 2][l & 3] = L3;
+        if (lg == 4 && l < 4) ut[l >> 1][l & 1] = L4;
+        if (lg == 5 && l == 0) ut[0][0] = L5;
+      }
+    }
+  }
+  __syncthreads();
+  // the planes may still be read by the previous level's forward (the stream
+  // predecessor): write them only once it is done
+  griddep_wait();
+  const int R0 = y0 >> lg, C0 = x0 >> lg;
+  const size_t pitch = (size_t)pair_pitch(n);
+  float* Pf = reinterpret_cast<float*>(P);
+  float* PTf = reinterpret_cast<float*>(PT);
+  const int nw = w * w;
+  for (int e = threadIdx.x; e < nw; e += blockDim.x) {
+    const int rr = e / w, cc = e % w;  // consecutive threads along a row of u
+    const int R = R0 + rr, C = C0 + cc;
+    const float val = ut[rr][cc];
+    Pf[2 * (R * pitch + C + 1 + kPadC)] = val;
+    Pf[2 * (R * pitch + (n - 1 - C) + 1 + kPadC) + 1] = val;
+  }
+  for (int e = threadIdx.x; e < nw; e += blockDim.x) {
+    const int cc = e / w, rr = e % w;  // consecutive threads along a column of u
+    const int R = R0 + rr, C = C0 + cc;
+    const float val = ut[rr][cc];
+    PTf[2 * (C * pitch + R + 1 + kPadC)] = val;
+    PTf[2 * ((n - 1 - C) * pitch + R + 1 + kPadC) + 1] = val;
+  }
+  // zero padding: P rows of the left / right edge tiles, PT rows of the top / bottom
+  constexpr int kPadL = kPadC + 1;  // indices 0 .. kPadC (c = -1 - kPadC .. -1)
+  const int padR = (int)pitch - (n + 1 + kPadC);  // indices n + 1 + kPadC .. pitch - 1
+  const float2 z = make_float2(0.f, 0.f);
+  if (C0 == 0)
+    for (int e = threadIdx.x; e < w * kPadL; e += blockDim.x)
+      P[(R0 + e / kPadL) * pitch + e % kPadL] = z;
+  if (C0 + w == n)
+    for (int e = threadIdx.x; e < w * padR; e += blockDim.x)
+      P[(R0 + e / padR) * pitch + n + 1 + kPadC + e % padR] = z;
+  if (R0 == 0)
+    for (int e = threadIdx.x; e < w * kPadL; e += blockDim.x)
+      PT[(C0 + e / kPadL) * pitch + e % kPadL] = z;
+  if (R0 + w == n)
+    for (int e = threadIdx.x; e < w * padR; e += blockDim.x)
+      PT[(C0 + e / padR) * pitch + n + 1 + kPadC + e % padR] = z;
+}
+
 // ---- SAGA image side --------------------------------------------------------
 
 // Coarse level (factor f > 1): phi_new = U_f(bp)/f^2 is constant on f x f
@@ -611,6 +701,16 @@ cudaError_t launch_compensate(const float* x, float* out, int side, const CompPa
     k_compensate<32><<<grid, 256, 0, s>>>(x, out, side, cp);
   else
     k_compensate<64><<<grid, 256, 0, s>>>(x, out, side, cp);
+  return cudaGetLastError();
+}
+
+bool stage32_ok(int side, int f, int r) { return side % 32 == 0 && f <= 32 && r <= 6; }
+
+cudaError_t launch_stage32(const float* x, int side, int f, const CompParams& cp, float2* P,
+                           float2* PT, cudaStream_t s) {
+  int lg = 0;
+  while ((1 << lg) < f) ++lg;
+  launch_pdl(k_stage32, dim3(side / 32, side / 32), dim3(256), 0, s, x, side, lg, cp, P, PT);
   return cudaGetLastError();
 }
 

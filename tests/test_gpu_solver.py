@@ -473,3 +473,27 @@ def test_sharded_step_graph_with_nccl():
     assert out["graph_eq_eager"], out
     assert out["rel_x_vs_single"] <= 1e-6 and out["rel_y_vs_single"] <= 1e-6, out
     assert out["graphs_captured"] >= 2, out
+
+
+@pytest.mark.parametrize("args", [(1024, 1440, 1449, 6, 8), (256, 360, 363, 4, 12),
+                                  (512, 720, 725, 5, 10, 2, 1)])
+def test_fused_staging_bit_identical(args, tmp_path):
+    """x goes to the forward's value planes in one kernel (restriction or
+    compensation fused into the pair-plane staging, k_stage32) or through
+    restriction / compensation + k_prepare (IMASK_FUSED_STAGE=0): every level
+    at both dual parities, then a seeded schedule; iterates bit-identical.
+    The switch is read once per process, so each runs in a subprocess."""
+    import os
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for name, env_extra in (("fused", {}), ("two_kernels", {"IMASK_FUSED_STAGE": "0"})):
+        out = str(tmp_path / f"{name}.npz")
+        env = dict(os.environ, OUT=out, **env_extra)
+        subprocess.run([sys.executable, os.path.join(repo, "tools", "repro_steps.py"),
+                        *map(str, args)], env=env, check=True, capture_output=True, timeout=300)
+        outs[name] = np.load(out)
+    for key in ("x", "y"):
+        assert np.array_equal(outs["fused"][key], outs["two_kernels"][key]), key

@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-bash tools/gpu_bench_env.sh IMASK_ADJ_CTAS=2:24 IMASK_ADJ_CTAS=2:32 IMASK_ADJ_CTAS=2:24,4:24 IMASK_ADJ_CTAS=2:24,4:12 IMASK_ADJ_CTAS=2:24,8:24,16:24
+timeout 900 python -m pytest tests/test_gpu_solver.py -q -x -p no:cacheprovider --timeout 400 -k "fused_staging" > gpurun_out/pytest_fs.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_fs.log
