@@ -296,6 +296,11 @@ IMASK_API int imask_prox_tv_nonneg(int side, const float* xp, float* out, double
                                    double mu_g, int inner_iters, double inner_tol, void* scratch,
                                    void* stream);
 
+/* Test / measurement helper (no reference counterpart): re-read the IMASK_*
+ * path switches from the environment (imask_common.cuh lists them; they are
+ * otherwise read once). Plans created afterwards use the new values. */
+IMASK_API int imask_reload_switches(void);
+
 /* Measurement helper (no reference counterpart): thread-level FP32 FFMA
  * throughput of `device` from an FFMA-chain microbenchmark, the FP32-issue
  * denominator of bench.py's roofline. */

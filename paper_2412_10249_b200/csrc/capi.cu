@@ -83,13 +83,24 @@ const char* const kKnobNames[(int)Knob::kCount] = {
     "IMASK_ADJ_WIN_KB", "IMASK_ADJ_CLUSTER", "IMASK_ADJ_TILE", "IMASK_ADJ_CTAS",
     "IMASK_FWD_TWO_DET", "IMASK_FUSED_STAGE"};
 
+std::string g_knob_vals[(int)Knob::kCount];
+bool g_knob_set[(int)Knob::kCount];
+std::mutex g_knob_mu;
+bool g_knobs_read = false;
+
+void read_knobs() {
+  for (int i = 0; i < (int)Knob::kCount; ++i) {
+    const char* e = std::getenv(kKnobNames[i]);
+    g_knob_set[i] = e != nullptr;
+    g_knob_vals[i] = e ? e : "";
+  }
+  g_knobs_read = true;
+}
+
 const char* knob_raw(Knob k) {
-  static const char* vals[(int)Knob::kCount];
-  static std::once_flag once;
-  std::call_once(once, [] {
-    for (int i = 0; i < (int)Knob::kCount; ++i) vals[i] = std::getenv(kKnobNames[i]);
-  });
-  return vals[(int)k];
+  std::lock_guard<std::mutex> lk(g_knob_mu);
+  if (!g_knobs_read) read_knobs();
+  return g_knob_set[(int)k] ? g_knob_vals[(int)k].c_str() : nullptr;
 }
 }  // namespace
 
@@ -769,6 +780,12 @@ int imask_plan_create_list(int side, int n_angles, int n_det, int n_loc, const i
     }
   }
   *out = pl;
+  return IMASK_OK;
+}
+
+int imask_reload_switches(void) {
+  std::lock_guard<std::mutex> lk(g_knob_mu);
+  read_knobs();
   return IMASK_OK;
 }
 

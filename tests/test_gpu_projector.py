@@ -234,30 +234,43 @@ def test_mirror_closed_shards_match_full(n_angles, world):
 @pytest.mark.parametrize("geom_args", [(1024, 1440, 1449, 1), (1024, 1440, 1449, 2),
                                        (1024, 1440, 1449, 8), (256, 360, 363, 1),
                                        (256, 360, 363, 2), (256, 360, 363, 4)])
-def test_forward_paths_bit_identical(geom_args, tmp_path):
+def test_forward_paths_bit_identical(geom_args, monkeypatch):
     """The four-ray (quad) TMA forward, the pair TMA forward and the L1 forward
     trace the same rays with the same arithmetic: bit-identical sinograms, with
     the difference pairs read from the difference planes or formed from the
-    value planes (P[c+1] - P[c]), and with one or two detectors per thread. The path switches are read once per process,
-    so each runs in a subprocess."""
-    import subprocess
-    import sys
+    value planes (P[c+1] - P[c]), and with one or two detectors per thread.
+    The path switches are environment variables re-read by
+    imask_reload_switches; each variant gets a fresh plan."""
+    from paper_2412_10249_b200 import _lib
 
-    script = os.path.join(REPO, "tools", "repro_quad.py")
+    side, na, nd, f = geom_args
+    geom = ctmodel.Geometry(side, na, nd)
+    n = side // f
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    u = torch.rand(n * n, device="cuda", generator=gen)
     outs = {}
-    for name, env_extra in (("quad", {}), ("pair", {"IMASK_NO_QUAD": "1"}),
-                            ("l1", {"IMASK_NO_TMA": "1"}),
-                            ("quad_planes", {"IMASK_FWD_VAL": "0"}),
-                            ("pair_planes", {"IMASK_NO_QUAD": "1", "IMASK_FWD_VAL": "0"}),
-                            ("l1_planes", {"IMASK_NO_TMA": "1", "IMASK_FWD_VAL_L1": "0"}),
-                            # one detector per thread (f >= 2 default: two)
-                            ("one_det", {"IMASK_FWD_TWO_DET": "0"}),
-                            ("one_det_planes", {"IMASK_FWD_TWO_DET": "0", "IMASK_FWD_VAL": "0"}),
-                            ("pair_one_det", {"IMASK_NO_QUAD": "1", "IMASK_FWD_TWO_DET": "0"})):
-        out = str(tmp_path / f"{name}.npy")
-        env = dict(os.environ, OUT=out, **env_extra)
-        subprocess.run([sys.executable, script, *map(str, geom_args)], env=env, check=True,
-                       capture_output=True, timeout=300)
-        outs[name] = np.load(out)
+    variants = (("quad", {}), ("pair", {"IMASK_NO_QUAD": "1"}), ("l1", {"IMASK_NO_TMA": "1"}),
+                ("quad_planes", {"IMASK_FWD_VAL": "0"}),
+                ("pair_planes", {"IMASK_NO_QUAD": "1", "IMASK_FWD_VAL": "0"}),
+                ("l1_planes", {"IMASK_NO_TMA": "1", "IMASK_FWD_VAL_L1": "0"}),
+                # one detector per thread (f >= 2 default: two)
+                ("one_det", {"IMASK_FWD_TWO_DET": "0"}),
+                ("one_det_planes", {"IMASK_FWD_TWO_DET": "0", "IMASK_FWD_VAL": "0"}),
+                ("pair_one_det", {"IMASK_NO_QUAD": "1", "IMASK_FWD_TWO_DET": "0"}))
+    names = {k for _, env in variants for k in env}
+    try:
+        for name, env in variants:
+            for k in names:
+                monkeypatch.delenv(k, raising=False)
+            for k, v in env.items():
+                monkeypatch.setenv(k, v)
+            _lib.check(_lib.lib().imask_reload_switches())
+            plan = ctmodel.Plan(geom)
+            outs[name] = host(plan.project(u, f))
+            del plan
+    finally:
+        for k in names:
+            monkeypatch.delenv(k, raising=False)
+        _lib.check(_lib.lib().imask_reload_switches())
     for name in outs:
         assert np.array_equal(outs["quad"], outs[name]), name

@@ -477,23 +477,44 @@ def test_sharded_step_graph_with_nccl():
 
 @pytest.mark.parametrize("args", [(1024, 1440, 1449, 6, 8), (256, 360, 363, 4, 12),
                                   (512, 720, 725, 5, 10, 2, 1)])
-def test_fused_staging_bit_identical(args, tmp_path):
+def test_fused_staging_bit_identical(args, monkeypatch):
     """x goes to the forward's value planes in one kernel (restriction or
     compensation fused into the pair-plane staging, k_stage32) or through
     restriction / compensation + k_prepare (IMASK_FUSED_STAGE=0): every level
-    at both dual parities, then a seeded schedule; iterates bit-identical.
-    The switch is read once per process, so each runs in a subprocess."""
-    import os
-    import subprocess
-    import sys
+    at both dual parities, then a seeded schedule; iterates bit-identical."""
+    from paper_2412_10249_b200 import _lib
+    from paper_2412_10249_b200 import dist as dist_mod
 
-    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    side, na, nd, r, K = args[:5]
+    world, rank = args[5:7] if len(args) > 5 else (1, 0)
+    geom = ctmodel.Geometry(side, na, nd)
+    b = np.random.default_rng(3).standard_normal(geom.m)
+    fam = mrsketch.make_family(r, side, [1.0 / r] * r, mode="coarse")
     outs = {}
-    for name, env_extra in (("fused", {}), ("two_kernels", {"IMASK_FUSED_STAGE": "0"})):
-        out = str(tmp_path / f"{name}.npz")
-        env = dict(os.environ, OUT=out, **env_extra)
-        subprocess.run([sys.executable, os.path.join(repo, "tools", "repro_steps.py"),
-                        *map(str, args)], env=env, check=True, capture_output=True, timeout=300)
-        outs[name] = np.load(out)
-    for key in ("x", "y"):
-        assert np.array_equal(outs["fused"][key], outs["two_kernels"][key]), key
+    try:
+        for name, val in (("fused", None), ("two_kernels", "0")):
+            if val is None:
+                monkeypatch.delenv("IMASK_FUSED_STAGE", raising=False)
+            else:
+                monkeypatch.setenv("IMASK_FUSED_STAGE", val)
+            _lib.check(_lib.lib().imask_reload_switches())
+            ctmodel._plan_cache.clear()  # fresh plans take the switch
+            prob = dist_mod.make_sharded_problem(geom, dist_mod.local_rows(geom, b, rank, world),
+                                                 fam, 1e-2, rank, world)
+            prob.engine.shard = solvers.Shard()  # the phases on one GPU, no collective
+            st = solvers.init_state(prob, seed=4)
+            gen = torch.Generator(device="cuda").manual_seed(0)
+            st.x.copy_(torch.rand(side * side, device="cuda", generator=gen))
+            prm = solvers._params(1e-6, 1e-2, 1e-2)
+            levels = list(range(r)) * 2 + [int(v) for v in
+                                           solvers.draw_levels(4, 0, K, prob.cum_probs)]
+            for lv in levels:
+                solvers._device_step(prob.engine, st, lv, prm)
+            outs[name] = (host(st.x), host(st.y))
+            del prob, st
+    finally:
+        monkeypatch.delenv("IMASK_FUSED_STAGE", raising=False)
+        _lib.check(_lib.lib().imask_reload_switches())
+        ctmodel._plan_cache.clear()
+    assert np.array_equal(outs["fused"][0], outs["two_kernels"][0])
+    assert np.array_equal(outs["fused"][1], outs["two_kernels"][1])
