@@ -81,7 +81,7 @@ const char* const kKnobNames[(int)Knob::kCount] = {
     "IMASK_NO_TMA", "IMASK_NO_QUAD", "IMASK_NO_QUAD_L1", "IMASK_FWD_VAL", "IMASK_FWD_VAL_L1",
     "IMASK_TMA_MIN_N", "IMASK_ADJ_AFTER_STAGE_MIN_N", "IMASK_SAGA_SPLIT_MIN_N",
     "IMASK_ADJ_WIN_KB", "IMASK_ADJ_CLUSTER", "IMASK_ADJ_TILE", "IMASK_ADJ_CTAS",
-    "IMASK_FWD_TWO_DET", "IMASK_FUSED_STAGE"};
+    "IMASK_FWD_TWO_DET", "IMASK_FUSED_STAGE", "IMASK_FWD_TWO_DET_MIN_WAVES"};
 
 std::string g_knob_vals[(int)Knob::kCount];
 bool g_knob_set[(int)Knob::kCount];
@@ -342,6 +342,16 @@ int get_tables(imask_plan* pl, int f, LevelTables** out) {
         const int row = e4.x >= 0 ? e4.x : e4.z;
         if (row >= 0 && !(fw[row].xi_dj > 0.0 && fw[row].xi_dj < 0.999)) ok = false;
       }
+      // a small grid (an angle shard) runs latency-bound along each CTA's band
+      // walk: halving its CTAs costs more than the shared reads save (1/8 shard
+      // f=2 forward 71 -> 97 us), so two detectors only where the two-detector
+      // grid still fills >= IMASK_FWD_TWO_DET_MIN_WAVES x SM count CTAs
+      const long long ctas2 = (long long)((pl->n_det + 63) / 64) *
+                              (long long)((pl->n_tma_entries + forward_tma_entries_per_cta() - 1) /
+                                          forward_tma_entries_per_cta());
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->device);
+      if (ctas2 < (long long)knob(Knob::kFwdTwoDetMinWaves, 6) * sms) ok = false;
       t.two_det = ok;
     }
     if (pl->sym && !knob(Knob::kNoTma, 0)) {

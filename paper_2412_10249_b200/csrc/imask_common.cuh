@@ -62,6 +62,7 @@ enum class Knob {
   kAdjCtas,          // IMASK_ADJ_CTAS: "f:ctas_per_sm,..." adjoint split target
   kFwdTwoDet,        // IMASK_FWD_TWO_DET (0/1): two detectors per thread in the TMA forward (f >= 2)
   kFusedStage,       // IMASK_FUSED_STAGE (0/1): x -> value planes in one kernel
+  kFwdTwoDetMinWaves,  // IMASK_FWD_TWO_DET_MIN_WAVES: two-detector grids need >= this x SMs CTAs
   kCount
 };
 // Integer value of a switch, or `dflt` when unset (a set-but-valueless flag

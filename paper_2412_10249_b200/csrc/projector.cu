@@ -783,16 +783,20 @@ int sm_count() {
 }
 }  // namespace
 
-// Value-plane staging (kVal) where the grid is large (the whole angle set):
-// its CTAs take half the shared memory, so they co-reside with the concurrent
-// adjoint's (f=1 step 932 -> 907 us on one GPU) while the projection alone runs
-// as fast. A small grid (an angle shard: a fraction of a wave) runs latency-
-// bound along each CTA's band walk, where the extra packed subtractions cost
-// (1/8 and 1/4 shards' f=1 forward +7% / +15%), so it stages both planes.
+// Value-plane staging (kVal): its CTAs take half the shared memory, so they
+// co-reside with the concurrent adjoint's (f=1 step 932 -> 907 us on one GPU)
+// while the projection alone runs as fast. On a small grid (an angle shard: a
+// fraction of a wave, latency-bound along each CTA's band walk) the extra
+// packed subtractions make the projection alone slower (1/4 shard's f=1
+// forward 169 -> 188 us), but with the fused staging x -> value planes
+// (k_stage32) the shard steps are faster too (f=1 step: 1/8 shard 167.5 ->
+// 161.3 us on rank 0, 148.8 -> 138.7 us on rank 7; 1/4 shard 270 -> 262 us),
+// so every grid stages value planes (IMASK_FWD_VAL=0: both planes).
 bool forward_tma_val(int ctas) {
+  (void)ctas;
   const int forced = knob(Knob::kFwdVal, -1);
   if (forced == 0 || forced == 1) return forced == 1;
-  return ctas >= 6 * sm_count();
+  return true;
 }
 
 bool forward_tma_val_grid(int n_det, int n_entries) {
