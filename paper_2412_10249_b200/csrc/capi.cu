@@ -81,7 +81,8 @@ const char* const kKnobNames[(int)Knob::kCount] = {
     "IMASK_NO_TMA", "IMASK_NO_QUAD", "IMASK_NO_QUAD_L1", "IMASK_FWD_VAL", "IMASK_FWD_VAL_L1",
     "IMASK_TMA_MIN_N", "IMASK_ADJ_AFTER_STAGE_MIN_N", "IMASK_SAGA_SPLIT_MIN_N",
     "IMASK_ADJ_WIN_KB", "IMASK_ADJ_CLUSTER", "IMASK_ADJ_TILE", "IMASK_ADJ_CTAS",
-    "IMASK_FWD_TWO_DET", "IMASK_FUSED_STAGE", "IMASK_FWD_TWO_DET_MIN_WAVES"};
+    "IMASK_FWD_TWO_DET", "IMASK_FUSED_STAGE", "IMASK_FWD_TWO_DET_MIN_WAVES",
+    "IMASK_ADJ_ROW_PAIR"};
 
 std::string g_knob_vals[(int)Knob::kCount];
 bool g_knob_set[(int)Knob::kCount];

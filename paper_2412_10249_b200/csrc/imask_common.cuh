@@ -63,6 +63,7 @@ enum class Knob {
   kFwdTwoDet,        // IMASK_FWD_TWO_DET (0/1): two detectors per thread in the TMA forward (f >= 2)
   kFusedStage,       // IMASK_FUSED_STAGE (0/1): x -> value planes in one kernel
   kFwdTwoDetMinWaves,  // IMASK_FWD_TWO_DET_MIN_WAVES: two-detector grids need >= this x SMs CTAs
+  kAdjRowPair,       // IMASK_ADJ_ROW_PAIR (0/1): the f=1 symmetric adjoint on row pairs (off)
   kCount
 };
 // Integer value of a switch, or `dflt` when unset (a set-but-valueless flag

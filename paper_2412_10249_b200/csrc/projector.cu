@@ -931,13 +931,32 @@ __device__ __forceinline__ float angle0_value(const float* __restrict__ sino, co
 #ifndef IMASK_ADJ_SYM_MINB
 #define IMASK_ADJ_SYM_MINB 7
 #endif
-template <bool kPair, int T, bool kSym, int kPPT>
+// kRP (row pairs; factor 1, mirror symmetry, T = 32): a thread's eight pixels
+// are four pairs of vertically adjacent pixels. At f = 1 the lower pixel's
+// footprint sits sin(theta) in [0, 1] bins further on (angles in [0, pi)),
+// so its two bins are the upper pixel's two or the next two: one window of
+// single bins (y_a[k], y_{n-a}[k]) read at k, k+1, k+2 feeds both pixels
+// and their mirrors (3 LDS.64 per pixel pair and angle instead of 2 LDS.128)
+// with packed FMAs, the same float operations in the same order as the
+// pair path, so the backprojection is bit-identical.
+template <int T, bool kRP>
+__device__ __forceinline__ void adj_pix(int p, int k, int& dx, int& dy) {
+  if constexpr (kRP) {
+    dx = ((p >> 5) << 3) + (((p >> 4) & 1) << 2) + (p & 3);
+    dy = 2 * (((p >> 2) & 3) + 4 * (k >> 1)) + (k & 1);
+  } else {
+    adj_pixel<T>(p, k, dx, dy);
+  }
+}
+
+template <bool kPair, int T, bool kSym, int kPPT, bool kRP = false>
 __global__ void __launch_bounds__(kAdjThreads, kSym ? IMASK_ADJ_SYM_MINB : 8)
 k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W, int CA,
           int a_begin, int a_per_split, int a_end, int n_mirror, int n_det,
           const AdjAngle* __restrict__ ang, int add_a0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  using WinT = typename AdjWin<kPair, kSym>::T;
+  static_assert(!kRP || (kPair && kSym && T == 32 && kPPT == 8), "row pairs: f = 1 symmetric");
+  using WinT = typename AdjWin<kPair && !kRP, kSym>::T;
   constexpr int lanes = T * T / kPPT;
   constexpr int G = kAdjThreads / lanes;
   static_assert(lanes == (T == 32 ? 128 : 32), "adj_pixel layout");
@@ -953,7 +972,7 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
   const int a_lo = a_begin + blockIdx.z * a_per_split;
   const int a_hi = min(a_end, a_lo + a_per_split);
   int dx, dy;
-  adj_pixel<T>(pix0, 0, dx, dy);
+  adj_pix<T, kRP>(pix0, 0, dx, dy);
   const int warp = tid >> 5, lane = tid & 31;
   float acc[NACC][kPPT];
 #pragma unroll
@@ -1005,7 +1024,9 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
         const int j = jb + k;
         const bool in0 = j >= 0 && j < n_det, in1 = j + 1 >= 0 && j + 1 < n_det;
         const float v0 = in0 ? __ldg(yrow + j) * wsc : 0.f;
-        if constexpr (kPair && kSym) {
+        if constexpr (kRP) {
+          win[t * W + k] = make_float2(v0, in0 ? __ldg(mrow + j) * wsc : 0.f);
+        } else if constexpr (kPair && kSym) {
           win[t * W + k] = make_float4(v0, in1 ? __ldg(yrow + j + 1) * wsc : 0.f,
                                        in0 ? __ldg(mrow + j) * wsc : 0.f,
                                        in1 ? __ldg(mrow + j + 1) * wsc : 0.f);
@@ -1019,7 +1040,39 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
       }
     }
     __syncthreads();
-    if constexpr (kPair) {
+    if constexpr (kRP) {
+      const float2* win2 = reinterpret_cast<const float2*>(win);
+#pragma unroll 2
+      for (int t = 0; t < na; ++t) {
+        const AdjStage s = st[t];
+        Fix32 e = fix_from(s.E0 + (long long)dx * s.Dc + (long long)dy * s.Ds);
+        const Fix32 estep = fix_from(8 * s.Ds);  // next pair: 8 rows down
+        const Fix32 eds = fix_from(s.Ds);        // the lower pixel: one row down
+#pragma unroll
+        for (int k2 = 0; k2 < kPPT / 2; ++k2) {
+          const float2 v0 = win2[e.hi], v1 = win2[e.hi + 1], v2 = win2[e.hi + 2];
+          Fix32 eb = e;
+          fix_add(eb, eds);
+          const bool cy = eb.hi != e.hi;
+          const float oa = onep32(e.lo), ob = onep32(eb.lo);
+          const float w0a = __saturatef(fmaf(fabsf(s.c0 - oa), s.kneg, s.Rk));
+          const float w1a = __saturatef(fmaf(oa, s.k1a, s.k1b));
+          const float w0b = __saturatef(fmaf(fabsf(s.c0 - ob), s.kneg, s.Rk));
+          const float w1b = __saturatef(fmaf(ob, s.k1a, s.k1b));
+          float2 pa = make_float2(acc[0][2 * k2], acc[1][2 * k2]);
+          float2 pb = make_float2(acc[0][2 * k2 + 1], acc[1][2 * k2 + 1]);
+          pa = ffma2(w0a, v0, pa);
+          pa = ffma2(w1a, v1, pa);
+          pb = ffma2(w0b, cy ? v1 : v0, pb);
+          pb = ffma2(w1b, cy ? v2 : v1, pb);
+          acc[0][2 * k2] = pa.x;
+          acc[1][2 * k2] = pa.y;
+          acc[0][2 * k2 + 1] = pb.x;
+          acc[1][2 * k2 + 1] = pb.y;
+          fix_add(e, estep);
+        }
+      }
+    } else if constexpr (kPair) {
 #pragma unroll 2
       for (int t = 0; t < na; ++t) {
         const AdjStage s = st[t];
@@ -1095,7 +1148,7 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
   auto store = [&](int i, float v) {
     const int q = i / (lanes * kPPT), r = i % (lanes * kPPT);
     int px, py;
-    adj_pixel<T>(r % lanes, r / lanes, px, py);
+    adj_pix<T, kRP>(r % lanes, r / lanes, px, py);
     const int row = y0 + py;
     const int col = q == 0 ? x0 + px : n - 1 - (x0 + px);
     if (row < n && col >= 0 && col < n) {
@@ -1245,6 +1298,8 @@ void init_kernel_attributes() {
 #define ADJ_ATTR(P_, T_, S_, K_)                                                          \
   cudaFuncSetAttribute(k_adjoint<P_, T_, S_, K_>,                                        \
                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
+  cudaFuncSetAttribute(k_adjoint<true, 32, true, 8, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   ADJ_ATTR(true, 32, false, 8);
   ADJ_ATTR(true, 32, true, 8);
   ADJ_ATTR(false, 32, false, 8);
@@ -1326,7 +1381,7 @@ int adjoint_planes(int n, int factor, int n_loc, bool sym, int sym_s) {
   return planes > 1 ? planes : 0;
 }
 
-template <bool kPair, int T, bool kSym>
+template <bool kPair, int T, bool kSym, bool kRP = false>
 static void adj_launch_(dim3 grid, size_t smem, cudaStream_t stream, int cz, const float* sino,
                         float* dst, int n, int W, int CA, int a_begin, int per_split, int a_end,
                         int n_mirror, int n_det, const AdjAngle* ang, int add_a0) {
@@ -1342,14 +1397,19 @@ static void adj_launch_(dim3 grid, size_t smem, cudaStream_t stream, int cz, con
   attr[0].val.clusterDim.z = (unsigned)cz;
   cfg.attrs = attr;
   cfg.numAttrs = cz > 1 ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, k_adjoint<kPair, T, kSym, (T >= 16 ? 8 : 2)>, sino, dst, n, W, CA,
-                     a_begin, per_split, a_end, n_mirror, n_det, ang, add_a0);
+  cudaLaunchKernelEx(&cfg, k_adjoint<kPair, T, kSym, (T >= 16 ? 8 : 2), kRP>, sino, dst, n, W,
+                     CA, a_begin, per_split, a_end, n_mirror, n_det, ang, add_a0);
 }
 
 static void adj_dispatch(bool pair, int T, bool sym, dim3 grid, size_t smem, cudaStream_t stream,
                          int cz, const float* sino, float* dst, int n, int W, int CA, int a_begin,
                          int per_split, int a_end, int n_mirror, int n_det, const AdjAngle* ang,
-                         int add_a0) {
+                         int add_a0, bool rp = false) {
+  if (rp) {
+    adj_launch_<true, 32, true, true>(grid, smem, stream, cz, sino, dst, n, W, CA, a_begin,
+                                      per_split, a_end, n_mirror, n_det, ang, add_a0);
+    return;
+  }
 #define ADJ_CALL(P_, T_, S_)                                                                   \
   adj_launch_<P_, T_, S_>(grid, smem, stream, cz, sino, dst, n, W, CA, a_begin, per_split, a_end, \
                           n_mirror, n_det, ang, add_a0)
@@ -1420,14 +1480,19 @@ cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n,
   const int planes = S / cz;
   float* dst = planes > 1 ? partial : out;
   int CA;
-  const size_t smem = adj_smem(pair, sym, T, W, &CA);
+  // factor 1 with mirror symmetry: the row-pair kernel (single-bin windows) is
+  // bit-identical but measured slower (whole-set f=1 adjoint 515 -> 524 us,
+  // 1/8 shard 81 -> 85 us: the carry selects cost more issue than the 25%
+  // fewer shared wavefronts save), so it is an A/B switch, off by default
+  const bool rp = pair && sym && knob(Knob::kAdjRowPair, 0) != 0;
+  const size_t smem = adj_smem(pair && !rp, sym, T, W, &CA);
   if (sym) {
     // rows [sym_s, n_loc) with their mirrors over the left-half tiles; the
     // unpaired angle 0 (rows [0, sym_s)) in the epilogue
     const int per_split = (n_loc - sym_s + S - 1) / S;
     dim3 grid(n / (2 * T), (n + T - 1) / T, S);
     adj_dispatch(pair, T, true, grid, smem, stream, cz, sino, dst, n, W, CA, sym_s, per_split,
-                 n_loc, sym_s + n_loc - 1, n_det, ang, sym_s > 0 ? 1 : 0);
+                 n_loc, sym_s + n_loc - 1, n_det, ang, sym_s > 0 ? 1 : 0, rp);
   } else {
     const int per_split = (n_loc + S - 1) / S;
     dim3 grid((n + T - 1) / T, (n + T - 1) / T, S);

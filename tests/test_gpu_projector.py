@@ -274,3 +274,30 @@ def test_forward_paths_bit_identical(geom_args, monkeypatch):
         _lib.check(_lib.lib().imask_reload_switches())
     for name in outs:
         assert np.array_equal(outs["quad"], outs[name]), name
+
+@pytest.mark.parametrize("geom_args,world,rank", [((1024, 1440, 1449), 1, 0), ((256, 360, 363), 1, 0),
+                                                  ((256, 360, 363), 4, 1), ((64, 90, 91), 1, 0)])
+def test_adjoint_row_pairs_bit_identical(geom_args, world, rank, monkeypatch):
+    """The f=1 symmetric adjoint on row pairs (single-bin windows shared by two
+    vertically adjacent pixels; an A/B variant, off by default) and the
+    pair-window kernel evaluate the same weights and sums in the same order:
+    bit-identical backprojections."""
+    from paper_2412_10249_b200 import _lib
+
+    geom = ctmodel.Geometry(*geom_args)
+    rows = ctmodel.shard_angles(geom.n_angles, rank, world)
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    y = torch.randn(len(rows) * geom.n_detectors, device="cuda", generator=gen)
+    outs = {}
+    try:
+        for name, val in (("rows", "1"), ("pairs", "0")):
+            monkeypatch.setenv("IMASK_ADJ_ROW_PAIR", val)
+            _lib.check(_lib.lib().imask_reload_switches())
+            plan = ctmodel.Plan(geom, angles=rows)
+            assert plan.symmetric
+            outs[name] = host(plan.backproject(y, 1))
+            del plan
+    finally:
+        monkeypatch.delenv("IMASK_ADJ_ROW_PAIR", raising=False)
+        _lib.check(_lib.lib().imask_reload_switches())
+    assert np.array_equal(outs["rows"], outs["pairs"])
