@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import threading
 from dataclasses import dataclass
 from typing import Optional, Sequence
@@ -117,6 +118,50 @@ def shard_angles(n_angles: int, rank: int, world: int) -> tuple:
     return tuple(([0] if rank == 0 else []) + mine + mirrors)
 
 
+_FWD_GROUP = 8  # entries per TMA forward CTA (projector.cu kFE)
+
+
+def _shard_quads_cyclic(n_angles: int, rank: int, world: int):
+    """Block-cyclic quad shards, or None where they do not apply.
+
+    The whole set's forward entry list (capi.cu: the singles 0 and n/2, the
+    quads of a = 1..n/4-1, the pair {n/4, 3n/4}) is cut into the groups of 8
+    adjacent entries one forward CTA traces, and rank p takes the groups
+    g = p (mod world): every rank gets the same mix of near-axis and oblique
+    angles (a contiguous run gives rank 0 the near-axis ones, whose rays leave
+    a third of the detector blocks empty), while a CTA's eight entries stay
+    adjacent in angle, as its shared TMA windows need. Used when every rank
+    gets >= 4 whole groups; the entries beyond the last whole cycle are cut
+    into contiguous runs, so the row counts differ by a few rows only."""
+    if os.environ.get("IMASK_SHARD_CYCLIC", "1") == "0":
+        return None
+    h, q = n_angles // 2, n_angles // 4
+    n_entries = q + 2
+    if n_entries // _FWD_GROUP < 4 * world:
+        return None
+    # whole cycles of groups go round-robin; the entries left over (fewer than
+    # `world` groups) are cut into `world` contiguous runs, one short CTA each
+    n_cyc = (n_entries // _FWD_GROUP // world) * world
+    rest = n_entries - n_cyc * _FWD_GROUP
+    lo = n_cyc * _FWD_GROUP + (rest * rank) // world
+    hi = n_cyc * _FWD_GROUP + (rest * (rank + 1)) // world
+    mine = [e for g in range(rank, n_cyc, world)
+            for e in range(g * _FWD_GROUP, (g + 1) * _FWD_GROUP)] + list(range(lo, hi))
+    low = set()
+    for e in mine:
+        if e == 0:
+            continue  # angle 0: first row of its rank's list
+        if e == 1:
+            low.add(h)
+        elif e == q + 1:
+            low.add(q)
+        else:
+            low.update((e - 1, h - (e - 1)))
+    low = sorted(low)
+    mirrors = sorted(n_angles - a for a in low if a != h)
+    return tuple(([0] if rank == 0 else []) + low + mirrors)
+
+
 def _shard_quads(n_angles: int, rank: int, world: int) -> tuple:
     """shard_angles when n_angles % 4 == 0: shards closed under the mirror
     a -> n - a and the transpose a -> n/2 - a as well, so every rank's forward
@@ -126,6 +171,9 @@ def _shard_quads(n_angles: int, rank: int, world: int) -> tuple:
     ascending + their mirrors ascending."""
     h, q = n_angles // 2, n_angles // 4
     quads = list(range(1, q))
+    cyc = _shard_quads_cyclic(n_angles, rank, world)
+    if cyc is not None:
+        return cyc
     # rows before unit i: rank 0's two singles, four per quad; the pair adds 2 at the end
     cum = 2 + 4 * np.arange(1, len(quads) + 1)
     edges = [0] + [int(np.searchsorted(cum, (k + 1) * n_angles / world - 0.5)) + 1

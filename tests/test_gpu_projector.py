@@ -206,10 +206,14 @@ def test_slab_rows_match_full():
     assert rel_l2(bp_sum, ref) <= 1e-6
 
 
-@pytest.mark.parametrize("n_angles,world", [(90, 2), (90, 3), (91, 4), (180, 8)])
+@pytest.mark.parametrize("n_angles,world", [(90, 2), (90, 3), (91, 4), (180, 8), (360, 2)])
 def test_mirror_closed_shards_match_full(n_angles, world):
     """Every shard of shard_angles runs the symmetric kernels; its rows equal the
-    full plan's rows, and the shards' backprojections sum to the full one."""
+    full plan's rows, and the shards' backprojections sum to the full one.
+    (360 angles on 2 ranks: the block-cyclic quad shards.)"""
+    if n_angles == 360:
+        a0 = ctmodel.shard_angles(n_angles, 0, world)
+        assert 6 in a0 and 7 not in a0 and 15 in a0  # groups of 8 forward entries alternate
     geom = ctmodel.Geometry(64, n_angles, 91)
     x = dev(ellipse_phantom(64, 6).ravel())
     y = np.random.default_rng(3).standard_normal(geom.m).reshape(n_angles, 91)

@@ -22,6 +22,7 @@ from paper_2412_10249_b200.synth import CONFIGS  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--worlds", default="1,2,4,8")
 ap.add_argument("--reps", type=int, default=30)
+ap.add_argument("--all-ranks", action="store_true")
 args = ap.parse_args()
 cfg = CONFIGS["D"]
 r = cfg.levels
@@ -36,7 +37,7 @@ prm = solvers._params(1e-6, cfg.mu_g, cfg.mu_g)
 results = {}
 for W in [int(w) for w in args.worlds.split(",")]:
     per_rank = []
-    for rank in sorted({0, W - 1}):
+    for rank in (range(W) if args.all_ranks else sorted({0, W - 1})):
         idx = torch.as_tensor(ctmodel.shard_angles(geom.n_angles, rank, W), device=dev)
         b_loc = b_full.reshape(geom.n_angles, geom.n_detectors)[idx].reshape(-1).contiguous()
         prob = dist_mod.make_sharded_problem(geom, b_loc, fam, cfg.mu_g, rank=rank, world=W)
