@@ -652,6 +652,37 @@ def main():
         torch.cuda.synchronize()
         return float(np.mean([ev[2 * q].elapsed_time(ev[2 * q + 1]) for q in range(reps)]))
 
+    # the same launch back to back over rotating image-side buffer sets (x, phi_sum,
+    # phi table, bp) whose total exceeds L2, events around the whole batch: the
+    # per-launch time without the ~6 us an event pair adds around one small launch
+    # (tools/probes/stream_probe.cu: an empty kernel reads 6.1 us between events,
+    # a plain float4 kernel of the same traffic 8.2 / 10.2 us cold and 6.3 / 7.8 us
+    # back to back, whatever its grid shape)
+    n_sets = 12
+    tab_len = st.phi_tab.numel()
+    sets = []
+    for _ in range(n_sets):
+        bufs = [torch.zeros(cfg.d, device=device) for _ in range(3)] + \
+               [torch.zeros(tab_len, device=device)]
+        cs = _lib.ImaskState(bufs[0].data_ptr(), st.y.data_ptr(), eng.b.data_ptr(),
+                             bufs[1].data_ptr(), st.psi_sum.data_ptr(), bufs[3].data_ptr(),
+                             st.psi_tab.data_ptr(), bufs[2].data_ptr(), None, None)
+        sets.append((bufs, cs))
+
+    def time_image_b2b(level0):
+        rounds = []
+        for q in range(8):
+            flush_sink.copy_(flush.sum())
+            ev[0].record(stream)
+            for _, cs in sets:
+                _lib.check(_lib.lib().imask_step_image(plan.handle, ctypes.byref(cs), level0,
+                                                       ctypes.byref(prm), plan.stream))
+            ev[1].record(stream)
+            torch.cuda.synchronize()
+            if q >= 2:
+                rounds.append(ev[0].elapsed_time(ev[1]) / n_sets)
+        return float(np.median(rounds))
+
     hbm_kernels = []
     for level0, name in ((r - 1, "k_saga_image_full32 (f=1, compensation fused)"),
                          (0, f"k_saga_image_coarse32 (f={2 ** (r - 1)})")):
@@ -660,9 +691,16 @@ def main():
         nbytes = 4.0 * (7 * cfg.d) if f == 1 else 4.0 * (4 * cfg.d + 3 * di)
         ms = time_image(level0)
         gbs = nbytes / (ms * 1e-3) / 1e9
+        ms_b = time_image_b2b(level0)
+        gbs_b = nbytes / (ms_b * 1e-3) / 1e9
         hbm_kernels.append({"kernel": name, "algorithmic_bytes": nbytes, "avg_launch_ms": round(ms, 4),
                             "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                             "frac": round(gbs / hbm_peak, 4),
+                            "back_to_back": {
+                                "avg_launch_ms": round(ms_b, 4), "achieved": round(gbs_b, 1),
+                                "frac": round(gbs_b / hbm_peak, 4), "sets": n_sets,
+                                "note": "launches over rotating buffer sets larger than L2, "
+                                        "events around the batch (no per-launch event overhead)"},
                             "traffic": traffic_tab.get("saga_image_full" if f == 1 else
                                                        "saga_image_coarse"),
                             "traffic_note": "ncu DRAM bytes of the launch inside the fused step "

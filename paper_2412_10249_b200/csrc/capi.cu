@@ -58,6 +58,7 @@ cudaError_t launch_resum(const float* phi_tab, float* phi_sum, int side, const f
 void init_kernel_attributes();
 int forward_tma_entries_per_cta();
 int forward_tma_window();
+int forward_tma_bands(bool quad, bool val);
 struct TmaMaps {
   CUtensorMap row, row_m, col, col_m;
 };
@@ -357,7 +358,9 @@ int get_tables(imask_plan* pl, int f, LevelTables** out) {
     }
     if (pl->sym && !knob(Knob::kNoTma, 0)) {
       const int n = pl->side / f;
-      const unsigned bh = pl->tma_quad ? 8 : 16;
+      // box height = bands per chunk of the TMA kernel this level launches
+      const bool val = t.two_det || forward_tma_val_grid(pl->n_det, pl->n_tma_entries);
+      const unsigned bh = (unsigned)forward_tma_bands(pl->tma_quad, val);
       t.tma = encode_pair_map(&t.maps.row, pl->P, n, bh) &&
               encode_pair_map(&t.maps.row_m, pl->PM, n, bh) &&
               encode_pair_map(&t.maps.col, pl->PT, n, bh) &&

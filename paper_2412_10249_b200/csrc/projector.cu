@@ -335,6 +335,14 @@ k_forward_quad(const float2* __restrict__ P, const float2* __restrict__ PT,
 // rounded down to an even pair index: a tensor copy must start 16-byte aligned.
 constexpr int kFB = 16;           // bands per chunk (pair mode)
 constexpr int kFBQuad = 8;        // bands per chunk (quad mode: twice the images)
+#ifndef IMASK_FWD_FBQ
+#define IMASK_FWD_FBQ 16
+#endif
+// quad mode on value planes stages two images per chunk, like pair mode on both
+// planes: chunks of 16 bands halve the per-chunk work of every warp (barrier
+// wait, window origin, position rebuild, release: ~80 of the ~210 instructions
+// a warp spent per 8-band chunk)
+constexpr int kFBQuadVal = IMASK_FWD_FBQ;
 #ifndef IMASK_FWD_ENTRIES
 #define IMASK_FWD_ENTRIES 8
 #endif
@@ -345,7 +353,7 @@ constexpr int kFE = IMASK_FWD_ENTRIES;  // entries per CTA (4 per warp row, kFE 
 constexpr int kFThreads = kFE * 32;     // 8 detectors x 4 entries per warp, 32 detectors per CTA
 constexpr int kFWc = IMASK_FWD_WINDOW;  // window width in pair columns: the TMA box; the
                                         // window write costs kFWc / (32 kFE) of the reads
-constexpr int kFMaxChunks = 1024;  // side up to 8192
+constexpr int kFMaxChunks = 1024;  // side up to 8192 (the tables hold the launch's own chunk count)
 
 struct TmaMaps {
   CUtensorMap row, row_m, col, col_m;  // P, PM, PT, PTM of one level
@@ -414,8 +422,8 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
               const float2* __restrict__ PT, const float2* __restrict__ PM,
               const float2* __restrict__ PTM, int n, int pitch, const FwdAngle* __restrict__ ang,
               const int4* __restrict__ entries, int n_entries, int row_ctas, int n_det,
-              float* __restrict__ sino, SinoSaga saga) {
-  constexpr int FB = kQuad ? kFBQuad : kFB;  // bands per chunk
+              float* __restrict__ sino, SinoSaga saga, int nch_cap) {
+  constexpr int FB = kQuad ? (kVal ? kFBQuadVal : kFBQuad) : kFB;  // bands per chunk
   // staged images per chunk: kVal stages only the value planes (P, and PT in
   // quad mode) and forms the difference pair of column c as P[c+1] - P[c], the
   // subtraction k_prepare does for the difference planes (bit-identical sums,
@@ -430,7 +438,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   uint64_t* empty = full + 2;
   FwdWarpInfo* info = reinterpret_cast<FwdWarpInfo*>(empty + 2);
   int* cmin_tab = reinterpret_cast<int*>(info + kFE);
-  int* ctl = cmin_tab + kFMaxChunks;  // [0] overflow, [1] first band, [2] chunks, then cmax_tab
+  int* ctl = cmin_tab + nch_cap;  // [0] overflow, [1] first band, [2] chunks, then cmax_tab
 
   // A warp holds 4 entries x 8 consecutive detectors (lane = 8 q + d): each
   // half-warp's 8-byte window reads then span ~10 pair columns of one band,
@@ -483,7 +491,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   // per entry slot (8 per CTA): positions of its first and last detector and the
   // union of the lockstep band ranges of the four warps holding it (every lane
   // walks its warp's whole range)
-  int* cmax_tab = ctl + 4;  // [kFMaxChunks]
+  int* cmax_tab = ctl + 4;  // [nch_cap]
   if (threadIdx.x < kFE) {
     info[threadIdx.x] = FwdWarpInfo{0, 0, 0, n, 0};
     ctl[0] = 0;
@@ -510,7 +518,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
     }
     ctl[1] = blo;
     ctl[2] = bhi > blo ? (bhi - blo + FB - 1) / FB : 0;
-    if (ctl[2] > kFMaxChunks) ctl[0] = 1;
+    if (ctl[2] > nch_cap) ctl[0] = 1;
   }
   __syncthreads();
   const int blo = ctl[1], nch = ctl[2];
@@ -765,10 +773,20 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   }
 }
 
-size_t forward_tma_smem(bool val) {
-  // both modes stage 2 x (1 or 2) x 16 or 2 x (2 or 4) x 8 bands of kFWc pairs
-  return (val ? 1 : 2) * 2 * kFB * kFWc * sizeof(float2) + 4 * sizeof(uint64_t) +
-         kFE * sizeof(FwdWarpInfo) + (2 * kFMaxChunks + 4) * sizeof(int);
+int forward_tma_bands(bool quad, bool val) { return quad ? (val ? kFBQuadVal : kFBQuad) : kFB; }
+
+// chunk-table entries a launch on an n-band image needs
+static int forward_tma_chunk_cap(int n, bool quad, bool val) {
+  const int fb = forward_tma_bands(quad, val);
+  const int cap = (n + fb - 1) / fb + 2;
+  return cap < kFMaxChunks ? cap : kFMaxChunks;
+}
+
+size_t forward_tma_smem(bool val, bool quad, int nch_cap) {
+  // two stages of (1 or 2) x (quad: 2) images of FB bands x kFWc pairs
+  const size_t ni = (quad ? 2 : 1) * (val ? 1 : 2);
+  return 2 * ni * forward_tma_bands(quad, val) * kFWc * sizeof(float2) + 4 * sizeof(uint64_t) +
+         kFE * sizeof(FwdWarpInfo) + (2 * (size_t)nch_cap + 4) * sizeof(int);
 }
 
 namespace {
@@ -811,13 +829,14 @@ cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float
   const int kk = two_det ? 2 : 1;
   dim3 grid((n_det + 32 * kk - 1) / (32 * kk), (n_entries + kFE - 1) / kFE);
   const bool val = two_det || forward_tma_val((int)(grid.x * grid.y));
-  const size_t smem = forward_tma_smem(val);
+  const int cap = forward_tma_chunk_cap(n, quad, val);
+  const size_t smem = forward_tma_smem(val, quad, cap);
   SinoSaga none{};
   const SinoSaga sg = saga ? *saga : none;
   float* out = saga ? nullptr : sino;
 #define FWD_TMA(S_, Q_, V_, K_)                                                                  \
   launch_pdl(k_forward_tma<S_, Q_, V_, K_>, grid, dim3(kFThreads), smem, stream, maps, P, PT, PM, \
-             PTM, n, pair_pitch(n), ang, entries, n_entries, row_ctas, n_det, out, sg)
+             PTM, n, pair_pitch(n), ang, entries, n_entries, row_ctas, n_det, out, sg, cap)
 #define FWD_TMA_V(S_, Q_)                                 \
   if (two_det) FWD_TMA(S_, Q_, true, 2);                  \
   else if (val) FWD_TMA(S_, Q_, true, 1);                 \
@@ -1277,7 +1296,7 @@ cudaError_t launch_forward(const float2* P, const float2* PT, const float2* PM, 
 void init_kernel_attributes() {
 #define FWD_ATTR(S_, Q_, V_)                                                                  \
   cudaFuncSetAttribute(k_forward_tma<S_, Q_, V_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                       (int)forward_tma_smem(V_))
+                       (int)forward_tma_smem(V_, Q_, kFMaxChunks))
   FWD_ATTR(true, false, false);
   FWD_ATTR(false, false, false);
   FWD_ATTR(true, true, false);
@@ -1289,7 +1308,8 @@ void init_kernel_attributes() {
 #undef FWD_ATTR
 #define FWD_ATTR2(S_, Q_)                                                                    \
   cudaFuncSetAttribute(k_forward_tma<S_, Q_, true, 2>,                                       \
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)forward_tma_smem(true))
+                       cudaFuncAttributeMaxDynamicSharedMemorySize,                            \
+                       (int)forward_tma_smem(true, Q_, kFMaxChunks))
   FWD_ATTR2(true, true);
   FWD_ATTR2(false, true);
   FWD_ATTR2(true, false);

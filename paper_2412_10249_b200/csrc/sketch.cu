@@ -232,7 +232,7 @@ __device__ __forceinline__ float saga_px(float pn, float& tab, float& sum, float
 
 // Full level, fast path: phi_new = S_r(bp) by the 32x32 tile pyramid, then the
 // SAGA image update, all with 128-bit accesses.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 6)  // 40 registers: 888 of the 1024 CTAs of a 1024^2 image resident
 k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, ImageSaga sg) {
   __shared__ __align__(16) Pyr32Smem sm;
   const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
