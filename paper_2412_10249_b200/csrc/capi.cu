@@ -83,7 +83,7 @@ const char* const kKnobNames[(int)Knob::kCount] = {
     "IMASK_TMA_MIN_N", "IMASK_ADJ_AFTER_STAGE_MIN_N", "IMASK_SAGA_SPLIT_MIN_N",
     "IMASK_ADJ_WIN_KB", "IMASK_ADJ_CLUSTER", "IMASK_ADJ_TILE", "IMASK_ADJ_CTAS",
     "IMASK_FWD_TWO_DET", "IMASK_FUSED_STAGE", "IMASK_FWD_TWO_DET_MIN_WAVES",
-    "IMASK_ADJ_ROW_PAIR"};
+    "IMASK_ADJ_ROW_PAIR", "IMASK_FWD_TWO_DET_MIN_N"};
 
 std::string g_knob_vals[(int)Knob::kCount];
 bool g_knob_set[(int)Knob::kCount];
@@ -354,6 +354,11 @@ int get_tables(imask_plan* pl, int f, LevelTables** out) {
       int sms = 148;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->device);
       if (ctas2 < (long long)knob(Knob::kFwdTwoDetMinWaves, 6) * sms) ok = false;
+      // with 16-band chunks (half the per-chunk work per ray) one detector per
+      // thread is faster on coarse sides below 512 (config D, in the step:
+      // f=4 223 -> 217 us, f=8 137 -> 132 us); at n = 512 the two-detector
+      // kernel's smaller footprint beside the adjoint still wins (354 vs 359 us)
+      if (pl->side / f < knob(Knob::kFwdTwoDetMinN, 512)) ok = false;
       t.two_det = ok;
     }
     if (pl->sym && !knob(Knob::kNoTma, 0)) {
