@@ -225,6 +225,9 @@ k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
 // Singles and the pair (n/4, 3n/4) come as entries with -1 slots; padding
 // entries (all -1) idle. L1-cached loads: the coarse levels, where the images
 // fit on chip and the walks are short.
+#ifndef IMASK_FWDQ_UNROLL
+#define IMASK_FWDQ_UNROLL 4
+#endif
 template <bool kSaga, bool kVal>
 __global__ void __launch_bounds__(256, 4)
 k_forward_quad(const float2* __restrict__ P, const float2* __restrict__ PT,
@@ -264,12 +267,15 @@ k_forward_quad(const float2* __restrict__ P, const float2* __restrict__ PT,
   griddep_wait();  // the pair images come from the stream predecessor (k_prepare)
   float2 acc2 = make_float2(0.f, 0.f), accT = make_float2(0.f, 0.f);
   int b = wlo;
+  // kU bands per iteration: 4 kU independent 8-byte loads in flight per thread
+  // (the walk is bound by the latency of its L1 loads)
+  constexpr int kU = IMASK_FWDQ_UNROLL;
 #pragma unroll 1
-  for (; b + 2 <= whi; b += 2) {
-    float2 v[2], vd[2], vt[2], vdt[2];
-    float g[2];
+  for (; b + kU <= whi; b += kU) {
+    float2 v[kU], vd[kU], vt[kU], vdt[kU];
+    float g[kU];
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < kU; ++k) {
       v[k] = __ldg(P + Y.hi);
       vt[k] = __ldg(PT + Y.hi);
       if (kVal) {  // difference pairs as P[c+1] - P[c] (k_prepare's subtraction)
@@ -283,7 +289,7 @@ k_forward_quad(const float2* __restrict__ P, const float2* __restrict__ PT,
       fix_add(Y, dY);
     }
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < kU; ++k) {
       if (kVal) {
         vd[k] = fsub2(vd[k], v[k]);
         vdt[k] = fsub2(vdt[k], vt[k]);
@@ -294,7 +300,7 @@ k_forward_quad(const float2* __restrict__ P, const float2* __restrict__ PT,
       accT = ffma2(g[k], vdt[k], accT);
     }
   }
-  if (b < whi) {
+  for (; b < whi; ++b) {
     const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
     const float2 v = __ldg(P + Y.hi), vt = __ldg(PT + Y.hi);
     const float2 vd = kVal ? fsub2(__ldg(P + Y.hi + 1), v) : __ldg(PM + Y.hi);
@@ -303,6 +309,7 @@ k_forward_quad(const float2* __restrict__ P, const float2* __restrict__ PT,
     acc2 = ffma2(g, vd, acc2);
     accT = fadd2(accT, vt);
     accT = ffma2(g, vdt, accT);
+    fix_add(Y, dY);
   }
   if (j < n_det) {
     const float vals[4] = {acc2.x, acc2.y, accT.x, accT.y};
@@ -1039,6 +1046,33 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
       const float wsc = st[t].wsc;
       const float* yrow = sino + (size_t)(a0 + t) * n_det;
       const float* mrow = sino + (size_t)(kSym ? n_mirror - (a0 + t) : 0) * n_det;
+      if (jb >= 0 && jb + W + 1 <= n_det) {
+        // window inside the detector (almost every tile and angle): no edge
+        // tests, 32-bit offsets from two per-angle pointers (the tested loop
+        // below spends ~35 instructions per 32 bins, mostly on predicates and
+        // 64-bit addresses; at f >= 8 staging was a quarter to two fifths of
+        // the kernel's instructions)
+        const float* yp = yrow + jb;
+        const float* mp = mrow + jb;
+        WinT* wt = win + t * W;
+#pragma unroll 4
+        for (unsigned k = lane; k < (unsigned)W; k += 32) {
+          const float v0 = __ldg(yp + k) * wsc;
+          if constexpr (kRP) {
+            wt[k] = make_float2(v0, __ldg(mp + k) * wsc);
+          } else if constexpr (kPair && kSym) {
+            wt[k] = make_float4(v0, __ldg(yp + k + 1) * wsc, __ldg(mp + k) * wsc,
+                                __ldg(mp + k + 1) * wsc);
+          } else if constexpr (kPair) {
+            wt[k] = make_float2(v0, __ldg(yp + k + 1) * wsc);
+          } else if constexpr (kSym) {
+            wt[k] = make_float2(v0, __ldg(mp + k) * wsc);
+          } else {
+            wt[k] = v0;
+          }
+        }
+        continue;
+      }
       for (int k = lane; k < W; k += 32) {
         const int j = jb + k;
         const bool in0 = j >= 0 && j < n_det, in1 = j + 1 >= 0 && j + 1 < n_det;
