@@ -95,7 +95,9 @@ def shard_angles(n_angles: int, rank: int, world: int) -> tuple:
     same rank, so every rank runs the mirror-symmetric kernels. The base angles
     1..floor(n_angles/2) are split contiguously, balancing the row count (two
     rows per base, one for the self-mirrored pi/2 and for angle 0, which rank 0
-    takes). Row order: [0 on rank 0] + bases ascending + mirrors ascending,
+    takes); angle counts divisible by 4 are split by quads (_shard_quads:
+    block-cyclically when every rank gets at least four forward CTA groups).
+    Row order: [0 on rank 0] + bases ascending + mirrors ascending,
     the layout imask_plan_create_list detects. world = 1 gives 0..n_angles-1.
     """
     if world < 1 or not 0 <= rank < world:

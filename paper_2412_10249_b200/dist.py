@@ -1,9 +1,10 @@
 """Angle-sharded multi-GPU ImaSk.
 
 One process per GPU. Rank p owns a mirror-closed angle shard
-(ctmodel.shard_angles): a contiguous run of base angles a in 1..n/2 plus
-their mirrors n - a (theta -> pi - theta), and angle 0 on rank 0, so every
-rank runs the mirror-symmetric kernels; its rows of y, b, the psi table and
+(ctmodel.shard_angles): base angles a in 1..n/2 (block-cyclic groups of the
+forward's eight-entry CTAs, contiguous runs on small angle sets) plus their
+mirrors n - a (theta -> pi - theta), and angle 0 on rank 0, so every rank
+runs the mirror-symmetric kernels; its rows of y, b, the psi table and
 psi_sum live only there. Every rank draws the same level from the
 counter-based RNG, backprojects its shard, and the coarse partial image is
 summed with one NCCL all-reduce -- the only collective -- while the forward
