@@ -773,10 +773,11 @@ def main():
         prob_w = dist_mod.make_sharded_problem(geom, b_host.to(device), fam, cfg.mu_g,
                                                rank, world, group)
         prob_w.engine.capture_all(solvers.init_state(prob_w, seed=SEED), prm)
-        solvers.run(prob_w, "sketch", SIGMA, cfg.mu_g, e2e_steps, record_every=1, seed=SEED,
-                    x_ref=xref_host.to(device))
-        del prob_w
         x_out = torch.empty(cfg.d, dtype=torch.float32).pin_memory()
+        rep_w = solvers.run(prob_w, "sketch", SIGMA, cfg.mu_g, e2e_steps, record_every=1,
+                            seed=SEED, x_ref=xref_host.to(device))
+        x_out.copy_(rep_w.x)  # the warm-up is the identical call, read-back included
+        del prob_w, rep_w
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()

@@ -16,6 +16,7 @@ synthetic inputs live in `synth.py`.
 from __future__ import annotations
 
 import ctypes
+import functools
 import math
 import os
 import threading
@@ -88,7 +89,30 @@ def slab_bounds(n_angles: int, rank: int, world: int) -> tuple[int, int]:
     return begin, begin + base + (1 if rank < extra else 0)
 
 
+class _AngleTuple(tuple):
+    """A tuple of Python ints that has been validated once (angle index lists
+    are passed around per level and per call; re-converting 1440 entries each
+    time was a third of make_problem's host time)."""
+
+
+def _int_tuple(angles) -> "_AngleTuple":
+    if type(angles) is _AngleTuple:
+        return angles
+    return _AngleTuple(int(a) for a in angles)
+
+
 def shard_angles(n_angles: int, rank: int, world: int) -> tuple:
+    """Mirror-closed angle shard of one rank (see _shard_angles; cached)."""
+    return _shard_angles_cached(int(n_angles), int(rank), int(world),
+                                os.environ.get("IMASK_SHARD_CYCLIC", "1"))
+
+
+@functools.lru_cache(maxsize=256)
+def _shard_angles_cached(n_angles: int, rank: int, world: int, _cyclic: str) -> tuple:
+    return _AngleTuple(_shard_angles(n_angles, rank, world))
+
+
+def _shard_angles(n_angles: int, rank: int, world: int) -> tuple:
     """Mirror-closed angle shard of one rank (global indices, local row order).
 
     Angle a and its mirror n_angles - a (theta -> pi - theta) always land on the
@@ -215,12 +239,17 @@ def _ptr(t: torch.Tensor) -> ctypes.c_void_p:
     return ctypes.c_void_p(t.data_ptr())
 
 
+@functools.lru_cache(maxsize=64)
+def _full_range(begin: int, end: int) -> "_AngleTuple":
+    return _AngleTuple(range(begin, end))
+
+
 def _angle_list(geom: Geometry, angles=None, angle_begin: int = 0,
                 angle_end: Optional[int] = None) -> tuple:
     if angles is not None:
-        return tuple(int(a) for a in angles)
+        return _int_tuple(angles)
     angle_end = geom.n_angles if angle_end is None else angle_end
-    return tuple(range(angle_begin, angle_end))
+    return _full_range(angle_begin, angle_end)
 
 
 class Plan:
@@ -383,7 +412,7 @@ def _projector_linop(geom: Geometry, factor: int, scale: float = 1.0, angles=Non
 
     The plan is resolved at first apply (after the caller has picked its CUDA device).
     """
-    angles = None if angles is None else tuple(int(a) for a in angles)
+    angles = None if angles is None else _int_tuple(angles)
     n_rows = geom.n_angles if angles is None else len(angles)
     low = geom.side // factor
     meta = ProjectorMeta(geom, factor, scale, angles)
