@@ -228,8 +228,11 @@ k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
 #ifndef IMASK_FWDQ_UNROLL
 #define IMASK_FWDQ_UNROLL 4
 #endif
+#ifndef IMASK_FWDQ_MINB
+#define IMASK_FWDQ_MINB 4
+#endif
 template <bool kSaga, bool kVal>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, IMASK_FWDQ_MINB)
 k_forward_quad(const float2* __restrict__ P, const float2* __restrict__ PT,
                const float2* __restrict__ PM, const float2* __restrict__ PTM, int n, int pitch,
                const FwdAngle* __restrict__ ang, const int4* __restrict__ entries, int n_entries,
