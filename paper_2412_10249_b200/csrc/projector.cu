@@ -958,7 +958,7 @@ __device__ __forceinline__ float angle0_value(const float* __restrict__ sino, co
 }
 
 #ifndef IMASK_ADJ_SYM_MINB
-#define IMASK_ADJ_SYM_MINB 7
+#define IMASK_ADJ_SYM_MINB 8  // 64 registers: f=1 adjoint 514.7 -> 512.4 us, f=8 80.3 -> 78.4 us, every step -0.2..-1% (A/B, two rounds)
 #endif
 // kRP (row pairs; factor 1, mirror symmetry, T = 32): a thread's eight pixels
 // are four pairs of vertically adjacent pixels. At f = 1 the lower pixel's
