@@ -301,6 +301,14 @@ IMASK_API int imask_prox_tv_nonneg(int side, const float* xp, float* out, double
  * otherwise read once). Plans created afterwards use the new values. */
 IMASK_API int imask_reload_switches(void);
 
+/* Debug helper (no reference counterpart): the index checks of a library built
+ * with -DIMASK_BOUNDS_CHECK=1 (every shared-memory window read of the
+ * projectors and every pair-image read of the L1 forwards against the range
+ * it must stay in). out4 = {violations, first site code, first index, first
+ * limit}; reset != 0 clears the counter. Returns 1 when the checks are
+ * compiled in, 0 when not (out4 zeroed), < 0 on error. */
+IMASK_API int imask_debug_bounds(unsigned long long* out4, int reset);
+
 /* Measurement helper (no reference counterpart): thread-level FP32 FFMA
  * throughput of `device` from an FFMA-chain microbenchmark, the FP32-issue
  * denominator of bench.py's roofline. */

@@ -73,6 +73,7 @@ SIGNATURES = {
     "imask_sq_dist": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _vp]),
     "imask_metric_row": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _vp]),
     "imask_reload_switches": (ctypes.c_int, []),
+    "imask_debug_bounds": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]),
     "imask_plan_create": (
         ctypes.c_int,
         [

@@ -58,6 +58,7 @@ cudaError_t launch_resum(const float* phi_tab, float* phi_sum, int side, const f
 void init_kernel_attributes();
 int forward_tma_entries_per_cta();
 int forward_tma_window();
+bool debug_bounds_read(unsigned long long* out4, bool reset);
 int forward_tma_bands(bool quad, bool val);
 struct TmaMaps {
   CUtensorMap row, row_m, col, col_m;
@@ -800,6 +801,11 @@ int imask_plan_create_list(int side, int n_angles, int n_det, int n_loc, const i
   }
   *out = pl;
   return IMASK_OK;
+}
+
+int imask_debug_bounds(unsigned long long* out4, int reset) {
+  if (!out4) return fail(IMASK_EINVAL, "out4 is null");
+  return debug_bounds_read(out4, reset != 0) ? 1 : 0;
 }
 
 int imask_reload_switches(void) {

@@ -27,6 +27,34 @@ namespace cg = cooperative_groups;
 
 namespace imask {
 
+// Debug build (-DIMASK_BOUNDS_CHECK=1): every shared-memory window read of the
+// projectors and every pair-image read of the L1 forwards is checked against
+// the range it must stay in (the staged window row of its band / angle; the
+// padded image row); violations are counted in a device word the host reads
+// with imask_debug_bounds. compute-sanitizer is closed on the B200 pool, so
+// this build, run through the GPU test suite (tools/gpu_bounds_check.sh),
+// stands in for memcheck on the kernels' computed indices.
+#ifndef IMASK_BOUNDS_CHECK
+#define IMASK_BOUNDS_CHECK 0
+#endif
+#if IMASK_BOUNDS_CHECK
+__device__ unsigned long long g_bounds[4];  // violations, first: site code, index, limit
+__device__ __noinline__ void bounds_fail(int code, long long idx, long long limit) {
+  if (atomicAdd(&g_bounds[0], 1ull) == 0ull) {
+    g_bounds[1] = (unsigned long long)code;
+    g_bounds[2] = (unsigned long long)idx;
+    g_bounds[3] = (unsigned long long)limit;
+  }
+}
+#define IMASK_CHECK_RANGE(code, idx, limit)                                       \
+  do {                                                                            \
+    const long long i_ = (long long)(idx), l_ = (long long)(limit);               \
+    if (i_ < 0 || i_ >= l_) bounds_fail(code, i_, l_);                            \
+  } while (0)
+#else
+#define IMASK_CHECK_RANGE(code, idx, limit) ((void)0)
+#endif
+
 // bands b in [lo, hi) where the ray's left chord partner floor(xi) is in [-1, n-1]
 __device__ __forceinline__ bool band_ok(long long X0, long long step, int b, int n) {
   const long long X = X0 + (long long)b * step;
@@ -101,6 +129,7 @@ k_forward(const float2* __restrict__ P, const float2* __restrict__ PT, int n, in
     float g[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
+      IMASK_CHECK_RANGE(10, Y.hi, (long long)n * pitch);
       v[k] = __ldg(img + Y.hi);
       g[k] = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
       fix_add(Y, dY);
@@ -183,6 +212,7 @@ k_forward_sym(const float2* __restrict__ P, const float2* __restrict__ PT,
     float g[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
+      IMASK_CHECK_RANGE(11, Y.hi, (long long)n * pitch);
       v[k] = __ldg(img + Y.hi);
       vd[k] = __ldg(imgm + Y.hi);
       g[k] = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
@@ -279,6 +309,7 @@ k_forward_quad(const float2* __restrict__ P, const float2* __restrict__ PT,
     float g[kU];
 #pragma unroll
     for (int k = 0; k < kU; ++k) {
+      IMASK_CHECK_RANGE(12, (long long)Y.hi + (kVal ? 1 : 0), (long long)n * pitch);
       v[k] = __ldg(P + Y.hi);
       vt[k] = __ldg(PT + Y.hi);
       if (kVal) {  // difference pairs as P[c+1] - P[c] (k_prepare's subtraction)
@@ -304,6 +335,7 @@ k_forward_quad(const float2* __restrict__ P, const float2* __restrict__ PT,
     }
   }
   for (; b < whi; ++b) {
+    IMASK_CHECK_RANGE(13, (long long)Y.hi + (kVal ? 1 : 0), (long long)n * pitch);
     const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
     const float2 v = __ldg(P + Y.hi), vt = __ldg(PT + Y.hi);
     const float2 vd = kVal ? fsub2(__ldg(P + Y.hi + 1), v) : __ldg(PM + Y.hi);
@@ -656,10 +688,22 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
         const long long X = X0 + (long long)bs * A.step;
         Fix32 Y = fix_from(X + ((long long)((bs - b0) * kFWc - cmin_tab[i] + s * NI * kBox) << 32));
         int b = bs;
+#if IMASK_BOUNDS_CHECK
+        // element index relative to the first image of this stage: band row
+        // (b - b0), column within [0, kFWc - partners)
+        auto chk = [&](const Fix32& y, int band) {
+          const long long rel = (long long)y.hi - (long long)s * NI * kBox;
+          IMASK_CHECK_RANGE(20, rel - (long long)(band - b0) * kFWc,
+                            kFWc - (kVal ? 1 : 0) - (kK == 2 ? 1 : 0));
+        };
+#else
+        auto chk = [](const Fix32&, int) {};
+#endif
         if constexpr (kK == 2) {
           // three value pairs per plane feed both rays; the second ray's pair
           // (value, difference) is the first's or the next one's (carry)
           for (; b < be; ++b) {
+            chk(Y, b);
             float2 v3[3], t3[3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
@@ -691,6 +735,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
           float g[4];
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
+            chk(Y, b + k);
             v[k] = win[Y.hi];
             if (kVal) {
               vd[k] = win[Y.hi + 1];  // value pair of column c + 1 (difference below)
@@ -723,6 +768,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
           }
         }
         for (; kK == 1 && b < be; ++b) {
+          chk(Y, b);
           const float g = __saturatef(fmaf(onep_from_frac(Y.lo), S, B));
           const float2 v = win[Y.hi];
           const float2 vd = kVal ? fsub2(win[Y.hi + 1], v) : win[Y.hi + kBox];
@@ -1106,6 +1152,7 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
         const Fix32 eds = fix_from(s.Ds);        // the lower pixel: one row down
 #pragma unroll
         for (int k2 = 0; k2 < kPPT / 2; ++k2) {
+          IMASK_CHECK_RANGE(32, (long long)e.hi - (long long)t * W, W - 2);
           const float2 v0 = win2[e.hi], v1 = win2[e.hi + 1], v2 = win2[e.hi + 2];
           Fix32 eb = e;
           fix_add(eb, eds);
@@ -1136,6 +1183,7 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
         const Fix32 estep = fix_from(s.estep);
 #pragma unroll
         for (int k = 0; k < kPPT; ++k) {
+          IMASK_CHECK_RANGE(30, (long long)e.hi - (long long)t * W, W);
           const WinT pr = win[e.hi];
           const float onep = onep32(e.lo);
           const float w0 = __saturatef(fmaf(fabsf(s.c0 - onep), s.kneg, s.Rk));
@@ -1162,6 +1210,7 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
 #pragma unroll
         for (int k = 0; k < kPPT; ++k) {
           base[k] = (int)e.hi;
+          IMASK_CHECK_RANGE(31, (long long)e.hi - (long long)t * W, W - s.nb + 1);
           u[k] = s.c0 - onep32(e.lo);
           fix_add(e, (T == 16 && (k & 1)) ? estep2 : estep);
         }
@@ -1571,6 +1620,23 @@ cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n,
 }  // namespace imask
 
 namespace imask {
+// out4 = {violations, first site code, first index, first limit}; returns
+// whether the checks are compiled in (projector.cu IMASK_BOUNDS_CHECK)
+bool debug_bounds_read(unsigned long long* out4, bool reset) {
+#if IMASK_BOUNDS_CHECK
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out4, g_bounds, sizeof(unsigned long long) * 4);
+  if (reset) {
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_bounds, z, sizeof(z));
+  }
+  return true;
+#else
+  (void)reset;
+  out4[0] = out4[1] = out4[2] = out4[3] = 0;
+  return false;
+#endif
+}
 int forward_tma_entries_per_cta() { return kFE; }
 int forward_tma_window() { return kFWc; }
 }  // namespace imask

@@ -32,6 +32,32 @@ def pytest_collection_modifyitems(config, items):
             item.add_marker(skip)
 
 
+def pytest_sessionfinish(session, exitstatus):
+    """With a library built with -DIMASK_BOUNDS_CHECK=1 (tools/gpu_bounds_check.sh)
+    the kernels count every window / pair-image read outside its range: report
+    the count after the GPU tests and fail the session if it is not zero."""
+    try:
+        import ctypes
+
+        import torch
+
+        if not torch.cuda.is_available():
+            return
+        from paper_2412_10249_b200 import _lib
+
+        if _lib._lib is None:
+            return
+        out = (ctypes.c_ulonglong * 4)()
+        if _lib.lib().imask_debug_bounds(out, 0) != 1:
+            return
+        print(f"\n[bounds check] violations {out[0]} (first: site {out[1]}, index "
+              f"{ctypes.c_longlong(out[2]).value}, limit {out[3]})")
+        if out[0]:
+            session.exitstatus = 1
+    except Exception as exc:  # pragma: no cover
+        print(f"\n[bounds check] not read: {exc}")
+
+
 def golden(name):
     return np.load(os.path.join(GOLDEN, name), allow_pickle=False)
 
