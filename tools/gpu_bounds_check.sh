@@ -1,5 +1,5 @@
 # The GPU test suite on the index-checked build (tools/variants/lib_bounds.so,
-# built with -DIMASK_BOUNDS_CHECK=1): compute-sanitizer is closed on the pool, so
+# built here first with `make -C paper_2412_10249_b200/csrc bounds`: -DIMASK_BOUNDS_CHECK=1): compute-sanitizer is closed on the pool, so
 # the kernels' own range checks on every window / pair-image read stand in for
 # memcheck. The session ends with "[bounds check] violations N".
 mkdir -p gpurun_out
