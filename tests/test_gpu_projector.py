@@ -169,6 +169,27 @@ def test_full_size_properties(key):
         assert rel_l2(via_coarse, via_full) <= TOL, f
 
 
+def test_projections_repeat_bit_for_bit():
+    """Every launch of a projector gives the same bits (config D, every kernel
+    family: TMA one- and two-detector forwards, the L1 quad forward, pair /
+    unrolled / bin-loop adjoints with their split planes): a shared-memory or
+    barrier race would show as run-to-run differences, which compute-sanitizer
+    (closed on the pool) cannot be asked about."""
+    cfg = CONFIGS["D"]
+    geom = ctmodel.Geometry(cfg.side, cfg.n_angles, cfg.n_det)
+    plan = ctmodel.get_plan(geom)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    y = torch.randn(geom.m, device="cuda", generator=gen)
+    for f in (1, 2, 4, 8, 32):
+        u = torch.rand((cfg.side // f) ** 2, device="cuda", generator=gen)
+        s0, b0 = plan.project(u, f).clone(), plan.backproject(y, f).clone()
+        for _ in range(5):
+            # other work in between changes the CTA schedule from launch to launch
+            plan.backproject(y, 2 * f if f < 32 else 1)
+            assert torch.equal(plan.project(u, f), s0), f
+            assert torch.equal(plan.backproject(y, f), b0), f
+
+
 def test_empty_and_degenerate_inputs():
     geom = ctmodel.Geometry(16, 20, 23)
     K = ctmodel.projector_op(geom)
