@@ -13,6 +13,7 @@
 //                primal ridge prox (proxlib.py:51-55), one pass over HBM.
 //   resum      : _resum (solvers.py:184-191).
 #include "imask_common.cuh"
+#include "metric.cuh"
 #include "sketch.cuh"
 
 namespace imask {
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(256)
 k_compensate(const float* __restrict__ x, float* __restrict__ out, int side, CompParams cp) {
   __shared__ float tile[TT * TT];
   __shared__ float pyr[TT * TT / 3 + 8];
-  const int ts = min(TT, side);
+  const int ts = side / (int)gridDim.x;  // the launcher's tile (cover_tile): divides side, <= TT
   const int x0 = blockIdx.x * ts, y0 = blockIdx.y * ts;
   for (int e = threadIdx.x; e < ts * ts; e += blockDim.x)
     tile[e] = __ldg(x + (size_t)(y0 + e / ts) * side + x0 + e % ts);
@@ -230,6 +231,19 @@ __device__ __forceinline__ float saga_px(float pn, float& tab, float& sum, float
   return d;
 }
 
+// Fused metric row of the 32 x 32-tile kernels (256 threads, four pixels each):
+// ||x' - ref||^2 of this thread's pixels in float64, then the block / grid tail.
+__device__ __forceinline__ void image_metric_row(const ImageSaga& sg, size_t g, const float4 xn) {
+  const float4 r = __ldg(reinterpret_cast<const float4*>(sg.mref + g));
+  double s = 0.0, d;
+  d = (double)xn.x - (double)r.x; s = fma(d, d, s);
+  d = (double)xn.y - (double)r.y; s = fma(d, d, s);
+  d = (double)xn.z - (double)r.z; s = fma(d, d, s);
+  d = (double)xn.w - (double)r.w; s = fma(d, d, s);
+  metric_row_tail<256>(s, sg.mpart, sg.mrows, blockIdx.y * gridDim.x + blockIdx.x,
+                       gridDim.x * gridDim.y);
+}
+
 // Full level, fast path: phi_new = S_r(bp) by the 32x32 tile pyramid, then the
 // SAGA image update, all with 128-bit accesses.
 __global__ void __launch_bounds__(256, 6)  // 40 registers: 888 of the 1024 CTAs of a 1024^2 image resident
@@ -259,6 +273,7 @@ k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, Image
   *reinterpret_cast<float4*>(sg.phi_sum + g) = sum;
   *reinterpret_cast<float4*>(sg.x + g) = xv;
   extrapolate4(sg, g, xo, xv);
+  if (sg.mref) image_metric_row(sg, g, xv);
 }
 
 // Coarse level, fast path (side % 32 == 0, f <= 32): 32 x 32 full-resolution
@@ -328,6 +343,7 @@ k_saga_image_coarse32(const float* __restrict__ bp, int side, int lg, float inv_
     const int q = ((y0 >> lg) + (threadIdx.x >> lt)) * n + (x0 >> lg) + (threadIdx.x & (tc - 1));
     sg.phi_tab[q] = (sg.n_planes > 0 ? cv[threadIdx.x] : __ldg(bp + q)) * inv_f2;
   }
+  if (sg.mref) image_metric_row(sg, g, xv);
 }
 
 // ---- projector staging ------------------------------------------------------
@@ -532,7 +548,7 @@ __global__ void __launch_bounds__(256)
 k_saga_image_full(const float* __restrict__ bp, int side, CompParams cp, ImageSaga sg) {
   __shared__ float tile[TT * TT];
   __shared__ float pyr[TT * TT / 3 + 8];
-  const int ts = min(TT, side);
+  const int ts = side / (int)gridDim.x;  // the launcher's tile (cover_tile): divides side, <= TT
   const int x0 = blockIdx.x * ts, y0 = blockIdx.y * ts;
   for (int e = threadIdx.x; e < ts * ts; e += blockDim.x)
     tile[e] = __ldg(bp + (size_t)(y0 + e / ts) * side + x0 + e % ts);
@@ -688,6 +704,18 @@ cudaError_t launch_prolong(const float* u, float* x, int side, int f, float alph
 
 static inline int comp_tile(int r) { return (r <= 6) ? 32 : 64; }
 
+// Tile side of the generic (any-size) kernels: the largest multiple of `align`
+// (the block side the tile must hold whole: 2^(r-1) for the compensation
+// pyramid, f for the coarse image update) that is <= cap and divides `side`,
+// so the grid side / ts covers the image exactly. (side / 32 tiles of 32 left
+// the last side % 32 rows and columns of a 48^2 image untouched.)
+static inline int cover_tile(int side, int align, int cap) {
+  int best = align;
+  for (int ts = align; ts <= cap && ts <= side; ts += align)
+    if (side % ts == 0) best = ts;
+  return best;
+}
+
 cudaError_t launch_compensate(const float* x, float* out, int side, const CompParams& cp,
                               cudaStream_t s) {
   if (side % 32 == 0 && cp.r <= 6) {
@@ -695,13 +723,20 @@ cudaError_t launch_compensate(const float* x, float* out, int side, const CompPa
     return cudaGetLastError();
   }
   const int TT = comp_tile(cp.r);
-  const int ts = side < TT ? side : TT;
+  const int ts = cover_tile(side, 1 << (cp.r - 1), TT);
   dim3 grid(side / ts, side / ts);
   if (TT == 32)
     k_compensate<32><<<grid, 256, 0, s>>>(x, out, side, cp);
   else
     k_compensate<64><<<grid, 256, 0, s>>>(x, out, side, cp);
   return cudaGetLastError();
+}
+
+// Whether the image-side launch at this level runs a 32 x 32-tile kernel (the
+// ones that can fold a metric row in).
+bool image_fast_path(int side, int f, int r, bool full_level) {
+  if (side % 32 != 0) return false;
+  return full_level ? r <= 6 : (f <= 32 && 32 % f == 0);
 }
 
 bool stage32_ok(int side, int f, int r) { return side % 32 == 0 && f <= 32 && r <= 6; }
@@ -731,8 +766,7 @@ cudaError_t launch_saga_image_coarse(const float* bp, int side, int f, const Ima
                1.0f / (float)(f * f), sg);
     return cudaGetLastError();
   }
-  int ts = f > 32 ? f : 32;
-  if (ts > side) ts = side;
+  const int ts = cover_tile(side, f, f > 32 ? f : 32);
   dim3 grid(side / ts, side / ts);
   k_saga_image_coarse<<<grid, 256, 0, s>>>(bp, side, f, ts, 1.0f / (float)(f * f), sg);
   return cudaGetLastError();
@@ -745,7 +779,7 @@ cudaError_t launch_saga_image_full(const float* bp, int side, const CompParams& 
     return cudaGetLastError();
   }
   const int TT = comp_tile(cp.r);
-  const int ts = side < TT ? side : TT;
+  const int ts = cover_tile(side, 1 << (cp.r - 1), TT);
   dim3 grid(side / ts, side / ts);
   if (TT == 32)
     k_saga_image_full<32><<<grid, 256, 0, s>>>(bp, side, cp, sg);

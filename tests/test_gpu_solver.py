@@ -518,3 +518,79 @@ def test_fused_staging_bit_identical(args, monkeypatch):
         ctmodel._plan_cache.clear()
     assert np.array_equal(outs["fused"][0], outs["two_kernels"][0])
     assert np.array_equal(outs["fused"][1], outs["two_kernels"][1])
+
+
+@pytest.mark.parametrize("side,na,nd,r,record_every", [(64, 90, 91, 3, 1), (64, 90, 91, 3, 4),
+                                                       (48, 60, 69, 2, 1)])
+def test_rows_written_by_the_steps_match_separate_reductions(side, na, nd, r, record_every):
+    """run() lets the fused steps write their metric rows (the image-side kernel
+    reduces ||x' - x_ref||^2 where the level runs its 32 x 32-tile kernels, one
+    reduction launch after the update elsewhere: side 48). The rows equal the
+    ones a separate imask_metric_row launch per record gives (same float64
+    block-order sums up to the block shape: <= 1e-13 relative), and x is
+    bit-identical."""
+    geom = ctmodel.Geometry(side, na, nd)
+    probs = [1.0 / r] * r
+    rng = np.random.default_rng(11)
+    b = rng.random(geom.m)
+    x_ref = rng.random(side * side).astype(np.float32)
+    fam = mrsketch.make_family(r, side, probs, mode="coarse")
+    K = ctmodel.projector_op(geom)
+    pr = solvers.make_problem(K, b, fam, proxlib.ridge_fn(1e-2), proxlib.quadratic_conjugate_fn(b),
+                              coarse_projector=lambda f: ctmodel.coarse_projector(geom, f))
+    iters = 23
+    rep = solvers.run(pr, "sketch", 2e-4, 1e-2, iters, record_every=record_every, seed=5,
+                      x_ref=x_ref)
+    # the same solve with every row from the stand-alone reduction
+    st = solvers.init_state(pr, seed=5)
+    rec = solvers._Recorder(torch.from_numpy(x_ref).cuda(), st.x.device, iters + 2, 0.0)
+    rec.record(0, 0.0, 0, st.x)
+    for k in range(1, iters + 1):
+        solvers.sketch_step(st, pr, 2e-4, 1e-2)
+        if k % record_every == 0 or k == iters:
+            rec.record(k, st.cost, st.last_level, st.x)
+    ref_rows = rec.rows()
+    assert torch.equal(rep.x, st.x)
+    assert len(rep.rows) == len(ref_rows)
+    for a, c in zip(rep.rows, ref_rows):
+        assert a[:3] == c[:3]
+        assert abs(a[3] - c[3]) <= 1e-13 * abs(c[3])
+        assert abs(a[4] - c[4]) <= 1e-9
+    # seconds: non-decreasing device times
+    secs = [row[5] for row in rep.rows]
+    assert all(t1 >= t0 for t0, t1 in zip(secs, secs[1:]))
+
+
+@pytest.mark.parametrize("side,na,nd,r", [(48, 60, 69, 2), (40, 60, 59, 3), (96, 120, 137, 4)])
+def test_sides_not_a_multiple_of_32_match_oracle(side, na, nd, r):
+    """Image sides the 32 x 32-tile kernels do not take run the any-size sketch
+    and image-side kernels, whose tiles must still cover the whole image (a
+    48^2 image once kept a 32^2 corner only): compensation and 30 iterations
+    against the float64 oracle, and a second solve bit-identical to the first."""
+    probs = [1.0 / r] * r
+    geom = ctmodel.Geometry(side, na, nd)
+    rng = np.random.default_rng(3)
+    x0 = rng.random(side * side)
+    fam = mrsketch.make_family(r, side, probs, mode="coarse")
+    ops = so.SketchedCT(side, na, nd, probs)
+    got = fam.apply_sketch(torch.from_numpy(x0.astype(np.float32)).cuda(), r).double().cpu().numpy()
+    from oracle import sketch_oracle
+    want = sketch_oracle.apply_sketch(x0.reshape(side, side), probs, r).ravel()
+    assert rel_l2(got, want) <= 1e-5
+    b = ops.proj[1].apply(x0) + 0.01 * rng.standard_normal(geom.m)
+    K = ctmodel.projector_op(geom)
+    pr = solvers.make_problem(K, b, fam, proxlib.ridge_fn(1e-2), proxlib.quadratic_conjugate_fn(b),
+                              coarse_projector=lambda f: ctmodel.coarse_projector(geom, f))
+    runs = []
+    for _ in range(2):
+        st = solvers.init_state(pr, seed=9)
+        for _ in range(30):
+            solvers.sketch_step(st, pr, 2e-4, 1e-2)
+        runs.append((st.x.clone(), st.y.clone()))
+    assert torch.equal(runs[0][0], runs[1][0]) and torch.equal(runs[0][1], runs[1][1])
+    ost = so.init_state(ops, seed=9)
+    for _ in range(30):
+        so.sketch_step(ost, ops, b, 2e-4, 1e-2, 1e-2)
+    assert rel_l2(runs[0][0].double().cpu().numpy(), ost.x) <= 1e-3
+    assert rel_l2(runs[0][1].double().cpu().numpy(), ost.y) <= 1e-3
+
