@@ -91,17 +91,6 @@ typedef struct imask_step_params {
   double tv_tol;
   double tv_mu;
   void* tv_scratch;
-  /* Metric row of the iteration (run()'s record row, solvers.py:382-390,
-   * 470-478): with metric_ref != NULL the image-side update also writes
-   * ||x^{k+1} - metric_ref||^2 (float64, fixed-order reduction) and the device
-   * timer into the next slot of metric_rows, the row buffer of
-   * imask_metric_row -- folded into the image-side kernel where the level
-   * runs its 32 x 32-tile kernels, otherwise one reduction launch after it.
-   * metric_scratch: imask_metric_scratch_len(side) doubles, zero-initialised
-   * once. All three NULL: no row. */
-  const float* metric_ref;
-  double* metric_scratch;
-  double* metric_rows;
 } imask_step_params;
 
 /* Library version string. */
@@ -292,8 +281,6 @@ IMASK_API int imask_sq_dist(const float* x, const float* ref, int64_t n, double*
  * when it was final; the counter then advances. `rows` is device memory of
  * 2 + 2 * capacity doubles with rows[0] = 0 initially; `scratch` as for
  * imask_sq_dist. A run's rows are read back once at the end. */
-/* Doubles of device scratch a step with a metric row needs (>= IMASK_SQDIST_SCRATCH). */
-IMASK_API long long imask_metric_scratch_len(int side);
 IMASK_API int imask_metric_row(const float* x, const float* ref, int64_t n, double* scratch,
                                double* rows, void* stream);
 

@@ -54,10 +54,7 @@ class ImaskPdhgParams(ctypes.Structure):
 class ImaskStepParams(ctypes.Structure):
     _fields_ = [("sigma", ctypes.c_double), ("mu", ctypes.c_double), ("mu_g", ctypes.c_double),
                 ("g_kind", ctypes.c_int), ("tv_iters", ctypes.c_int), ("tv_tol", ctypes.c_double),
-                ("tv_mu", ctypes.c_double), ("tv_scratch", ctypes.c_void_p),
-                # metric row folded into the step (imask_b200.h): all NULL = no row
-                ("metric_ref", ctypes.c_void_p), ("metric_scratch", ctypes.c_void_p),
-                ("metric_rows", ctypes.c_void_p)]
+                ("tv_mu", ctypes.c_double), ("tv_scratch", ctypes.c_void_p)]
 
 
 # name -> (restype, argtypes)
@@ -77,7 +74,6 @@ SIGNATURES = {
     "imask_metric_row": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, _vp, _vp]),
     "imask_reload_switches": (ctypes.c_int, []),
     "imask_debug_bounds": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]),
-    "imask_metric_scratch_len": (ctypes.c_longlong, [ctypes.c_int]),
     "imask_plan_create": (
         ctypes.c_int,
         [

@@ -42,7 +42,6 @@ cudaError_t launch_compensate(const float* x, float* out, int side, const CompPa
 cudaError_t launch_prepare(const float* u, int n, float2* P, float2* PT, float2* PM,
                            float2* PTM, bool diff, cudaStream_t s);
 bool stage32_ok(int side, int f, int r);
-bool image_fast_path(int side, int f, int r, bool full_level);
 cudaError_t launch_stage32(const float* x, int side, int f, const CompParams& cp, float2* P,
                            float2* PT, cudaStream_t s);
 bool forward_tma_val_grid(int n_det, int n_entries);
@@ -487,8 +486,6 @@ int check_params(const imask_step_params* prm) {
   if (prm->g_kind == 1 && (!(prm->tv_mu > 0.0) || prm->tv_iters < 0 || !prm->tv_scratch))
     return fail(IMASK_EINVAL, "TV step needs tv_mu > 0, tv_iters >= 0 and tv_scratch");
   if (prm->g_kind != 0 && prm->g_kind != 1) return fail(IMASK_EINVAL, "unknown g_kind");
-  if (prm->metric_ref && (!prm->metric_scratch || !prm->metric_rows))
-    return fail(IMASK_EINVAL, "a metric row needs metric_scratch and metric_rows");
   return IMASK_OK;
 }
 
@@ -806,12 +803,6 @@ int imask_plan_create_list(int side, int n_angles, int n_det, int n_loc, const i
   return IMASK_OK;
 }
 
-long long imask_metric_scratch_len(int side) {
-  // [stand-alone reduction: IMASK_SQDIST_SCRATCH][fused: 1 + blocks partials + counter]
-  const long long tiles = ((long long)(side + 31) / 32) * ((side + 31) / 32);
-  return IMASK_SQDIST_SCRATCH + tiles + 2;
-}
-
 int imask_debug_bounds(unsigned long long* out4, int reset) {
   if (!out4) return fail(IMASK_EINVAL, "out4 is null");
   return debug_bounds_read(out4, reset != 0) ? 1 : 0;
@@ -1118,16 +1109,6 @@ int step_image(imask_plan* pl, const imask_state* st, int level0, const imask_st
   sg.s = (float)s;
   sg.inv_den = tv ? 1.0f : (float)(1.0 / (1.0 + s * prm->mu_g));  // TV: x - s xi, prox below
   if (tv && xbar) return fail(IMASK_EINVAL, "the sequential variant takes the ridge g only");
-  // metric row: folded into the 32 x 32-tile kernels (x' is final there: no TV
-  // prox after them), else one reduction launch after the update
-  const bool row = prm->metric_ref != nullptr;
-  const bool row_fused = row && !tv && image_fast_path(pl->side, f, pl->r, level0 == pl->r - 1);
-  if (row_fused) {
-    sg.mref = prm->metric_ref;
-    // the stand-alone reduction owns the first IMASK_SQDIST_SCRATCH doubles
-    sg.mpart = prm->metric_scratch + IMASK_SQDIST_SCRATCH;
-    sg.mrows = prm->metric_rows;
-  }
   if (level0 < pl->r - 1)
     LAUNCH(launch_saga_image_coarse(st->bp, pl->side, f, sg, S(stream)), "saga_image");
   else
@@ -1138,12 +1119,6 @@ int step_image(imask_plan* pl, const imask_state* st, int level0, const imask_st
                                          prm->tv_tol, prm->tv_scratch, stream);
     if (trc) return fail(trc, std::string("prox_tv_nonneg: ") + cudaGetErrorString(cudaGetLastError()));
     g_launches += prm->tv_iters + 1;  // iteration kernels + the recovery (plus one memset)
-  }
-  if (row && !row_fused) {
-    if ((rc = imask_metric_row(st->x, prm->metric_ref, (int64_t)pl->side * pl->side,
-                               prm->metric_scratch, prm->metric_rows, stream)))
-      return fail(rc, "metric row");
-    ++g_launches;
   }
   return IMASK_OK;
 }

@@ -229,14 +229,6 @@ struct ImageSaga {
   const float* planes = nullptr;
   int n_planes = 0;
   long long plane_len = 0;
-  // mref != nullptr: the kernel also reduces ||x' - mref||^2 (float64, fixed
-  // order: block partials mpart[1 + block], summed in block order by the last
-  // block to finish, counter at mpart[1 + blocks]) into the next slot of the
-  // metric row buffer mrows together with the device timer (run()'s record
-  // row, solvers.py:382-390) -- no separate launch per recorded iteration
-  const float* mref = nullptr;
-  double* mpart = nullptr;
-  double* mrows = nullptr;
 };
 
 // Primal extrapolation of sketch_seq_step (solvers.py:296-300) for one pixel /

@@ -6,16 +6,31 @@
 #include <cuda_runtime.h>
 
 #include "imask_b200.h"
-#include "metric.cuh"
 
 namespace {
 
 constexpr int kBlocks = IMASK_SQDIST_SCRATCH - 2;
 constexpr int kThreads = 256;
 
-__device__ __forceinline__ double block_sum(double v) { return imask::metric_block_sum<kThreads>(v); }
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double red[kThreads / 32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < kThreads / 32 ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  }
+  return v;
+}
 
-__device__ __forceinline__ unsigned long long globaltimer_ns() { return imask::metric_timer_ns(); }
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // rows == nullptr: *result = ||x - ref||^2. Otherwise a metric row: at slot
 // k = rows[0] (a 64-bit counter) rows[2 + 2k] = ||x - ref||^2 and

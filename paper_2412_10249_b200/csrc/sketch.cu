@@ -13,7 +13,6 @@
 //                primal ridge prox (proxlib.py:51-55), one pass over HBM.
 //   resum      : _resum (solvers.py:184-191).
 #include "imask_common.cuh"
-#include "metric.cuh"
 #include "sketch.cuh"
 
 namespace imask {
@@ -231,19 +230,6 @@ __device__ __forceinline__ float saga_px(float pn, float& tab, float& sum, float
   return d;
 }
 
-// Fused metric row of the 32 x 32-tile kernels (256 threads, four pixels each):
-// ||x' - ref||^2 of this thread's pixels in float64, then the block / grid tail.
-__device__ __forceinline__ void image_metric_row(const ImageSaga& sg, size_t g, const float4 xn) {
-  const float4 r = __ldg(reinterpret_cast<const float4*>(sg.mref + g));
-  double s = 0.0, d;
-  d = (double)xn.x - (double)r.x; s = fma(d, d, s);
-  d = (double)xn.y - (double)r.y; s = fma(d, d, s);
-  d = (double)xn.z - (double)r.z; s = fma(d, d, s);
-  d = (double)xn.w - (double)r.w; s = fma(d, d, s);
-  metric_row_tail<256>(s, sg.mpart, sg.mrows, blockIdx.y * gridDim.x + blockIdx.x,
-                       gridDim.x * gridDim.y);
-}
-
 // Full level, fast path: phi_new = S_r(bp) by the 32x32 tile pyramid, then the
 // SAGA image update, all with 128-bit accesses.
 __global__ void __launch_bounds__(256, 6)  // 40 registers: 888 of the 1024 CTAs of a 1024^2 image resident
@@ -273,7 +259,6 @@ k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, Image
   *reinterpret_cast<float4*>(sg.phi_sum + g) = sum;
   *reinterpret_cast<float4*>(sg.x + g) = xv;
   extrapolate4(sg, g, xo, xv);
-  if (sg.mref) image_metric_row(sg, g, xv);
 }
 
 // Coarse level, fast path (side % 32 == 0, f <= 32): 32 x 32 full-resolution
@@ -343,7 +328,6 @@ k_saga_image_coarse32(const float* __restrict__ bp, int side, int lg, float inv_
     const int q = ((y0 >> lg) + (threadIdx.x >> lt)) * n + (x0 >> lg) + (threadIdx.x & (tc - 1));
     sg.phi_tab[q] = (sg.n_planes > 0 ? cv[threadIdx.x] : __ldg(bp + q)) * inv_f2;
   }
-  if (sg.mref) image_metric_row(sg, g, xv);
 }
 
 // ---- projector staging ------------------------------------------------------
@@ -730,13 +714,6 @@ cudaError_t launch_compensate(const float* x, float* out, int side, const CompPa
   else
     k_compensate<64><<<grid, 256, 0, s>>>(x, out, side, cp);
   return cudaGetLastError();
-}
-
-// Whether the image-side launch at this level runs a 32 x 32-tile kernel (the
-// ones that can fold a metric row in).
-bool image_fast_path(int side, int f, int r, bool full_level) {
-  if (side % 32 != 0) return false;
-  return full_level ? r <= 6 : (f <= 32 && 32 % f == 0);
 }
 
 bool stage32_ok(int side, int f, int r) { return side % 32 == 0 && f <= 32 && r <= 6; }

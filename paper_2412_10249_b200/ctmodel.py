@@ -299,7 +299,6 @@ class Plan:
         self.handle = handle
         self.graph_cache: dict = {}  # step graphs of solvers.Engine (destroyed with the plan)
         self.state_pool: list = []  # free solver-state buffers of run() (solvers.run)
-        self.rec_pool: dict = {}  # run()'s metric-row buffers (stable addresses for the step graphs)
         self.phi_offsets = []
         off = 0
         for f in self.factors:

@@ -739,33 +739,14 @@ class _Recorder:
     """
 
     def __init__(self, x_ref: Optional[torch.Tensor], device: torch.device, capacity: int,
-                 t0: float, pool: Optional[dict] = None, side: int = 0):
+                 t0: float):
         self.ref = None if x_ref is None else x_ref.float().contiguous().reshape(-1)
         x_ref = self.ref
         self.device = device
-        # ||x_ref||^2 stays on the device until rows() (no host synchronisation here:
-        # the host goes on enqueuing the steps while x_ref is still being copied in)
-        self._ref_sq_dev = (torch.dot(x_ref.double(), x_ref.double())
-                            if x_ref is not None else None)
-        need_rows = 2 + 2 * max(capacity, 1)
-        self.fused = pool is not None and x_ref is not None and side > 0
-        if self.fused:
-            # rows folded into the steps (imask_step_params.metric_*): the steps'
-            # graphs bake the three addresses in, so the buffers live with the plan
-            n_scr = int(_lib.lib().imask_metric_scratch_len(side))
-            if (pool.get("ref") is None or pool["ref"].numel() != x_ref.numel()
-                    or pool["rows"].numel() < need_rows or pool["scratch"].numel() != n_scr):
-                pool["ref"] = torch.empty_like(x_ref)
-                pool["scratch"] = torch.empty(n_scr, dtype=torch.float64, device=device)
-                pool["rows"] = torch.empty(max(need_rows, 8192), dtype=torch.float64, device=device)
-            pool["ref"].copy_(x_ref)
-            pool["scratch"].zero_()
-            pool["rows"][:2].zero_()
-            self.ref, self.scratch, self.dev_rows = pool["ref"], pool["scratch"], pool["rows"]
-        else:
-            self.scratch = torch.zeros(_lib.IMASK_SQDIST_SCRATCH, dtype=torch.float64, device=device)
-            self.dev_rows = torch.zeros(need_rows, dtype=torch.float64, device=device)
-        x_ref = self.ref
+        self.ref_sq = (float(torch.dot(x_ref.double(), x_ref.double()))
+                       if x_ref is not None else float("nan"))
+        self.scratch = torch.zeros(_lib.IMASK_SQDIST_SCRATCH, dtype=torch.float64, device=device)
+        self.dev_rows = torch.zeros(2 + 2 * max(capacity, 1), dtype=torch.float64, device=device)
         self.meta: list = []
         self.t0 = t0
         self.t_first: Optional[float] = None
@@ -774,37 +755,21 @@ class _Recorder:
         self._rows_ptr = ctypes.c_void_p(self.dev_rows.data_ptr())
         self._stream = ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
-    def with_row(self, prm: _lib.ImaskStepParams) -> _lib.ImaskStepParams:
-        """A copy of ``prm`` whose step also writes the next metric row."""
-        out = _lib.ImaskStepParams.from_buffer_copy(prm)
-        out.metric_ref = self.ref.data_ptr()
-        out.metric_scratch = self.scratch.data_ptr()
-        out.metric_rows = self.dev_rows.data_ptr()
-        return out
-
-    def record(self, k: int, cost: float, level: int, x: torch.Tensor,
-               in_step: bool = False) -> None:
-        """Row k; ``in_step``: the step just enqueued wrote it (with_row)."""
+    def record(self, k: int, cost: float, level: int, x: torch.Tensor) -> None:
         if self.t_first is None:
             self.t_first = time.perf_counter() - self.t0
         if self.ref is not None and (x.numel() != self.ref.numel() or x.dtype != torch.float32):
             raise ValueError("x_ref must match the iterate's shape")
         if len(self.meta) >= (self.dev_rows.numel() - 2) // 2:
             raise RuntimeError("metric row buffer full")
-        if not in_step:
-            _lib.check(_lib.lib().imask_metric_row(
-                ctypes.c_void_p(x.data_ptr()), self._ref_ptr,
-                0 if self.ref is None else x.numel(), self._scratch_ptr, self._rows_ptr,
-                self._stream))
+        _lib.check(_lib.lib().imask_metric_row(
+            ctypes.c_void_p(x.data_ptr()), self._ref_ptr,
+            0 if self.ref is None else x.numel(), self._scratch_ptr, self._rows_ptr,
+            self._stream))
         self.meta.append((k, cost, level, x.numel()))
-
-    @property
-    def ref_sq(self) -> float:
-        return float("nan") if self._ref_sq_dev is None else float(self._ref_sq_dev)
 
     def rows(self) -> list:
         host = self.dev_rows[:2 + 2 * len(self.meta)].cpu().numpy()
-        ref_sq = self.ref_sq
         out = []
         ts0 = host[3] if self.meta else 0.0
         for idx, (k, cost, level, d) in enumerate(self.meta):
@@ -812,7 +777,7 @@ class _Recorder:
                 rel = snr = float("nan")
             else:
                 err = float(host[2 + 2 * idx])
-                rel = err / ref_sq if ref_sq > 0 else float("nan")
+                rel = err / self.ref_sq if self.ref_sq > 0 else float("nan")
                 snr = 300.0 if err == 0.0 else min(300.0, 10.0 * math.log10(d / err))
             secs = self.t_first + (float(host[3 + 2 * idx]) - ts0) * 1e-9
             out.append((k, cost, level, rel, snr, secs))
@@ -980,13 +945,8 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
     schedule = draw_levels(seed, 0, iters, prob.cum_probs)
 
     n_rows = 2 + iters // max(record_every, 1)
-    # rows of the fused engine are written by the steps themselves (the image-side
-    # kernel reduces ||x' - x_ref||^2): no launch per recorded iteration
-    rec = _Recorder(x_ref_t, dev, n_rows, t0,
-                    pool=eng.plan.rec_pool if fused else None,
-                    side=eng.geom.side if fused else 0)
+    rec = _Recorder(x_ref_t, dev, n_rows, t0)
     record = rec.record
-    prm_row = rec.with_row(prm) if rec.fused else None
 
     record(0, 0.0, 0, state.x)
     # single-GPU fused steps: the (level, dual parity) -> step graph map is
@@ -998,14 +958,11 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
     stream = eng.plan.stream if eng is not None else None
     for k in range(1, iters + 1):
         i = int(schedule[k - 1])
-        rows_now = k % record_every == 0 or k == iters
-        in_step = rows_now and prm_row is not None
-        p_k = prm_row if in_step else prm
         if fast:
-            h = graphs.get((i, state.parity, in_step))
+            h = graphs.get((i, state.parity))
             if h is None:
-                h = eng.graph(state, i, p_k)[0]
-                graphs[(i, state.parity, in_step)] = h
+                h = eng.graph(state, i, prm)[0]
+                graphs[(i, state.parity)] = h
             rc = launch(h, stream)
             if rc:
                 _lib.check(rc)
@@ -1024,15 +981,15 @@ def run(prob: Problem, algorithm: str, sigma: float, mu: float, iters: int,
         else:
             if seq:
                 _lib.check(_lib.lib().imask_seq_step(
-                    eng.plan.handle, ctypes.byref(state.c_state(eng.b)), i, ctypes.byref(p_k),
+                    eng.plan.handle, ctypes.byref(state.c_state(eng.b)), i, ctypes.byref(prm),
                     float(theta_extrap), eng.plan.stream))
             else:
-                _device_step(eng, state, i, p_k)
+                _device_step(eng, state, i, prm)
             _advance(state, prob, i)
         while budgets and state.cost >= budgets[0]:
             snapshots[budgets.pop(0)] = state.x.clone()
-        if rows_now:
-            record(k, state.cost, state.last_level, state.x, in_step=in_step and fused)
+        if k % record_every == 0 or k == iters:
+            record(k, state.cost, state.last_level, state.x)
     x_out, y_out = (state.x.clone(), state.y.clone()) if pooled is not None else (state.x, state.y)
     rows = rec.rows()  # (synchronises: every step has completed)
     if pooled is not None:

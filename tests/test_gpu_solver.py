@@ -522,13 +522,10 @@ def test_fused_staging_bit_identical(args, monkeypatch):
 
 @pytest.mark.parametrize("side,na,nd,r,record_every", [(64, 90, 91, 3, 1), (64, 90, 91, 3, 4),
                                                        (48, 60, 69, 2, 1)])
-def test_rows_written_by_the_steps_match_separate_reductions(side, na, nd, r, record_every):
-    """run() lets the fused steps write their metric rows (the image-side kernel
-    reduces ||x' - x_ref||^2 where the level runs its 32 x 32-tile kernels, one
-    reduction launch after the update elsewhere: side 48). The rows equal the
-    ones a separate imask_metric_row launch per record gives (same float64
-    block-order sums up to the block shape: <= 1e-13 relative), and x is
-    bit-identical."""
+def test_run_rows_match_an_explicit_step_loop(side, na, nd, r, record_every):
+    """run()'s metric rows (device-side reductions, one read-back per run) and
+    final iterate equal an explicit sketch_step loop recording the same
+    iterations, also on a side the 32 x 32-tile kernels do not take (48)."""
     geom = ctmodel.Geometry(side, na, nd)
     probs = [1.0 / r] * r
     rng = np.random.default_rng(11)
