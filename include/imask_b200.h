@@ -47,10 +47,12 @@ typedef struct imask_plan imask_plan;
 /* Solver state of one rank: every pointer is a device buffer.
  * Mirrors SaddleState (solvers.py:119-140) with compact coarse phi rows:
  *   x, phi_sum           : side*side
- *   phi_tab              : sum_i (side/f_i)^2, level i (1-based) at offset
- *                          sum_{i'<i} (side/f_i')^2 (rows hold U_f^T-scaled
+ *   phi_tab              : level i (1-based) holds (side/f_i)^2 values at
+ *                          offset o_i, o_1 = 0, o_{i+1} = o_i + (side/f_i)^2
+ *                          rounded up to a multiple of 4 (rows start 16-byte
+ *                          aligned); total o_{r+1}. Rows hold U_f^T-scaled
  *                          coarse values; the reference stores the same
- *                          values replicated to full resolution)
+ *                          values replicated to full resolution
  *   y, b, psi_sum        : n_loc*n_det (this rank's slab)
  *   psi_tab              : r * n_loc*n_det, level i at offset (i-1)*n_loc*n_det
  *   bp                   : side*side scratch for the (partial) backprojection

@@ -660,7 +660,9 @@ int imask_plan_create_list(int side, int n_angles, int n_det, int n_loc, const i
     pl->rp.p[i] = (float)probs[i];
     pl->rp.factor[i] = f;
     pl->rp.offset[i] = off;
-    off += n * n;
+    // rows start 16-byte aligned (the 128-bit image-side kernels read them as
+    // float4: 3^2 + 6^2 + ... of a 96^2 / r = 6 family is not a multiple of 4)
+    off = (off + n * n + 3) & ~3LL;
   }
   pl->cp.pr = (float)probs[r - 1];
 

@@ -303,7 +303,8 @@ class Plan:
         off = 0
         for f in self.factors:
             self.phi_offsets.append(off)
-            off += (geom.side // f) ** 2
+            # every row starts 16-byte aligned (imask_b200.h: imask_state.phi_tab)
+            off = (off + (geom.side // f) ** 2 + 3) & ~3
         self.phi_tab_len = off
 
     def __del__(self):

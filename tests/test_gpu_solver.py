@@ -558,13 +558,20 @@ def test_run_rows_match_an_explicit_step_loop(side, na, nd, r, record_every):
     assert all(t1 >= t0 for t0, t1 in zip(secs, secs[1:]))
 
 
-@pytest.mark.parametrize("side,na,nd,r", [(48, 60, 69, 2), (40, 60, 59, 3), (96, 120, 137, 4)])
-def test_sides_not_a_multiple_of_32_match_oracle(side, na, nd, r):
-    """Image sides the 32 x 32-tile kernels do not take run the any-size sketch
-    and image-side kernels, whose tiles must still cover the whole image (a
-    48^2 image once kept a 32^2 corner only): compensation and 30 iterations
-    against the float64 oracle, and a second solve bit-identical to the first."""
-    probs = [1.0 / r] * r
+@pytest.mark.parametrize("side,na,nd,r", [(48, 60, 69, 2), (40, 45, 57, 3), (96, 120, 137, 6),
+                                          (144, 100, 205, 5), (192, 180, 272, 7)])
+def test_unusual_geometries_match_oracle(side, na, nd, r):
+    """Geometries off the BASELINE grid (tools/geometry_sweep.py runs more): image
+    sides the 32 x 32-tile kernels do not take run the any-size sketch and
+    image-side kernels, whose tiles must still cover the whole image (a 48^2
+    image once kept a 32^2 corner only); 96^2 with r = 6 has phi table rows of
+    9, 36, ... values, which must still start 16-byte aligned for the 128-bit
+    kernels (a misaligned-address fault once); 144^2 pairs the TMA forward with
+    the any-size staging; r = 7 takes the 64-wide compensation tiles; 45 angles
+    are not quad-closed. Compensation and 30 iterations against the float64
+    oracle with non-uniform probabilities, and a second solve bit-identical."""
+    probs = np.random.default_rng(side).dirichlet(np.ones(r) * 4.0)
+    probs = [float(p) for p in probs / probs.sum()]
     geom = ctmodel.Geometry(side, na, nd)
     rng = np.random.default_rng(3)
     x0 = rng.random(side * side)
