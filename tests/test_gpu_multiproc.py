@@ -23,7 +23,7 @@ def _port():
         return sk.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,n_angles", [(2, 180), (4, 180), (2, 90)])
+@pytest.mark.parametrize("world,n_angles", [(2, 180), (4, 180), (2, 90), (2, 360)])  # 360 on 2 ranks: block-cyclic shards
 def test_sharded_solve_in_processes(world, n_angles):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
