@@ -58,7 +58,8 @@ cudaError_t launch_resum(const float* phi_tab, float* phi_sum, int side, const f
 void init_kernel_attributes();
 int forward_tma_entries_per_cta();
 int forward_tma_window();
-bool debug_bounds_read(unsigned long long* out4, bool reset);
+bool debug_bounds_read_projector(unsigned long long* out4, bool reset);
+bool debug_bounds_read_sketch(unsigned long long* out4, bool reset);
 int forward_tma_bands(bool quad, bool val);
 struct TmaMaps {
   CUtensorMap row, row_m, col, col_m;
@@ -807,7 +808,24 @@ int imask_plan_create_list(int side, int n_angles, int n_det, int n_loc, const i
 
 int imask_debug_bounds(unsigned long long* out4, int reset) {
   if (!out4) return fail(IMASK_EINVAL, "out4 is null");
-  return debug_bounds_read(out4, reset != 0) ? 1 : 0;
+  // projector.cu's counters, then sketch.cu's (the first failing site wins)
+  unsigned long long b[4] = {0, 0, 0, 0};
+  const bool on = debug_bounds_read_projector(out4, reset != 0);
+  debug_bounds_read_sketch(b, reset != 0);
+  if (out4[0] == ~0ull || b[0] == ~0ull) {
+    const unsigned long long* bad = out4[0] == ~0ull ? out4 : b;
+    return fail(IMASK_ECUDA, std::string("bounds counters unreadable (") +
+                                 (out4[0] == ~0ull ? "projector" : "sketch") + ", " +
+                                 (bad[2] == 1 ? "synchronize" : "memcpy") + ": " +
+                                 cudaGetErrorString((cudaError_t)bad[1]) + ")");
+  }
+  if (out4[0] == 0) {
+    out4[1] = b[1];
+    out4[2] = b[2];
+    out4[3] = b[3];
+  }
+  out4[0] += b[0];
+  return on ? 1 : 0;
 }
 
 int imask_reload_switches(void) {

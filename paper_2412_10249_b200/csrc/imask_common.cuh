@@ -42,6 +42,64 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 constexpr double kFix = 4294967296.0;  // 2^32
 
+// Debug build (-DIMASK_BOUNDS_CHECK=1): the kernels check their computed
+// indices against the range they must stay in -- every shared-memory window
+// read of the projectors and pair-image read of the L1 forwards, every plane
+// write of the staging kernels, every table / tile access of the any-size
+// sketch and image-side kernels -- and count violations in a per-file device
+// word the host reads with imask_debug_bounds. compute-sanitizer is closed on
+// the B200 pool, so this build, run through the GPU test suite
+// (tools/gpu_bounds_check.sh), stands in for memcheck on computed indices.
+#ifndef IMASK_BOUNDS_CHECK
+#define IMASK_BOUNDS_CHECK 0
+#endif
+#if IMASK_BOUNDS_CHECK
+static __device__ unsigned long long g_bounds[4];  // violations, first: site code, index, limit
+static __device__ __noinline__ void bounds_fail(int code, long long idx, long long limit) {
+  if (atomicAdd(&g_bounds[0], 1ull) == 0ull) {
+    g_bounds[1] = (unsigned long long)code;
+    g_bounds[2] = (unsigned long long)idx;
+    g_bounds[3] = (unsigned long long)limit;
+  }
+}
+#define IMASK_CHECK_RANGE(code, idx, limit)                                       \
+  do {                                                                            \
+    const long long i_ = (long long)(idx), l_ = (long long)(limit);               \
+    if (i_ < 0 || i_ >= l_) bounds_fail(code, i_, l_);                            \
+  } while (0)
+// out4 = this translation unit's {violations, first site code, index, limit}
+// (all ones when the device word cannot be read)
+static inline bool bounds_read(unsigned long long* out4, bool reset) {
+  out4[0] = out4[1] = out4[2] = out4[3] = ~0ull;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    out4[1] = (unsigned long long)e;
+    out4[2] = 1;
+    return true;
+  }
+  unsigned long long v[4];
+  e = cudaMemcpyFromSymbol(v, g_bounds, sizeof(v));
+  if (e != cudaSuccess) {
+    out4[1] = (unsigned long long)e;
+    out4[2] = 2;
+    return true;
+  }
+  for (int i = 0; i < 4; ++i) out4[i] = v[i];
+  if (reset) {
+    const unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_bounds, z, sizeof(z));
+  }
+  return true;
+}
+#else
+#define IMASK_CHECK_RANGE(code, idx, limit) ((void)0)
+static inline bool bounds_read(unsigned long long* out4, bool reset) {
+  (void)reset;
+  out4[0] = out4[1] = out4[2] = out4[3] = 0;
+  return false;
+}
+#endif
+
 // Path and tuning switches, read once from the environment (host code only).
 // Unset, the product defaults apply. They exist to select the alternative
 // code paths the bit-identity tests compare (IMASK_NO_QUAD, IMASK_NO_TMA,

@@ -27,34 +27,6 @@ namespace cg = cooperative_groups;
 
 namespace imask {
 
-// Debug build (-DIMASK_BOUNDS_CHECK=1): every shared-memory window read of the
-// projectors and every pair-image read of the L1 forwards is checked against
-// the range it must stay in (the staged window row of its band / angle; the
-// padded image row); violations are counted in a device word the host reads
-// with imask_debug_bounds. compute-sanitizer is closed on the B200 pool, so
-// this build, run through the GPU test suite (tools/gpu_bounds_check.sh),
-// stands in for memcheck on the kernels' computed indices.
-#ifndef IMASK_BOUNDS_CHECK
-#define IMASK_BOUNDS_CHECK 0
-#endif
-#if IMASK_BOUNDS_CHECK
-__device__ unsigned long long g_bounds[4];  // violations, first: site code, index, limit
-__device__ __noinline__ void bounds_fail(int code, long long idx, long long limit) {
-  if (atomicAdd(&g_bounds[0], 1ull) == 0ull) {
-    g_bounds[1] = (unsigned long long)code;
-    g_bounds[2] = (unsigned long long)idx;
-    g_bounds[3] = (unsigned long long)limit;
-  }
-}
-#define IMASK_CHECK_RANGE(code, idx, limit)                                       \
-  do {                                                                            \
-    const long long i_ = (long long)(idx), l_ = (long long)(limit);               \
-    if (i_ < 0 || i_ >= l_) bounds_fail(code, i_, l_);                            \
-  } while (0)
-#else
-#define IMASK_CHECK_RANGE(code, idx, limit) ((void)0)
-#endif
-
 // bands b in [lo, hi) where the ray's left chord partner floor(xi) is in [-1, n-1]
 __device__ __forceinline__ bool band_ok(long long X0, long long step, int b, int n) {
   const long long X = X0 + (long long)b * step;
@@ -1620,22 +1592,9 @@ cudaError_t launch_adjoint(const float* sino, float* out, float* partial, int n,
 }  // namespace imask
 
 namespace imask {
-// out4 = {violations, first site code, first index, first limit}; returns
-// whether the checks are compiled in (projector.cu IMASK_BOUNDS_CHECK)
-bool debug_bounds_read(unsigned long long* out4, bool reset) {
-#if IMASK_BOUNDS_CHECK
-  cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out4, g_bounds, sizeof(unsigned long long) * 4);
-  if (reset) {
-    const unsigned long long z[4] = {0, 0, 0, 0};
-    cudaMemcpyToSymbol(g_bounds, z, sizeof(z));
-  }
-  return true;
-#else
-  (void)reset;
-  out4[0] = out4[1] = out4[2] = out4[3] = 0;
-  return false;
-#endif
+// this file's index-check counters (imask_common.cuh: IMASK_BOUNDS_CHECK)
+bool debug_bounds_read_projector(unsigned long long* out4, bool reset) {
+  return bounds_read(out4, reset);
 }
 int forward_tma_entries_per_cta() { return kFE; }
 int forward_tma_window() { return kFWc; }

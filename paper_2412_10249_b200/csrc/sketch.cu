@@ -70,8 +70,12 @@ k_compensate(const float* __restrict__ x, float* __restrict__ out, int side, Com
   __shared__ float pyr[TT * TT / 3 + 8];
   const int ts = side / (int)gridDim.x;  // the launcher's tile (cover_tile): divides side, <= TT
   const int x0 = blockIdx.x * ts, y0 = blockIdx.y * ts;
-  for (int e = threadIdx.x; e < ts * ts; e += blockDim.x)
+  IMASK_CHECK_RANGE(50, (long long)(gridDim.x * ts) - side, 1);  // the tiles cover the image exactly
+  IMASK_CHECK_RANGE(51, ts, TT + 1);
+  for (int e = threadIdx.x; e < ts * ts; e += blockDim.x) {
+    IMASK_CHECK_RANGE(52, (size_t)(y0 + e / ts) * side + x0 + e % ts, (long long)side * side);
     tile[e] = __ldg(x + (size_t)(y0 + e / ts) * side + x0 + e % ts);
+  }
   __syncthreads();
   build_pyramid(tile, pyr, ts, cp.r);
   for (int e = threadIdx.x; e < ts * ts; e += blockDim.x) {
@@ -241,6 +245,8 @@ k_saga_image_full32(const float* __restrict__ bp, int side, CompParams cp, Image
   // the table row, the sum and x were last written by the previous step, which
   // completed before this step's adjoint (a plain launch) started: they are
   // loaded before the programmatic wait, overlapping the adjoint's tail
+  IMASK_CHECK_RANGE(64, (long long)(((uintptr_t)(sg.phi_tab + g) | (uintptr_t)(sg.phi_sum + g) |
+                                      (uintptr_t)(sg.x + g)) & 15), 1);  // 128-bit accesses aligned
   float4 tab = *reinterpret_cast<const float4*>(sg.phi_tab + g);
   float4 sum = *reinterpret_cast<const float4*>(sg.phi_sum + g);
   float4 xv = *reinterpret_cast<const float4*>(sg.x + g);
@@ -278,6 +284,8 @@ k_saga_image_coarse32(const float* __restrict__ bp, int side, int lg, float inv_
   float4 sum = *reinterpret_cast<const float4*>(sg.phi_sum + g);
   float4 xv = *reinterpret_cast<const float4*>(sg.x + g);
   float po[4];
+  IMASK_CHECK_RANGE(65, (long long)(((uintptr_t)(sg.phi_sum + g) | (uintptr_t)(sg.x + g)) & 15), 1);
+  IMASK_CHECK_RANGE(66, qrow + ((col + 3) >> lg), (long long)n * n);
 #pragma unroll
   for (int k = 0; k < 4; ++k) po[k] = sg.phi_tab[qrow + ((col + k) >> lg)];
   griddep_wait();  // bp (or the split planes) come from the stream predecessor (the adjoint)
@@ -466,6 +474,8 @@ k_stage32(const float* __restrict__ x, int side, int lg, CompParams cp, float2* 
     const int rr = e / w, cc = e % w;  // consecutive threads along a row of u
     const int R = R0 + rr, C = C0 + cc;
     const float val = ut[rr][cc];
+    IMASK_CHECK_RANGE(60, R * pitch + C + 1 + kPadC, (long long)n * pitch);
+    IMASK_CHECK_RANGE(61, R * pitch + (n - 1 - C) + 1 + kPadC, (long long)n * pitch);
     Pf[2 * (R * pitch + C + 1 + kPadC)] = val;
     Pf[2 * (R * pitch + (n - 1 - C) + 1 + kPadC) + 1] = val;
   }
@@ -473,6 +483,8 @@ k_stage32(const float* __restrict__ x, int side, int lg, CompParams cp, float2* 
     const int cc = e / w, rr = e % w;  // consecutive threads along a column of u
     const int R = R0 + rr, C = C0 + cc;
     const float val = ut[rr][cc];
+    IMASK_CHECK_RANGE(62, C * pitch + R + 1 + kPadC, (long long)n * pitch);
+    IMASK_CHECK_RANGE(63, (n - 1 - C) * pitch + R + 1 + kPadC, (long long)n * pitch);
     PTf[2 * (C * pitch + R + 1 + kPadC)] = val;
     PTf[2 * ((n - 1 - C) * pitch + R + 1 + kPadC) + 1] = val;
   }
@@ -505,10 +517,14 @@ k_saga_image_coarse(const float* __restrict__ bp, int side, int f, int ts, float
                     ImageSaga sg) {
   const int n = side / f;
   const int x0 = blockIdx.x * ts, y0 = blockIdx.y * ts;
+  IMASK_CHECK_RANGE(56, (long long)(gridDim.x * ts) - side, 1);  // the tiles cover the image exactly
+  IMASK_CHECK_RANGE(57, ts % f, 1);                              // and hold whole f x f blocks
   for (int e = threadIdx.x; e < ts * ts; e += blockDim.x) {
     const int row = y0 + e / ts, col = x0 + e % ts;
     const int q = (row / f) * n + col / f;
     const size_t p = (size_t)row * side + col;
+    IMASK_CHECK_RANGE(58, q, (long long)n * n);
+    IMASK_CHECK_RANGE(59, p, (long long)side * side);
     const float pn = __ldg(bp + q) * inv_f2;
     const float d = pn - sg.phi_tab[q];
     const float ps = sg.phi_sum[p];
@@ -534,8 +550,12 @@ k_saga_image_full(const float* __restrict__ bp, int side, CompParams cp, ImageSa
   __shared__ float pyr[TT * TT / 3 + 8];
   const int ts = side / (int)gridDim.x;  // the launcher's tile (cover_tile): divides side, <= TT
   const int x0 = blockIdx.x * ts, y0 = blockIdx.y * ts;
-  for (int e = threadIdx.x; e < ts * ts; e += blockDim.x)
+  IMASK_CHECK_RANGE(53, (long long)(gridDim.x * ts) - side, 1);
+  IMASK_CHECK_RANGE(54, ts, TT + 1);
+  for (int e = threadIdx.x; e < ts * ts; e += blockDim.x) {
+    IMASK_CHECK_RANGE(55, (size_t)(y0 + e / ts) * side + x0 + e % ts, (long long)side * side);
     tile[e] = __ldg(bp + (size_t)(y0 + e / ts) * side + x0 + e % ts);
+  }
   __syncthreads();
   build_pyramid(tile, pyr, ts, cp.r);
   for (int e = threadIdx.x; e < ts * ts; e += blockDim.x) {
@@ -714,6 +734,10 @@ cudaError_t launch_compensate(const float* x, float* out, int side, const CompPa
   else
     k_compensate<64><<<grid, 256, 0, s>>>(x, out, side, cp);
   return cudaGetLastError();
+}
+
+bool debug_bounds_read_sketch(unsigned long long* out4, bool reset) {
+  return bounds_read(out4, reset);
 }
 
 bool stage32_ok(int side, int f, int r) { return side % 32 == 0 && f <= 32 && r <= 6; }

@@ -32,4 +32,14 @@ out = (ctypes.c_ulonglong * 4)()
 rc = _lib.lib().imask_debug_bounds(out, 0)
 print(f"[bounds check] configs D and E, every level, whole set and two 1/8 shards: compiled in {rc}, violations {out[0]} (site {out[1]}, index {ctypes.c_longlong(out[2]).value}, limit {out[3]})")
 P
+# the geometries off the BASELINE grid (any-size sketch / image-side kernels), in one process
+python - >> gpurun_out/pytest_bounds.log 2>&1 <<'P'
+import ctypes, os, runpy, sys
+sys.path.insert(0, os.getcwd())
+runpy.run_path("tools/geometry_sweep.py", run_name="__main__")
+from paper_2412_10249_b200 import _lib
+out = (ctypes.c_ulonglong * 4)()
+rc = _lib.lib().imask_debug_bounds(out, 0)
+print(f"[bounds check] tools/geometry_sweep.py: compiled in {rc}, violations {out[0]} (site {out[1]}, index {ctypes.c_longlong(out[2]).value}, limit {out[3]})")
+P
 cp /tmp/lib_default.so $L
