@@ -1,7 +1,8 @@
 """Sweep of unusual geometries (image sides that are not multiples of 32, odd /
 non-quad angle counts, even and odd detector counts, every level count the side
 allows): projections at every level and 12 solver iterations against the
-float64 oracle, and a repeated solve bit for bit. One-off hardening check."""
+float64 oracle (memory sums re-formed every 5 iterations), and a repeated
+solve bit for bit. One-off hardening check."""
 import itertools
 import os
 import sys
@@ -46,12 +47,12 @@ for side, na, nd, r in cases:
                               coarse_projector=lambda f: ctmodel.coarse_projector(geom, f))
     runs = []
     for _ in range(2):
-        st = solvers.init_state(pr, seed=9)
+        st = solvers.init_state(pr, seed=9, resum_every=5)
         for _ in range(12):
             solvers.sketch_step(st, pr, 1e-4, 1e-2)
         runs.append((st.x.clone(), st.y.clone()))
     same = torch.equal(runs[0][0], runs[1][0]) and torch.equal(runs[0][1], runs[1][1])
-    ost = so.init_state(ops, seed=9)
+    ost = so.init_state(ops, seed=9, resum_every=5)
     for _ in range(12):
         so.sketch_step(ost, ops, b, 1e-4, 1e-2, 1e-2)
     ex = rel(runs[0][0].double().cpu().numpy(), ost.x)
