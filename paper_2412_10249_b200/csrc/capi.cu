@@ -68,7 +68,8 @@ cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float
                                const float2* PM, const float2* PTM, int n, const FwdAngle* ang,
                                const int4* entries, int n_entries, int row_ctas, bool quad,
                                int n_det, float* sino, const SinoSaga* saga, cudaStream_t stream,
-                               bool two_det);
+                               bool two_det, const int* tab_in, int* tab_out);
+size_t forward_tma_table_len(int n, int n_det, int n_entries, bool quad, bool two_det);
 }  // namespace imask
 
 struct imask_graph {
@@ -85,7 +86,7 @@ const char* const kKnobNames[(int)Knob::kCount] = {
     "IMASK_TMA_MIN_N", "IMASK_ADJ_AFTER_STAGE_MIN_N", "IMASK_SAGA_SPLIT_MIN_N",
     "IMASK_ADJ_WIN_KB", "IMASK_ADJ_CLUSTER", "IMASK_ADJ_TILE", "IMASK_ADJ_CTAS",
     "IMASK_FWD_TWO_DET", "IMASK_FUSED_STAGE", "IMASK_FWD_TWO_DET_MIN_WAVES",
-    "IMASK_ADJ_ROW_PAIR", "IMASK_FWD_TWO_DET_MIN_N"};
+    "IMASK_ADJ_ROW_PAIR", "IMASK_FWD_TWO_DET_MIN_N", "IMASK_FWD_TABLES"};
 
 std::string g_knob_vals[(int)Knob::kCount];
 bool g_knob_set[(int)Knob::kCount];
@@ -147,6 +148,7 @@ struct LevelTables {
   bool two_det = false;     // every TMA entry's detectors are < 1 column apart (and ascend):
                             // the two-detectors-per-thread forward applies
   TmaMaps maps{};           // boxes of 96 x 16 (pair mode) or 96 x 8 bands (quad mode)
+  int* fwd_tab = nullptr;   // device: per-CTA chunk tables of the TMA forward (geometry only)
 };
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
@@ -372,6 +374,20 @@ int get_tables(imask_plan* pl, int f, LevelTables** out) {
               encode_pair_map(&t.maps.row_m, pl->PM, n, bh) &&
               encode_pair_map(&t.maps.col, pl->PT, n, bh) &&
               encode_pair_map(&t.maps.col_m, pl->PTM, n, bh);
+      if (t.tma && pl->tma_entries && pl->n_loc > 0 && n >= knob(Knob::kTmaMinN, 128)) {
+        // the CTAs' chunk tables, built once by the kernel itself (tab_out)
+        const size_t len = forward_tma_table_len(n, pl->n_det, pl->n_tma_entries, pl->tma_quad,
+                                                 t.two_det);
+        int rc = cuda_check(cudaMalloc(&t.fwd_tab, sizeof(int) * len), "cudaMalloc fwd_tab");
+        if (rc) return rc;
+        rc = cuda_check(launch_forward_tma(t.maps, pl->P, pl->PT, pl->PM, pl->PTM, n, t.fwd,
+                                           pl->tma_entries, pl->n_tma_entries, pl->tma_row_ctas,
+                                           pl->tma_quad, pl->n_det, pl->sino_tmp, nullptr, nullptr,
+                                           t.two_det, nullptr, t.fwd_tab),
+                        "forward tables");
+        if (!rc) rc = cuda_check(cudaDeviceSynchronize(), "forward tables");
+        if (rc) return rc;
+      }
     }
     it = pl->tables.emplace(f, t).first;
   }
@@ -462,7 +478,8 @@ int run_forward(imask_plan* pl, int f, const LevelTables* t, float* sino, const 
   if (forward_uses_tma(pl, t, n))
     e = launch_forward_tma(t->maps, pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->tma_entries,
                            pl->n_tma_entries, pl->tma_row_ctas, pl->tma_quad, pl->n_det, sino,
-                           saga, s, t->two_det);
+                           saga, s, t->two_det, knob(Knob::kFwdTables, 1) ? t->fwd_tab : nullptr,
+                           nullptr);
   else {
     const bool quad = forward_quad_l1(pl);
     e = launch_forward(pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->n_loc, pl->n_det,
@@ -840,6 +857,7 @@ int imask_plan_destroy(imask_plan* pl) {
   for (auto& kv : pl->tables) {
     cudaFree(kv.second.fwd);
     cudaFree(kv.second.adj);
+    cudaFree(kv.second.fwd_tab);
   }
   cudaFree(pl->P);
   cudaFree(pl->PT);

@@ -123,6 +123,7 @@ enum class Knob {
   kFwdTwoDetMinWaves,  // IMASK_FWD_TWO_DET_MIN_WAVES: two-detector grids need >= this x SMs CTAs
   kAdjRowPair,       // IMASK_ADJ_ROW_PAIR (0/1): the f=1 symmetric adjoint on row pairs (off)
   kFwdTwoDetMinN,    // IMASK_FWD_TWO_DET_MIN_N: smallest coarse side with two detectors per thread (512)
+  kFwdTables,        // IMASK_FWD_TABLES (0/1): TMA forward reads its CTAs' prebuilt chunk tables (1)
   kCount
 };
 // Integer value of a switch, or `dflt` when unset (a set-but-valueless flag

@@ -436,7 +436,8 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
               const float2* __restrict__ PT, const float2* __restrict__ PM,
               const float2* __restrict__ PTM, int n, int pitch, const FwdAngle* __restrict__ ang,
               const int4* __restrict__ entries, int n_entries, int row_ctas, int n_det,
-              float* __restrict__ sino, SinoSaga saga, int nch_cap) {
+              float* __restrict__ sino, SinoSaga saga, int nch_cap, const int* __restrict__ tab_in,
+              int* __restrict__ tab_out) {
   constexpr int FB = kQuad ? (kVal ? kFBQuadVal : kFBQuad) : kFB;  // bands per chunk
   // staged images per chunk: kVal stages only the value planes (P, and PT in
   // quad mode) and forms the difference pair of column c as P[c+1] - P[c], the
@@ -506,6 +507,20 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
   // union of the lockstep band ranges of the four warps holding it (every lane
   // walks its warp's whole range)
   int* cmax_tab = ctl + 4;  // [nch_cap]
+  // The chunk tables of a CTA (overflow flag, first band, chunk count, window
+  // origin per chunk) depend on the geometry only: they are built once per
+  // plan and level by a launch of this kernel with tab_out set (which stops
+  // after writing them) and read back here -- the atomics and five of the
+  // seven barriers of the prologue go (ncu: the prologue was 10% of the
+  // instructions but 27% of the stall samples of the f=8 forward).
+  const int tab_stride = nch_cap + 3;
+  const size_t cta = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+  if (tab_in) {
+    const int* row = tab_in + cta * tab_stride;
+    if (threadIdx.x < 3) ctl[threadIdx.x] = row[threadIdx.x];
+    const int nrow = min(row[2], nch_cap);
+    for (int t = threadIdx.x; t < nrow; t += blockDim.x) cmin_tab[t] = row[3 + t];
+  } else {
   if (threadIdx.x < kFE) {
     info[threadIdx.x] = FwdWarpInfo{0, 0, 0, n, 0};
     ctl[0] = 0;
@@ -535,6 +550,7 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
     if (ctl[2] > nch_cap) ctl[0] = 1;
   }
   __syncthreads();
+  {
   const int blo = ctl[1], nch = ctl[2];
   // window (first pair column) of every chunk: extremes of the affine positions,
   // one (chunk, entry slot) item per thread
@@ -566,7 +582,17 @@ k_forward_tma(const __grid_constant__ TmaMaps maps, const float2* __restrict__ P
       cmin_tab[t] = corig;
     }
   }
+  }
+  }  // !tab_in
   __syncthreads();
+  const int blo = ctl[1], nch = ctl[2];
+  if (tab_out) {
+    int* row = tab_out + cta * tab_stride;
+    if (threadIdx.x < 3) row[threadIdx.x] = ctl[threadIdx.x];
+    const int nrow = min(ctl[2], nch_cap);
+    for (int t = threadIdx.x; t < nrow; t += blockDim.x) row[3 + t] = cmin_tab[t];
+    return;
+  }
   // everything above reads only tables and the solver state; the pair images
   // come from the stream predecessor (k_prepare)
   griddep_wait();
@@ -810,6 +836,16 @@ static int forward_tma_chunk_cap(int n, bool quad, bool val) {
   return cap < kFMaxChunks ? cap : kFMaxChunks;
 }
 
+// ints of the per-CTA chunk tables of a level's TMA forward (build: a launch
+// of the kernel with tab_out)
+bool forward_tma_val(int ctas);
+size_t forward_tma_table_len(int n, int n_det, int n_entries, bool quad, bool two_det) {
+  const int kk = two_det ? 2 : 1;
+  const size_t ctas = (size_t)((n_det + 32 * kk - 1) / (32 * kk)) * ((n_entries + kFE - 1) / kFE);
+  const bool val = two_det || forward_tma_val(0);
+  return ctas * (size_t)(forward_tma_chunk_cap(n, quad, val) + 3);
+}
+
 size_t forward_tma_smem(bool val, bool quad, int nch_cap) {
   // two stages of (1 or 2) x (quad: 2) images of FB bands x kFWc pairs
   const size_t ni = (quad ? 2 : 1) * (val ? 1 : 2);
@@ -853,7 +889,7 @@ cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float
                                const float2* PM, const float2* PTM, int n, const FwdAngle* ang,
                                const int4* entries, int n_entries, int row_ctas, bool quad,
                                int n_det, float* sino, const SinoSaga* saga, cudaStream_t stream,
-                               bool two_det) {
+                               bool two_det, const int* tab_in, int* tab_out) {
   const int kk = two_det ? 2 : 1;
   dim3 grid((n_det + 32 * kk - 1) / (32 * kk), (n_entries + kFE - 1) / kFE);
   const bool val = two_det || forward_tma_val((int)(grid.x * grid.y));
@@ -864,7 +900,8 @@ cudaError_t launch_forward_tma(const TmaMaps& maps, const float2* P, const float
   float* out = saga ? nullptr : sino;
 #define FWD_TMA(S_, Q_, V_, K_)                                                                  \
   launch_pdl(k_forward_tma<S_, Q_, V_, K_>, grid, dim3(kFThreads), smem, stream, maps, P, PT, PM, \
-             PTM, n, pair_pitch(n), ang, entries, n_entries, row_ctas, n_det, out, sg, cap)
+             PTM, n, pair_pitch(n), ang, entries, n_entries, row_ctas, n_det, out, sg, cap, tab_in, \
+             tab_out)
 #define FWD_TMA_V(S_, Q_)                                 \
   if (two_det) FWD_TMA(S_, Q_, true, 2);                  \
   else if (val) FWD_TMA(S_, Q_, true, 1);                 \
