@@ -149,6 +149,7 @@ struct LevelTables {
                             // the two-detectors-per-thread forward applies
   TmaMaps maps{};           // boxes of 96 x 16 (pair mode) or 96 x 8 bands (quad mode)
   int* fwd_tab = nullptr;   // device: per-CTA chunk tables of the TMA forward (geometry only)
+  bool fwd_tab_val = false;  // the staging mode (value planes) they were built for
 };
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
@@ -387,6 +388,7 @@ int get_tables(imask_plan* pl, int f, LevelTables** out) {
                         "forward tables");
         if (!rc) rc = cuda_check(cudaDeviceSynchronize(), "forward tables");
         if (rc) return rc;
+        t.fwd_tab_val = val;
       }
     }
     it = pl->tables.emplace(f, t).first;
@@ -463,6 +465,15 @@ bool forward_reads_diff(const imask_plan* pl, const LevelTables* t, int n) {
   return true;  // k_forward_sym
 }
 
+// The prebuilt chunk tables, when they match the kernel this launch picks (the
+// path switches can be re-read after the plan was built: chunk sizes differ
+// between the value-plane and the two-plane kernels).
+const int* forward_tables(const imask_plan* pl, const LevelTables* t) {
+  if (!t->fwd_tab || !knob(Knob::kFwdTables, 1)) return nullptr;
+  const bool val = t->two_det || forward_tma_val_grid(pl->n_det, pl->n_tma_entries);
+  return val == t->fwd_tab_val ? t->fwd_tab : nullptr;
+}
+
 int prepare_for_forward(imask_plan* pl, const LevelTables* t, const float* u, int n,
                         cudaStream_t s) {
   LAUNCH(launch_prepare(u, n, pl->P, pl->PT, pl->PM, pl->PTM, forward_reads_diff(pl, t, n), s),
@@ -478,8 +489,7 @@ int run_forward(imask_plan* pl, int f, const LevelTables* t, float* sino, const 
   if (forward_uses_tma(pl, t, n))
     e = launch_forward_tma(t->maps, pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->tma_entries,
                            pl->n_tma_entries, pl->tma_row_ctas, pl->tma_quad, pl->n_det, sino,
-                           saga, s, t->two_det, knob(Knob::kFwdTables, 1) ? t->fwd_tab : nullptr,
-                           nullptr);
+                           saga, s, t->two_det, forward_tables(pl, t), nullptr);
   else {
     const bool quad = forward_quad_l1(pl);
     e = launch_forward(pl->P, pl->PT, pl->PM, pl->PTM, n, t->fwd, pl->n_loc, pl->n_det,
