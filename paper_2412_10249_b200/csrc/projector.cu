@@ -1012,6 +1012,12 @@ __device__ __forceinline__ float angle0_value(const float* __restrict__ sino, co
   return v;
 }
 
+#ifndef IMASK_ADJ_STAGE_NB
+#define IMASK_ADJ_STAGE_NB 2
+#endif
+#ifndef IMASK_ADJ_PAIR_MINB
+#define IMASK_ADJ_PAIR_MINB 7  // factor 1: 72 registers with two angles staged per round
+#endif
 #ifndef IMASK_ADJ_SYM_MINB
 #define IMASK_ADJ_SYM_MINB 8  // 64 registers: f=1 adjoint 514.7 -> 512.4 us, f=8 80.3 -> 78.4 us, every step -0.2..-1% (A/B, two rounds)
 #endif
@@ -1034,7 +1040,7 @@ __device__ __forceinline__ void adj_pix(int p, int k, int& dx, int& dy) {
 }
 
 template <bool kPair, int T, bool kSym, int kPPT, bool kRP = false>
-__global__ void __launch_bounds__(kAdjThreads, kSym ? IMASK_ADJ_SYM_MINB : 8)
+__global__ void __launch_bounds__(kAdjThreads, kSym ? (kPair ? IMASK_ADJ_PAIR_MINB : IMASK_ADJ_SYM_MINB) : 8)
 k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W, int CA,
           int a_begin, int a_per_split, int a_end, int n_mirror, int n_det,
           const AdjAngle* __restrict__ ang, int add_a0) {
@@ -1099,36 +1105,103 @@ k_adjoint(const float* __restrict__ sino, float* __restrict__ out, int n, int W,
     }
     __syncthreads();
     // stage windows (one warp per angle): W bins scaled by wsc, zero outside the detector
+    constexpr int kNL = (kPair && !kRP ? 2 : 1) * (kSym ? 2 : 1);  // global loads per window element
+    auto interior = [&](int t) { return st[t].jb >= 0 && st[t].jb + W + 1 <= n_det; };
+    // one element of an interior window: its loads (l), then the scaled element
+    auto load_elem = [&](const float* yp, const float* mp, unsigned k, float (&l)[kNL]) {
+      l[0] = __ldg(yp + k);
+      if constexpr (kRP) {
+        l[1] = __ldg(mp + k);
+      } else if constexpr (kPair && kSym) {
+        l[1] = __ldg(yp + k + 1);
+        l[2] = __ldg(mp + k);
+        l[3] = __ldg(mp + k + 1);
+      } else if constexpr (kPair) {
+        l[1] = __ldg(yp + k + 1);
+      } else if constexpr (kSym) {
+        l[1] = __ldg(mp + k);
+      }
+    };
+    auto store_elem = [&](WinT* wt, unsigned k, const float (&l)[kNL], float wsc) {
+      if constexpr (kNL == 4) {
+        wt[k] = make_float4(l[0] * wsc, l[1] * wsc, l[2] * wsc, l[3] * wsc);
+      } else if constexpr (kNL == 2) {
+        wt[k] = make_float2(l[0] * wsc, l[1] * wsc);
+      } else {
+        wt[k] = l[0] * wsc;
+      }
+    };
     for (int t = warp; t < na; t += kAdjThreads / 32) {
       const int jb = st[t].jb;
       const float wsc = st[t].wsc;
       const float* yrow = sino + (size_t)(a0 + t) * n_det;
       const float* mrow = sino + (size_t)(kSym ? n_mirror - (a0 + t) : 0) * n_det;
-      if (jb >= 0 && jb + W + 1 <= n_det) {
-        // window inside the detector (almost every tile and angle): no edge
-        // tests, 32-bit offsets from two per-angle pointers (the tested loop
-        // below spends ~35 instructions per 32 bins, mostly on predicates and
-        // 64-bit addresses; at f >= 8 staging was a quarter to two fifths of
-        // the kernel's instructions)
-        const float* yp = yrow + jb;
-        const float* mp = mrow + jb;
-        WinT* wt = win + t * W;
+      if constexpr (!kPair) {
+        if (interior(t)) {
+          // window inside the detector (almost every tile and angle): no edge
+          // tests, 32-bit offsets from two per-angle pointers (the tested loop
+          // below spends ~35 instructions per 32 bins, mostly on predicates and
+          // 64-bit addresses)
+          const float* yp = yrow + jb;
+          const float* mp = mrow + jb;
+          WinT* wt = win + t * W;
 #pragma unroll 4
-        for (unsigned k = lane; k < (unsigned)W; k += 32) {
-          const float v0 = __ldg(yp + k) * wsc;
-          if constexpr (kRP) {
-            wt[k] = make_float2(v0, __ldg(mp + k) * wsc);
-          } else if constexpr (kPair && kSym) {
-            wt[k] = make_float4(v0, __ldg(yp + k + 1) * wsc, __ldg(mp + k) * wsc,
-                                __ldg(mp + k + 1) * wsc);
-          } else if constexpr (kPair) {
-            wt[k] = make_float2(v0, __ldg(yp + k + 1) * wsc);
-          } else if constexpr (kSym) {
-            wt[k] = make_float2(v0, __ldg(mp + k) * wsc);
-          } else {
-            wt[k] = v0;
+          for (unsigned k = lane; k < (unsigned)W; k += 32) {
+            const float v0 = __ldg(yp + k) * wsc;
+            if constexpr (kSym) {
+              wt[k] = make_float2(v0, __ldg(mp + k) * wsc);
+            } else {
+              wt[k] = v0;
+            }
           }
+          continue;
         }
+      } else if (interior(t)) {
+        // window inside the detector (almost every tile and angle): no edge
+        // tests, 32-bit offsets from two per-angle pointers. Two angles of this
+        // warp go together, two lane-chunks of each per round: up to 4 kNL
+        // independent loads are in flight before the first is used (ncu's
+        // source page of the f=1 kernel: the multiplies waiting on these loads
+        // held 11% of all stall samples, staging 30% with 12% of the
+        // instructions).
+        // (factor-1 kernel only, at 72 registers: f=1 adjoint 513 -> 505 us; the
+        // coarse kernels got slower with it -- f=4 115 -> 118 us, f=16 54 -> 62 us --
+        // and keep one angle and one lane-chunk per round)
+        // kNB consecutive angles of this warp (t, t + 4, ...) go together while
+        // they are interior
+        constexpr int kNB = IMASK_ADJ_STAGE_NB;
+        constexpr int kStep = kAdjThreads / 32;
+        int nbat = 1;
+        while (nbat < kNB && t + nbat * kStep < na && interior(t + nbat * kStep)) ++nbat;
+        const float* ypb[kNB];
+        const float* mpb[kNB];
+        float wscb[kNB];
+#pragma unroll
+        for (int q = 0; q < kNB; ++q) {
+          const int tq = t + (q < nbat ? q : 0) * kStep;
+          const int jq = st[tq].jb;
+          ypb[q] = sino + (size_t)(a0 + tq) * n_det + jq;
+          mpb[q] = sino + (size_t)(kSym ? n_mirror - (a0 + tq) : 0) * n_det + jq;
+          wscb[q] = st[tq].wsc;
+        }
+        for (unsigned k = lane; k < (unsigned)W; k += 64) {
+          float la[kNB][kNL], lb[kNB][kNL];
+          const bool more = k + 32 < (unsigned)W;
+#pragma unroll
+          for (int q = 0; q < kNB; ++q)
+            if (q < nbat) {
+              load_elem(ypb[q], mpb[q], k, la[q]);
+              if (more) load_elem(ypb[q], mpb[q], k + 32, lb[q]);
+            }
+#pragma unroll
+          for (int q = 0; q < kNB; ++q)
+            if (q < nbat) {
+              WinT* wq = win + (t + q * kStep) * W;
+              store_elem(wq, k, la[q], wscb[q]);
+              if (more) store_elem(wq, k + 32, lb[q], wscb[q]);
+            }
+        }
+        t += (nbat - 1) * kStep;  // those angles are done
         continue;
       }
       for (int k = lane; k < W; k += 32) {
