@@ -47,11 +47,20 @@ __device__ __forceinline__ void band_range(long long X0, long long step, double 
     const double elo = fmax(fmin(e1, e2), -1.0), ehi = fmin(fmax(e1, e2), (double)n + 1.0);
     lo = min(max((int)ceil(elo), 0), n);
     hi = min(max((int)ceil(ehi), lo), n);
+    // the bands of a ray are one interval and the estimate is within a band of
+    // it, so the first band is searched no further than the estimated end + 1
+    // (a ray that has left the image before band 0 used to walk all n bands
+    // here: half the instructions of a prologue-only launch at n = 1024)
+    const int guard = hi + 1;
     while (lo > 0 && band_ok(X0, step, lo - 1, n)) --lo;
-    while (lo < n && !band_ok(X0, step, lo, n)) ++lo;
-    if (hi < lo) hi = lo;
-    while (hi < n && band_ok(X0, step, hi, n)) ++hi;
-    while (hi > lo && !band_ok(X0, step, hi - 1, n)) --hi;
+    while (lo < n && lo <= guard && !band_ok(X0, step, lo, n)) ++lo;
+    if (lo >= n || lo > guard) {
+      lo = hi = 0;  // no band
+    } else {
+      if (hi < lo) hi = lo;
+      while (hi < n && band_ok(X0, step, hi, n)) ++hi;
+      while (hi > lo && !band_ok(X0, step, hi - 1, n)) --hi;
+    }
   }
   *lo_out = lo;
   *hi_out = hi;
