@@ -96,8 +96,8 @@ def test_double_buffered_dual_matches_in_place(graphs):
         assert np.array_equal(host(a), host(c))
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_phases_match_single_gpu(world):
+@pytest.mark.parametrize("world,key", [(2, None), (3, None), (8, "D")])
+def test_sharded_phases_match_single_gpu(world, key):
     """The multi-GPU step emulated in one process: every rank's
     mirror-closed shard runs step_adjoint on its own plan, the partial coarse
     backprojections are summed (the NCCL all-reduce), then step_forward and
@@ -107,11 +107,19 @@ def test_sharded_phases_match_single_gpu(world):
     from paper_2412_10249_b200 import _lib
     from paper_2412_10249_b200 import dist as dist_mod
 
-    side, na, nd, probs, mu_g = 64, 90, 91, [0.3, 0.3, 0.2, 0.2], 1e-2
+    if key is None:
+        side, na, nd, probs, mu_g = 64, 90, 91, [0.3, 0.3, 0.2, 0.2], 1e-2
+        orc = so.SketchedCT(side, na, nd, probs)
+        b = orc.proj[1].apply(np.random.default_rng(6).random(side * side))
+    else:
+        # the benchmarked configuration on 8 ranks: block-cyclic quad shards, the TMA
+        # kernels and fused staging on every shard
+        cfg = CONFIGS[key]
+        side, na, nd, mu_g = cfg.side, cfg.n_angles, cfg.n_det, cfg.mu_g
+        probs = [1.0 / cfg.levels] * cfg.levels
+        b = np.random.default_rng(6).random(na * nd) * side
     geom = ctmodel.Geometry(side, na, nd)
-    orc = so.SketchedCT(side, na, nd, probs)
-    b = orc.proj[1].apply(np.random.default_rng(6).random(side * side))
-    fam = mrsketch.make_family(4, side, probs, mode="coarse")
+    fam = mrsketch.make_family(len(probs), side, probs, mode="coarse")
     single = dist_mod.make_sharded_problem(geom, b, fam, mu_g)
     st1 = solvers.init_state(single, seed=2)
     ranks = []
@@ -122,7 +130,8 @@ def test_sharded_phases_match_single_gpu(world):
         ranks.append((pr, solvers.init_state(pr, seed=2)))
     prm = solvers._params(2e-4, 1e-2, mu_g)
     L = _lib.lib()
-    sched = solvers.draw_levels(2, 0, 10, single.cum_probs)
+    sched = (solvers.draw_levels(2, 0, 10, single.cum_probs) if key is None
+             else list(range(len(probs))) * 2)
     for lv in (int(v) for v in sched):
         solvers._device_step(single.engine, st1, lv, prm)
         n = (side // single.engine.plan.factors[lv]) ** 2
